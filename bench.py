@@ -1,0 +1,290 @@
+#!/usr/bin/env python3
+"""Benchmark: C_LP_S (ByteGrad / MinMaxUInt8) allreduce of a 100M-element fp32
+gradient bucket per GPU -- BASELINE.json's metric "effective gradient GB/s for
+C_LP_S allreduce at 1/2/4/8 B200 vs roofline".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...           (N > 1)
+
+A step is one c_lp_s call over the rank's resident 100M-element bucket (one
+fused cooperative kernel launch per step).  Inputs are deterministic synthetic
+gradients (splitmix64 hash, seed 2026 + rank) of 400 MB per GPU -- larger
+than the 126 MB L2, so no flush is needed between steps.  Each step consumes
+the previous step's output (always finite, the codec range never degenerates).
+
+value     = whole-job effective gradient GB/s = N_gpus * 4 * elements / t_step
+            (the per-GPU figure, BASELINE.md's definition 4N/wall, is
+            config.per_gpu_gbs)
+e2e       = same metric through the reference-facing API with HOST buffers:
+            pinned H2D copy of the bucket, c_lp_s, D2H copy of the result, per step
+roofline  = algorithmic bytes of the dominant (only) kernel / its event time,
+            against MEASURED_PEAKS.json HBM copy bandwidth (g <= 4) or the
+            measured 770 GB/s NVLink peer bandwidth (g = 8) -- see DESIGN.md 5
+cpu_baseline = the unmodified reference (oracle/_ref) C_LP_S on this host's
+            cores, one thread per worker, on a bounded sample (rank 0, N=1)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+N_ELEMS = 100_000_000
+HBM_FALLBACK_GBS = 6650.0
+NVL_PEER_GBS = 770.0   # measured peer copy, B200_PROFILING.md
+NVL_NOMINAL_GBS = 900.0
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+def algorithmic_bytes(n: int, g: int):
+    """HBM bytes 11N + N/g, NVLink ingress 2N(g-1)/g per GPU."""
+    return 11 * n + n // g, 2 * n * (g - 1) // g
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                return
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_reference_gbs(g: int, n_sample: int, reps: int):
+    """The unmodified reference (oracle/_ref) C_LP_S through its SimCluster harness."""
+    from oracle import Reference  # test/baseline infrastructure only
+    r = Reference()
+    secs = r.time_primitive(2, g, n_sample, reps)
+    return secs, r.backend()
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    g = world
+    n_sample = min(args.n, args.ref_sample)
+    secs, backend = cpu_reference_gbs(g, n_sample, args.warmup + args.steps)
+    timed = secs[args.warmup:] or secs
+    t = statistics.median(timed)
+    value = g * 4 * n_sample / t / 1e9
+    line = {
+        "metric": "effective gradient GB/s for C_LP_S allreduce", "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+u8", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"C_LP_S uint8 (no EC) allreduce, {n_sample} fp32 elements per worker (bounded "
+                               f"sample of the {args.n}-element bucket), {g} worker threads on SimCluster",
+                   "elements": n_sample, "workers": g},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": g, "kind": "reference",
+                         "sample": f"{n_sample} elements x {g} workers, median of {len(timed)} calls, "
+                                   f"kernels backend {backend}"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, rank: int, world: int):
+    import torch
+    import torch.distributed as dist
+    import paper_2107_01499_b200 as b2
+
+    dev = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(dev)
+    g = world
+    n = args.n
+    ep = b2.B200Endpoint(rank, world, dev)
+    codec = b2.Codec(b2.CodecKind.uniform8)
+    stream = torch.cuda.current_stream()
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    b2._lib.check(b2.lib.b2_fill_synthetic(x.data_ptr(), n, 2026 + rank, 0, stream.cuda_stream))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------- device-resident timing (value)
+    for _ in range(args.warmup):
+        b2.c_lp_s(ep, 0.0, x, codec, None, blocking=False)
+    ep.sync()
+    launches0 = ep.launches()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            b2.c_lp_s(ep, 0.0, x, codec, None, blocking=False)
+        ev1.record(stream)
+        ev1.synchronize()
+    ep.sync()
+    launches = ep.launches() - launches0
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    ms = ms_local
+    if world > 1:
+        t = torch.tensor([ms_local], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    barrier()
+
+    # ---------------- end to end through the public API with host buffers
+    host = torch.empty(n, dtype=torch.float32).pin_memory()
+    host.copy_(x.cpu())
+    xd = torch.empty_like(x)
+    for _ in range(max(1, args.warmup // 2)):
+        xd.copy_(host, non_blocking=True)
+        b2.c_lp_s(ep, 0.0, xd, codec, None, blocking=False)
+        host.copy_(xd, non_blocking=True)
+    ep.sync()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_steps = max(1, min(args.steps, args.e2e_steps))
+    e0.record(stream)
+    for _ in range(e_steps):
+        xd.copy_(host, non_blocking=True)
+        b2.c_lp_s(ep, 0.0, xd, codec, None, blocking=False)
+        host.copy_(xd, non_blocking=True)
+    e1.record(stream)
+    e1.synchronize()
+    ep.sync()
+    ems = e0.elapsed_time(e1) / e_steps
+    if world > 1:
+        t = torch.tensor([ems], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+
+    hbm_peak, peak_kind = measured_peaks()
+    hbm_b, nvl_b = algorithmic_bytes(n, g)
+    t_s = ms / 1e3
+    t_roof_hbm = hbm_b / (hbm_peak * 1e9)
+    t_roof_nvl = nvl_b / (NVL_PEER_GBS * 1e9)
+    if t_roof_nvl > t_roof_hbm:
+        roof = {"bound": "nvlink", "achieved": round(nvl_b / t_s / 1e9, 2), "peak": NVL_PEER_GBS,
+                "unit": "GB/s", "peak_kind": "measured peer copy (B200_PROFILING.md); nominal 900"}
+    else:
+        roof = {"bound": "hbm", "achieved": round(hbm_b / t_s / 1e9, 2), "peak": hbm_peak, "unit": "GB/s",
+                "peak_kind": f"{peak_kind} HBM copy (MEASURED_PEAKS.json)"}
+    roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    roof["traffic"] = args.traffic
+    roof["algorithmic_bytes"] = {"hbm": hbm_b, "nvlink_ingress": nvl_b}
+    roof["t_roof_us"] = round(max(t_roof_hbm, t_roof_nvl) * 1e6, 1)
+    roof["kernel"] = "central_kernel<uint8> (one fused launch per step)"
+
+    per_gpu = 4 * n / t_s / 1e9
+    line = {
+        "metric": "effective gradient GB/s for C_LP_S allreduce", "value": round(g * per_gpu, 2), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+u8",
+        "data": "synthetic (splitmix64 uniform [-1,1), seed 2026+rank)",
+        "config": {"workload": f"C_LP_S ByteGrad MinMaxUInt8 allreduce of {n} fp32 gradients per GPU (VGG16-sized), "
+                               f"g={g}", "elements_per_gpu": n, "parallelism": f"dp{g}",
+                   "per_gpu_gbs": round(per_gpu, 2), "l2": "inputs 400 MB/GPU > 126 MB L2, no flush"},
+        "roofline": roof,
+        "e2e": {"value": round(g * 4 * n / (ems / 1e3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
+                "d2h_bytes_per_step": 4 * n, "ms_per_step": round(ems, 3)},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_sample = min(n, args.cpu_sample)
+        secs, backend = cpu_reference_gbs(1, n_sample, 3)
+        tc = statistics.median(secs)
+        line["cpu_baseline"] = {"value": round(4 * n_sample / tc / 1e9, 4), "unit": "GB/s", "cores": 1,
+                                "kind": "reference",
+                                "sample": f"C_LP_S g=1 over {n_sample} elements, median of 3 calls "
+                                          f"(reference SimCluster harness, {backend} kernels)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ep.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=N_ELEMS)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-sample", type=int, default=25_000_000)
+    ap.add_argument("--ref-sample", type=int, default=25_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes/launch from an ncu --set full capture (profiles/)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if args.impl == "b200":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank))))
+        else:
+            dist.init_process_group("gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_b200(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

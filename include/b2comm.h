@@ -1,0 +1,162 @@
+/*
+ * b2comm.h -- C ABI of the B200-native rcomm hot path (libb2comm.so).
+ *
+ * Drop-in boundary for rcomm's communication primitives
+ * (/root/reference/proj/include/rcomm/collectives.hpp:50-87), the uniform8
+ * ("MinMaxUInt8") codec (codec.hpp:13-54) and bucket flattening
+ * (tensor.hpp:56-86).  Every entry point takes plain pointers and sizes; all
+ * float/byte buffers are DEVICE pointers on the communicator's GPU unless
+ * stated otherwise; `stream` is a cudaStream_t (NULL = legacy default stream).
+ *
+ * Semantics are the reference's, bit for bit:
+ * uniform8 codes and chunk min/max are bit-exact, fp64 reductions fold ranks
+ * in ascending order from +0.0 and round once, no FMA anywhere.
+ *
+ * Error model: every function returns a b2_status.  Argument errors are
+ * detected at the call and reported with a message retrievable through
+ * b2_last_error() (thread-local).  Data-dependent errors that the reference
+ * raises synchronously (non-finite encode input, codec.cpp:24-27) are found on
+ * the device; they are latched in the communicator's status word and returned
+ * by b2_comm_sync() (or b2_comm_poll()).  Where the reference would throw
+ * rcomm::Error, the C++ wrapper (include/rcomm_b200/) rethrows.
+ *
+ * Threading / ordering: one host thread (or process) per GPU calls the same
+ * primitive with the same bucket id, like one rcomm worker per Endpoint.
+ * Completion is stream-ordered; calls on one bucket must be stream-ordered on
+ * each rank (the reference's "one collective per tag at a time",
+ * SPEC.md:300).  Peer buffers are library-owned windows exchanged once per
+ * (bucket, primitive family, size) through the caller-supplied allgather.
+ */
+#ifndef B2COMM_H
+#define B2COMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define B2COMM_VERSION 1
+#define B2_MAX_RANKS 8
+/* hdr buffers for the standalone codec hold [min f32][max f32][2 x u32 scratch] */
+#define B2_U8_HDR_BYTES 16
+
+typedef enum {
+  B2_OK = 0,
+  B2_ERR_INVALID = 1,     /* bad argument (size mismatch, null, alignment)   */
+  B2_ERR_CUDA = 2,        /* CUDA runtime failure                            */
+  B2_ERR_NONFINITE = 3,   /* encode saw NaN/Inf  (codec.cpp:26)              */
+  B2_ERR_TIMEOUT = 4,     /* a peer never arrived (rendezvous timeout)       */
+  B2_ERR_UNSUPPORTED = 5, /* e.g. stochastic rounding, onebit codec          */
+  B2_ERR_BOOTSTRAP = 6    /* the allgather callback failed                   */
+} b2_status;
+
+typedef enum { B2_CODEC_IDENTITY = 0, B2_CODEC_UNIFORM8 = 1, B2_CODEC_ONEBIT = 2 } b2_codec_kind;
+typedef enum { B2_REDUCE_SUM = 0, B2_REDUCE_AVERAGE = 1 } b2_reduce_mode;
+typedef enum { B2_TOPO_RING = 0, B2_TOPO_RANDOM = 1, B2_TOPO_FULL = 2 } b2_topology_kind;
+
+typedef struct b2_comm* b2_comm_t;
+
+/* Bootstrap hook: gather `bytes` from every rank into recv (world * bytes,
+ * rank-major).  Called collectively (all ranks, same order) the first time a
+ * (bucket, family, size) window is used.  Return 0 on success. */
+typedef int (*b2_allgather_fn)(void* user, const void* send, size_t bytes, void* recv);
+
+/* ------------------------------------------------------------------ misc */
+int b2_version(void);
+const char* b2_last_error(void);
+const char* b2_status_string(int status);
+
+/* partition_range (collectives.hpp:42-43 / collectives.cpp:167-175) */
+void b2_partition_range(size_t len, int n, int k, size_t* lo, size_t* sz);
+/* owned_partition_len (collectives.hpp:87) */
+size_t b2_owned_partition_len(size_t len, int world, int idx);
+/* Codec::payload_size (codec.hpp:30, codec.cpp:31-38) */
+size_t b2_payload_size(int codec, size_t n);
+/* Topology::neighbors (collectives.hpp:18-25, collectives.cpp:181-213): sorted,
+ * self-inclusive; writes up to n ints into out, returns the count (or -1). */
+int b2_topology_neighbors(int kind, int n, uint64_t seed, int rank, uint64_t round, int* out);
+
+/* ------------------------------------------- uniform8 codec (one GPU)
+ * Codec::encode / decode (codec.hpp:32-35; codec.cpp:40-80, 93-109) split into
+ * SoA device buffers: codes[n] (byte k = level of x[k]) and hdr (>= 16 bytes:
+ * hdr[0] = min, hdr[1] = max as f32).  A non-finite input leaves a non-finite
+ * value in hdr[0] or hdr[1] (NaN propagates) -- the host wrapper turns that
+ * into the reference's Error.  n == 0 writes hdr = (0, 0). */
+int b2_u8_encode(const float* x, size_t n, uint8_t* codes, float* hdr, void* stream);
+int b2_u8_decode(const uint8_t* codes, const float* hdr, size_t n, float* out, void* stream);
+/* compensate_encode (codec.hpp:49-54, codec.cpp:125-137) with uniform8:
+ * y = x - delta; codes,hdr = Q(y); delta = y - D(Q(y)); decoded (nullable) = D(Q(y)) */
+int b2_u8_compensate_encode(const float* x, float* delta, size_t n, uint8_t* codes,
+                            float* hdr, float* decoded, void* stream);
+/* Exact reference wire bytes [min f32 LE][max f32 LE][u8 x n] (codec.hpp:21-24)
+ * into a device buffer of 8 + n bytes, and back. */
+int b2_u8_pack_wire(const uint8_t* codes, const float* hdr, size_t n, uint8_t* wire, void* stream);
+int b2_u8_unpack_wire(const uint8_t* wire, size_t n, uint8_t* codes, float* hdr, void* stream);
+
+/* ----------------------------------------------------- bucket arena
+ * BucketArena::flatten (tensor.hpp:76-81, tensor.cpp:46-68): concatenate
+ * count device tensors (srcs[i], lens[i] floats; pointer/len arrays on the
+ * HOST) into arena in registration order with no gaps, in one launch per 64
+ * members.  Validation (non-empty list, no zero-length member) mirrors the
+ * reference; name uniqueness is checked by the host wrappers.  unflatten
+ * copies the arena back out (the reference aliases instead; the wrappers
+ * return views and use this only when members must stay separate). */
+int b2_bucket_flatten(const float* const* srcs, const size_t* lens, int count, float* arena, void* stream);
+int b2_bucket_unflatten(const float* arena, float* const* dsts, const size_t* lens, int count, void* stream);
+
+/* Synthetic gradient: x[i] = splitmix64-hash(seed, offset+i)
+ * mapped to [-1, 1) with 24-bit resolution; identical to oracle's orc_synth. */
+int b2_fill_synthetic(float* x, size_t n, uint64_t seed, uint64_t offset, void* stream);
+
+/* ---------------------------------------------------- communicator
+ * One per (process or thread, GPU).  world <= B2_MAX_RANKS, all ranks on one
+ * NVLink/NVSwitch node.  allgather is used only to exchange window handles. */
+int b2_comm_create(int world, int rank, int device, b2_allgather_fn allgather, void* user, b2_comm_t* out);
+int b2_comm_destroy(b2_comm_t comm);
+int b2_comm_rank(b2_comm_t comm);
+int b2_comm_world(b2_comm_t comm);
+/* Synchronize `stream` and return (and clear) the latched device status. */
+int b2_comm_sync(b2_comm_t comm, void* stream);
+/* Return (and clear) the latched status without synchronizing. */
+int b2_comm_poll(b2_comm_t comm);
+/* Rendezvous timeout for device-side waits, in milliseconds (default 20000). */
+int b2_comm_set_timeout_ms(b2_comm_t comm, uint64_t ms);
+/* Number of kernel launches this communicator has issued (evidence counter). */
+uint64_t b2_comm_launches(b2_comm_t comm);
+
+/* --------------------------------------------------- the primitives
+ * x: this rank's bucket (device, n floats, 16-byte aligned), updated in place.
+ *
+ * c_fp_s  (collectives.hpp:51-52; scatter_reduce_fp collectives.cpp:42-87):
+ *   every rank ends with (float) sum_j (double) x_j, ranks folded ascending;
+ *   world == 1 leaves x untouched.
+ * c_lp_s  (collectives.hpp:59-61; scatter_reduce_lp collectives.cpp:91-163):
+ *   codec B2_CODEC_UNIFORM8 (ByteGrad) or B2_CODEC_IDENTITY.  delta/eps both
+ *   NULL = stateless; else ErrorState (codec.hpp:40-47): delta has n floats,
+ *   eps has owned_partition_len(n, world, rank) floats, both updated.
+ *   stochastic rounding is not supported (B2_ERR_UNSUPPORTED).
+ * d_fp_s  (collectives.hpp:64-66; collectives.cpp:229-258)
+ * d_lp_s  (collectives.hpp:69-72; collectives.cpp:260-288):
+ *   nbrs = Topology::neighbors(rank, round) (sorted, self-inclusive, HOST
+ *   array); the neighbour relation must be symmetric, as every rcomm
+ *   Topology is.  mode = B2_REDUCE_SUM / B2_REDUCE_AVERAGE. */
+int b2_c_fp_s(b2_comm_t comm, float* x, size_t n, uint32_t bucket, void* stream);
+int b2_c_lp_s(b2_comm_t comm, float* x, size_t n, int codec, float* delta, size_t delta_len,
+              float* eps, size_t eps_len, uint32_t bucket, void* stream);
+int b2_d_fp_s(b2_comm_t comm, float* x, size_t n, const int* nbrs, int n_nbrs, int mode,
+              uint32_t bucket, void* stream);
+int b2_d_lp_s(b2_comm_t comm, float* x, size_t n, const int* nbrs, int n_nbrs, int codec,
+              int mode, uint32_t bucket, void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* B2COMM_H */

@@ -1,0 +1,109 @@
+"""Build recipe for libb2comm.so (sm_100a) and librcomm_b200.so (C++ host layer).
+
+Plain nvcc/g++ invocations, outputs in-tree next to this file so the built
+libraries travel to the GPU box with the repo snapshot.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(PKG_DIR)
+CSRC = os.path.join(PKG_DIR, "csrc")
+HOST = os.path.join(PKG_DIR, "host")
+INCLUDE = os.path.join(REPO, "include")
+LIB = os.path.join(PKG_DIR, "libb2comm.so")
+HOSTLIB = os.path.join(PKG_DIR, "librcomm_b200.so")
+
+CUDA_SOURCES = ["codec.cu", "collectives.cu", "comm.cu"]
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC,-O2,-fvisibility=hidden",
+    "-Xptxas", "-v",
+    "--expt-relaxed-constexpr",
+]
+
+
+def _nvcc() -> str:
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if c and os.path.exists(c):
+            return c
+    raise RuntimeError("nvcc not found")
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _deps(dirpath: str, exts: tuple[str, ...]) -> list[str]:
+    return [os.path.join(dirpath, f) for f in sorted(os.listdir(dirpath)) if f.endswith(exts)]
+
+
+def build_cuda(force: bool = False, verbose: bool = False) -> str:
+    deps = _deps(CSRC, (".cu", ".cuh", ".h")) + [os.path.join(INCLUDE, "b2comm.h")]
+    if not force and not _stale(LIB, deps):
+        return LIB
+    objdir = os.path.join(PKG_DIR, "build")
+    os.makedirs(objdir, exist_ok=True)
+    nvcc = _nvcc()
+    objs = []
+    for src in CUDA_SOURCES:
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {src}")
+        if verbose:
+            sys.stderr.write(r.stderr)
+        with open(os.path.join(objdir, src + ".ptxas.txt"), "w") as f:
+            f.write(r.stderr)
+        objs.append(obj)
+    tmp = LIB + ".tmp"
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
+           "-Xlinker", "--exclude-libs,ALL"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc link failed")
+    os.replace(tmp, LIB)
+    return LIB
+
+
+def build_host(force: bool = False) -> str | None:
+    """C++ host layer mirroring rcomm's API over the C ABI."""
+    if not os.path.isdir(HOST):
+        return None
+    srcs = [p for p in _deps(HOST, (".cpp",))]
+    if not srcs:
+        return None
+    deps = srcs + _deps(os.path.join(INCLUDE, "rcomm_b200"), (".hpp",)) + [LIB]
+    if not force and not _stale(HOSTLIB, deps):
+        return HOSTLIB
+    cuda_inc = "/usr/local/cuda/include"
+    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INCLUDE, "-I", cuda_inc, *srcs,
+           "-o", HOSTLIB + ".tmp", "-L", PKG_DIR, "-lb2comm", "-Wl,-rpath,$ORIGIN",
+           "-L/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,/usr/local/cuda/lib64", "-lpthread"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("g++ failed on the host layer")
+    os.replace(HOSTLIB + ".tmp", HOSTLIB)
+    return HOSTLIB
+
+
+def build(force: bool = False, verbose: bool = False) -> None:
+    build_cuda(force=force, verbose=verbose)
+    build_host(force=force)
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,321 @@
+"""The four synchronous primitives behind rcomm's API (collectives.hpp:13-89).
+
+``B200Endpoint`` stands where rcomm's ``Endpoint`` stands (transport.hpp:52-85):
+one per worker (process or thread), bound to one GPU.  The primitive
+functions keep the reference signatures -- ``c_lp_s(ep, now, x, codec, es,
+rng=None, bucket=0)`` etc. -- update ``x`` in place, are blocking by default
+(the reference's rendezvous semantics) and return ``now`` unchanged (there is
+no virtual clock on real hardware; TcpEndpoint likewise passes clocks
+through, transport.hpp:276-279).
+
+``x`` may be a CUDA float32 tensor (zero-copy), a FlatTensor / BucketArena,
+or a host buffer (numpy array / CPU tensor), which is staged through pinned
+memory -- the end-to-end path a drop-in user of host vectors gets.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import Error, check, lib
+from .codec import Codec, CodecKind, ErrorState, Rounding
+
+
+class TopologyKind(enum.IntEnum):
+    ring = _lib.TOPO_RING
+    random = _lib.TOPO_RANDOM
+    full = _lib.TOPO_FULL
+
+
+class ReduceMode(enum.IntEnum):
+    sum = _lib.REDUCE_SUM
+    average = _lib.REDUCE_AVERAGE
+
+
+class phase:  # collectives.hpp:29-38
+    scatter, gather, inter, bcast = 0, 1, 2, 3
+
+    @staticmethod
+    def make_tag(bucket: int, ph: int) -> int:
+        return bucket * 16 + ph
+
+
+def partition_range(length: int, n: int, k: int):
+    lo, sz = C.c_size_t(), C.c_size_t()
+    lib.b2_partition_range(length, n, k, C.byref(lo), C.byref(sz))
+    return lo.value, sz.value
+
+
+def owned_partition_len(length: int, world: int, idx: int) -> int:
+    return int(lib.b2_owned_partition_len(length, world, idx))
+
+
+class Topology:
+    """Neighbour function N(i), sorted and self-inclusive (collectives.hpp:18-25)."""
+
+    def __init__(self, kind: TopologyKind = TopologyKind.full, n: int = 1, seed: int = 0):
+        self.kind, self.n, self.seed = TopologyKind(kind), int(n), int(seed)
+
+    def neighbors(self, rank: int, round_: int) -> list[int]:
+        out = (C.c_int * max(self.n, 3))()
+        m = lib.b2_topology_neighbors(int(self.kind), self.n, self.seed & (2**64 - 1), rank,
+                                      int(round_) & (2**64 - 1), out)
+        if m < 0:
+            raise Error(_lib.last_error())
+        return list(out[:m])
+
+
+# --------------------------------------------------------------- bootstrap
+class TorchBootstrap:
+    """Window-handle exchange over a gloo group of torch.distributed."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group if group is not None else dist.new_group(backend="gloo")
+
+    def allgather(self, data: bytes, world: int) -> list[bytes]:
+        t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+        outs = [torch.empty_like(t) for _ in range(world)]
+        self.dist.all_gather(outs, t, group=self.group)
+        return [o.numpy().tobytes() for o in outs]
+
+
+class ThreadBootstrap:
+    """In-process exchange for one thread per GPU (SimCluster's threading
+    model, sim_transport.cpp:93-128).  Share one instance among the threads."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self._barrier = threading.Barrier(world)
+        self._slots: list[bytes | None] = [None] * world
+        self._rank = threading.local()
+
+    def allgather(self, data: bytes, world: int, rank: int) -> list[bytes]:
+        self._slots[rank] = data
+        self._barrier.wait()
+        out = list(self._slots)
+        self._barrier.wait()
+        return out
+
+
+class B200Endpoint:
+    """One worker's handle on the B200 communicator (libb2comm b2_comm_t)."""
+
+    def __init__(self, rank: int | None = None, world_size: int | None = None, device: int | None = None,
+                 bootstrap=None, timeout_ms: int = 20000):
+        import torch.distributed as dist
+        if rank is None or world_size is None:
+            if dist.is_available() and dist.is_initialized():
+                rank, world_size = dist.get_rank(), dist.get_world_size()
+            else:
+                rank, world_size = 0, 1
+        if device is None:
+            device = int(os.environ.get("LOCAL_RANK", rank)) % max(torch.cuda.device_count(), 1)
+        self._rank, self._world, self.device = int(rank), int(world_size), int(device)
+        if bootstrap is None and self._world > 1:
+            bootstrap = TorchBootstrap()
+        self._bootstrap = bootstrap
+        self._cb = _lib.ALLGATHER_FN(self._allgather)  # keep alive
+        self._bytes_sent = 0
+        self._messages_sent = 0
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            check(lib.b2_comm_create(self._world, self._rank, self.device, self._cb, None, C.byref(h)))
+        self._h = h
+        check(lib.b2_comm_set_timeout_ms(h, timeout_ms))
+
+    def _allgather(self, user, send, nbytes, recv) -> int:
+        try:
+            data = C.string_at(send, nbytes)
+            if isinstance(self._bootstrap, ThreadBootstrap):
+                parts = self._bootstrap.allgather(data, self._world, self._rank)
+            else:
+                parts = self._bootstrap.allgather(data, self._world)
+            blob = b"".join(parts)
+            C.memmove(recv, blob, len(blob))
+            return 0
+        except Exception:  # surfaced to C as B2_ERR_BOOTSTRAP
+            return 1
+
+    # Endpoint interface (transport.hpp:214-242)
+    def rank(self) -> int:
+        return self._rank
+
+    def world_size(self) -> int:
+        return self._world
+
+    def node(self) -> int:
+        return 0
+
+    def node_of(self, rank: int) -> int:
+        if not 0 <= rank < self._world:
+            raise Error(f"unknown rank {rank}")
+        return 0
+
+    def bytes_sent(self) -> int:
+        return self._bytes_sent
+
+    def messages_sent(self) -> int:
+        return self._messages_sent
+
+    def reset_counters(self) -> None:
+        self._bytes_sent = self._messages_sent = 0
+
+    def launches(self) -> int:
+        return int(lib.b2_comm_launches(self._h))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def sync(self) -> None:
+        """Wait for this rank's queued primitives; raise on latched errors."""
+        check(lib.b2_comm_sync(self._h, self.stream()))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.b2_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _account(self, nbytes: int, msgs: int) -> None:
+        self._bytes_sent += nbytes
+        self._messages_sent += msgs
+
+
+# ------------------------------------------------------------ bucket staging
+class _Bucket:
+    """Resolve x to an aligned contiguous device float32 tensor; write back
+    on exit when a staging copy was needed (host input or misalignment)."""
+
+    def __init__(self, ep: B200Endpoint, x):
+        from .tensor import BucketArena, FlatTensor
+        self.orig = x
+        if isinstance(x, (FlatTensor, BucketArena)):
+            x = x.data()
+        self.host = not (isinstance(x, torch.Tensor) and x.is_cuda)
+        if self.host:
+            arr = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, np.float32))
+            self.host_t = arr
+            pinned = arr.to(torch.float32).reshape(-1).pin_memory()
+            self.dev = pinned.to(torch.device("cuda", ep.device), non_blocking=True)
+            self.view = None
+        else:
+            if x.dtype != torch.float32:
+                raise Error("bucket must be float32")
+            self.view = x
+            flat = x.reshape(-1) if x.is_contiguous() else None
+            if flat is None or flat.data_ptr() % 16:
+                self.dev = x.reshape(-1).clone()
+            else:
+                self.dev = flat
+        self.n = self.dev.numel()
+
+    def finish(self) -> None:
+        if self.host:
+            res = self.dev.cpu()
+            if isinstance(self.host_t, torch.Tensor):
+                self.host_t.copy_(res.view_as(self.host_t))
+            else:
+                np.copyto(self.host_t, res.numpy().reshape(np.shape(self.host_t)))
+        elif self.dev is not self.view and self.dev.data_ptr() != self.view.data_ptr():
+            self.view.copy_(self.dev.view_as(self.view))
+
+
+def _finish(ep: B200Endpoint, b: _Bucket, blocking: bool) -> None:
+    if blocking or b.host:
+        ep.sync()
+    b.finish()
+
+
+def c_fp_s(ep: B200Endpoint, now: float, x, bucket: int = 0, blocking: bool = True) -> float:
+    """Allreduce-equivalent; every rank ends with sum_j x_j folded in fp64 in
+    ascending rank order (collectives.hpp:50-52)."""
+    b = _Bucket(ep, x)
+    with torch.cuda.device(ep.device):
+        check(lib.b2_c_fp_s(ep.handle, b.dev.data_ptr(), b.n, bucket, ep.stream()))
+        _finish(ep, b, blocking)
+    g, me = ep.world_size(), ep.rank()
+    if g > 1:
+        ep._account(4 * (b.n - owned_partition_len(b.n, g, me)) + (g - 1) * 4 * owned_partition_len(b.n, g, me),
+                    2 * (g - 1))
+    return now
+
+
+def c_lp_s(ep: B200Endpoint, now: float, x, codec: Codec, es: ErrorState | None, rng=None,
+           bucket: int = 0, blocking: bool = True) -> float:
+    """Compressed ScatterReduce with two compression phases
+    (collectives.hpp:54-61).  es != None applies error compensation."""
+    codec._check_supported(rng)
+    b = _Bucket(ep, x)
+    g, me = ep.world_size(), ep.rank()
+    own = owned_partition_len(b.n, g, me)
+    dptr = eptr = 0
+    dlen = elen = 0
+    if es is not None:
+        if es.delta.numel() != b.n:
+            raise Error("c_lp_s: delta length does not match bucket length")
+        if es.epsilon.numel() != own:
+            raise Error("c_lp_s: epsilon length does not match owned partition")
+        if es.delta.data_ptr() % 16:
+            raise Error("c_lp_s: delta must be 16-byte aligned")
+        dptr, dlen = es.delta.data_ptr(), es.delta.numel()
+        eptr, elen = (es.epsilon.data_ptr() if own else es.delta.data_ptr()), own
+    with torch.cuda.device(ep.device):
+        check(lib.b2_c_lp_s(ep.handle, b.dev.data_ptr(), b.n, int(codec.kind), dptr, dlen, eptr, elen, bucket,
+                            ep.stream()))
+        _finish(ep, b, blocking)
+    if g > 1:
+        per = lambda m: codec.payload_size(m)  # noqa: E731
+        sent = sum(per(partition_range(b.n, g, k)[1]) for k in range(g) if k != me) + (g - 1) * per(own)
+        ep._account(sent, 2 * (g - 1))
+    return now
+
+
+def _neighbors(ep: B200Endpoint, topo: Topology, round_: int):
+    if topo.n != ep.world_size():
+        raise Error("topology size mismatch")  # collectives.cpp:232
+    nb = topo.neighbors(ep.rank(), round_)
+    return (C.c_int * len(nb))(*nb), len(nb)
+
+
+def d_fp_s(ep: B200Endpoint, now: float, x, topo: Topology, round_: int, mode: ReduceMode,
+           bucket: int = 0, blocking: bool = True) -> float:
+    """Neighbourhood sum / average (collectives.hpp:63-66)."""
+    arr, m = _neighbors(ep, topo, round_)
+    b = _Bucket(ep, x)
+    with torch.cuda.device(ep.device):
+        check(lib.b2_d_fp_s(ep.handle, b.dev.data_ptr(), b.n, arr, m, int(mode), bucket, ep.stream()))
+        _finish(ep, b, blocking)
+    ep._account((m - 1) * 4 * b.n, m - 1)
+    return now
+
+
+def d_lp_s(ep: B200Endpoint, now: float, x, topo: Topology, round_: int, codec: Codec, mode: ReduceMode,
+           rng=None, bucket: int = 0, blocking: bool = True) -> float:
+    """As d_fp_s, every contribution (self included) through Q
+    (collectives.hpp:68-72)."""
+    codec._check_supported(rng)
+    arr, m = _neighbors(ep, topo, round_)
+    b = _Bucket(ep, x)
+    with torch.cuda.device(ep.device):
+        check(lib.b2_d_lp_s(ep.handle, b.dev.data_ptr(), b.n, arr, m, int(codec.kind), int(mode), bucket,
+                            ep.stream()))
+        _finish(ep, b, blocking)
+    ep._account((m - 1) * codec.payload_size(b.n), m - 1)
+    return now

@@ -1,0 +1,38 @@
+// b2_host.h -- host-side helpers shared by the translation units of libb2comm.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "b2comm.h"
+
+namespace b2 {
+
+void set_error(const char* fmt, ...);
+
+#define B2_CUDA_TRY(expr)                                                        \
+  do {                                                                           \
+    cudaError_t _e = (expr);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      ::b2::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),    \
+                      __FILE__, __LINE__);                                       \
+      return B2_ERR_CUDA;                                                        \
+    }                                                                            \
+  } while (0)
+
+#define B2_REQUIRE(cond, ...)         \
+  do {                                \
+    if (!(cond)) {                    \
+      ::b2::set_error(__VA_ARGS__);   \
+      return B2_ERR_INVALID;          \
+    }                                 \
+  } while (0)
+
+// Persistent-grid size for a kernel: SMs x resident CTAs per SM.
+int persistent_grid(const void* func, int threads, size_t smem = 0);
+int sm_count();
+
+}  // namespace b2

@@ -1,0 +1,65 @@
+// collectives.cuh -- argument blocks and window layout shared by the
+// collective kernels (collectives.cu) and the communicator (comm.cu).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include "b2_device.cuh"
+
+namespace b2 {
+
+// Every rank's window for one (bucket, family, size) has the same layout.
+// The first 256 bytes are control words; data regions follow, 256-aligned.
+struct WinHdr {
+  unsigned long long arrive1;   // central: #ranks whose phase-1 chunk for me landed (cumulative)
+  unsigned long long ready2;    // central: epoch of my published phase-2 output
+  unsigned long long dready[2]; // decentral: epoch of my published buffer, per parity
+  unsigned long long dreads[2]; // decentral: #neighbour reads of my buffer completed (cumulative)
+  unsigned long long pad0[2];
+  float2 hdr1[kMaxRanks];       // central uint8: (min,max) of my chunk as encoded by rank j
+  float2 hdr2;                  // central uint8: (min,max) of my phase-2 payload
+  float2 dhdr[2];               // decentral uint8: (min,max) of my bucket, per parity
+};
+static_assert(sizeof(WinHdr) <= 256, "window header exceeds 256 bytes");
+
+enum Codec : int { kIdentity = 0, kU8 = 1 };
+
+// Centralized ScatterReduce (C_FP_S, C_LP_S).
+struct CentralArgs {
+  float* x;
+  size_t n;
+  int g, me;
+  int check_finite;             // identity c_lp_s: encode validates (codec.cpp:41)
+  unsigned long long epoch;     // 1-based call counter of this window
+  float* delta;                 // ErrorState::delta (n) or null
+  float* eps;                   // ErrorState::epsilon (owned len) or null
+  uint8_t* win[kMaxRanks];      // every rank's window base (peer-mapped; win[me] local)
+  size_t off_recv1, slot_stride, off_out2;
+  float2* partials;             // local workspace [(kMaxRanks + 1) * grid]
+  unsigned* cta_done;           // local workspace [kMaxRanks + 2]
+  float* scratch;               // local, owned-len y2 cache, or null (recompute)
+  int* status;                  // mapped host status word
+  unsigned long long timeout_ns;
+};
+
+// Decentralized neighbourhood reduce (D_FP_S, D_LP_S).
+struct DecentArgs {
+  float* x;
+  size_t n;
+  int me, nnb;
+  int nbrs[kMaxRanks];          // sorted, self-inclusive
+  int check_finite;
+  int parity;
+  unsigned long long epoch;
+  unsigned long long expected_reads;  // dreads[parity] must reach this before we overwrite
+  double inv;                   // 1/|N| (average) or 1.0 (sum), collectives.cpp:252-254
+  uint8_t* win[kMaxRanks];
+  size_t off_dbuf;              // offset of dbuf[parity]
+  float2* partials;
+  unsigned* cta_done;
+  int* status;
+  unsigned long long timeout_ns;
+};
+
+}  // namespace b2

@@ -1,0 +1,475 @@
+// comm.cu -- communicator, peer windows and the C-ABI entry points of the
+// primitives (include/b2comm.h).
+//
+// The reference's Endpoint moves opaque byte messages between workers
+// (transport.hpp:52-85; sim_transport.cpp:29-69, where send() copies the
+// payload into the peer's mailbox).  Here the "mailbox" is a window of
+// device memory that every peer maps: one cudaMalloc per (bucket, family,
+// size) whose CUDA IPC handle (or raw pointer, for ranks living in the same
+// process) is exchanged once through the caller's allgather.  Kernels then
+// store into / load from peer windows directly over NVLink/NVSwitch; the
+// (src, tag) FIFO matching of the reference becomes epoch-tagged counters in
+// each window's header (collectives.cuh: WinHdr).
+#include <cuda_runtime.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <random>
+#include <tuple>
+#include <vector>
+
+#include "b2_host.h"
+#include "collectives.cuh"
+
+namespace b2 {
+int launch_central(const CentralArgs& a, int codec, bool ec, cudaStream_t s);
+int launch_decent(const DecentArgs& a, int codec, cudaStream_t s);
+int max_persistent_grid();
+}  // namespace b2
+
+using namespace b2;
+
+namespace {
+
+enum Family { kCentral = 0, kDecentral = 1 };
+
+struct Window {
+  size_t bytes = 0;
+  uint8_t* local = nullptr;
+  uint8_t* peer[kMaxRanks] = {};
+  bool ipc_opened[kMaxRanks] = {};
+  size_t off_recv1 = 0, slot_stride = 0, off_out2 = 0, off_dbuf[2] = {0, 0};
+  unsigned long long epoch = 0;
+  unsigned long long exp_reads[2] = {0, 0};
+  float2* partials = nullptr;
+  unsigned* cta_done = nullptr;
+  float* scratch = nullptr;
+};
+
+struct Blob {  // what each rank publishes about one window
+  int pid;
+  int device;
+  unsigned long long ptr;
+  unsigned long long bytes;
+  cudaIpcMemHandle_t handle;
+};
+
+size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+struct b2_comm {
+  int world = 1, rank = 0, device = 0;
+  b2_allgather_fn allgather = nullptr;
+  void* user = nullptr;
+  std::map<std::tuple<uint32_t, int, size_t, int>, Window*> wins;
+  int* status_h = nullptr;  // mapped pinned host word
+  int* status_d = nullptr;
+  unsigned long long timeout_ns = 20000ull * 1000000ull;
+  unsigned long long launches = 0;
+  std::mutex mu;
+};
+
+namespace {
+
+struct DeviceGuard {  // make the communicator's GPU current for this call
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void free_window(b2_comm* c, Window* w) {
+  for (int j = 0; j < kMaxRanks; ++j)
+    if (w->ipc_opened[j]) cudaIpcCloseMemHandle(w->peer[j]);
+  if (w->local) cudaFree(w->local);
+  if (w->partials) cudaFree(w->partials);
+  if (w->cta_done) cudaFree(w->cta_done);
+  if (w->scratch) cudaFree(w->scratch);
+  delete w;
+  (void)c;
+}
+
+// Collective: every rank calls with identical (bucket, family, n, elem).
+int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Window** out) {
+  const auto key = std::make_tuple(bucket, family, n, elem);
+  auto it = c->wins.find(key);
+  if (it != c->wins.end()) {
+    *out = it->second;
+    return B2_OK;
+  }
+  const int g = c->world;
+  Window* w = new Window();
+  size_t off = 256;  // WinHdr
+  if (family == kCentral) {
+    const size_t maxchunk = (n + g - 1) / g;
+    w->slot_stride = round_up(size_t(elem) * (maxchunk + 8), 256);
+    w->off_recv1 = off;
+    off += size_t(g) * w->slot_stride;
+    w->off_out2 = off;
+    off += w->slot_stride;
+  } else {
+    const size_t b = round_up(size_t(elem) * (n + 8), 256);
+    w->off_dbuf[0] = off;
+    off += b;
+    w->off_dbuf[1] = off;
+    off += b;
+  }
+  w->bytes = off;
+  auto fail = [&](int rc) {
+    free_window(c, w);
+    return rc;
+  };
+  if (cudaMalloc(&w->local, w->bytes) != cudaSuccess ||
+      cudaMemset(w->local, 0, 256) != cudaSuccess ||
+      cudaMalloc(&w->partials, sizeof(float2) * (kMaxRanks + 1) * max_persistent_grid()) !=
+          cudaSuccess ||
+      cudaMalloc(&w->cta_done, sizeof(unsigned) * (kMaxRanks + 2)) != cudaSuccess ||
+      cudaMemset(w->cta_done, 0, sizeof(unsigned) * (kMaxRanks + 2)) != cudaSuccess) {
+    set_error("window allocation of %zu bytes failed: %s", w->bytes,
+              cudaGetErrorString(cudaGetLastError()));
+    return fail(B2_ERR_CUDA);
+  }
+  // Cache the owner's y2 in scratch when that costs fewer HBM bytes than
+  // re-folding the g contributions (4N/g written+read vs N re-read): g >= 4.
+  if (family == kCentral && elem == 1 && g >= 4) {
+    const size_t maxchunk = (n + g - 1) / g;
+    if (cudaMalloc(&w->scratch, sizeof(float) * (maxchunk + 8)) != cudaSuccess) {
+      set_error("scratch allocation failed");
+      return fail(B2_ERR_CUDA);
+    }
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    set_error("window init failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return fail(B2_ERR_CUDA);
+  }
+  w->peer[c->rank] = w->local;
+  if (g > 1) {
+    Blob mine{};
+    mine.pid = static_cast<int>(getpid());
+    mine.device = c->device;
+    mine.ptr = reinterpret_cast<unsigned long long>(w->local);
+    mine.bytes = w->bytes;
+    if (cudaIpcGetMemHandle(&mine.handle, w->local) != cudaSuccess) {
+      set_error("cudaIpcGetMemHandle failed: %s", cudaGetErrorString(cudaGetLastError()));
+      return fail(B2_ERR_CUDA);
+    }
+    std::vector<Blob> all(g);
+    if (!c->allgather || c->allgather(c->user, &mine, sizeof(Blob), all.data()) != 0) {
+      set_error("bootstrap allgather failed for bucket %u", bucket);
+      return fail(B2_ERR_BOOTSTRAP);
+    }
+    for (int j = 0; j < g; ++j) {
+      if (all[j].bytes != w->bytes) {
+        set_error("rank %d window size %llu != %zu: mismatched collective arguments", j,
+                  all[j].bytes, w->bytes);
+        return fail(B2_ERR_INVALID);
+      }
+      if (j == c->rank) continue;
+      if (all[j].pid == mine.pid) {  // same process: plain peer access
+        if (all[j].device != c->device) {
+          cudaError_t e = cudaDeviceEnablePeerAccess(all[j].device, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+            set_error("peer access %d->%d: %s", c->device, all[j].device, cudaGetErrorString(e));
+            return fail(B2_ERR_CUDA);
+          }
+          cudaGetLastError();
+        }
+        w->peer[j] = reinterpret_cast<uint8_t*>(all[j].ptr);
+      } else {
+        void* p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, all[j].handle, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+          set_error("cudaIpcOpenMemHandle(rank %d): %s", j, cudaGetErrorString(e));
+          return fail(B2_ERR_CUDA);
+        }
+        w->peer[j] = static_cast<uint8_t*>(p);
+        w->ipc_opened[j] = true;
+      }
+    }
+  }
+  c->wins[key] = w;
+  *out = w;
+  return B2_OK;
+}
+
+int check_comm(b2_comm* c, const float* x, size_t n) {
+  B2_REQUIRE(c, "null communicator");
+  B2_REQUIRE(n == 0 || x, "null bucket pointer");
+  B2_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0, "bucket must be 16-byte aligned");
+  return B2_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int b2_version(void) { return B2COMM_VERSION; }
+
+const char* b2_status_string(int s) {
+  switch (s) {
+    case B2_OK: return "ok";
+    case B2_ERR_INVALID: return "invalid argument";
+    case B2_ERR_CUDA: return "cuda error";
+    case B2_ERR_NONFINITE: return "encode: non-finite input value";
+    case B2_ERR_TIMEOUT: return "rendezvous timeout";
+    case B2_ERR_UNSUPPORTED: return "unsupported";
+    case B2_ERR_BOOTSTRAP: return "bootstrap failure";
+  }
+  return "unknown";
+}
+
+void b2_partition_range(size_t len, int n, int k, size_t* lo, size_t* sz) {
+  const size_t base = len / size_t(n), extra = len % size_t(n), uk = size_t(k);
+  *lo = uk * base + std::min(uk, extra);
+  *sz = base + (uk < extra ? 1 : 0);
+}
+
+size_t b2_owned_partition_len(size_t len, int world, int idx) {
+  size_t lo, sz;
+  b2_partition_range(len, world, idx, &lo, &sz);
+  return sz;
+}
+
+size_t b2_payload_size(int codec, size_t n) {  // codec.cpp:31-38
+  switch (codec) {
+    case B2_CODEC_IDENTITY: return 4 * n;
+    case B2_CODEC_UNIFORM8: return 8 + n;
+    case B2_CODEC_ONEBIT: return 4 + (n + 7) / 8;
+  }
+  return 0;
+}
+
+// Topology::neighbors, collectives.cpp:181-213 -- the random matching uses
+// the same mt19937_64 seed mix and std::shuffle, so every rank (and the
+// reference) agrees on it.
+int b2_topology_neighbors(int kind, int n, uint64_t seed, int rank, uint64_t round, int* out) {
+  if (rank < 0 || rank >= n || !out) {
+    set_error("topology: rank out of range");
+    return -1;
+  }
+  std::vector<int> nb;
+  if (kind == B2_TOPO_FULL) {
+    nb.resize(size_t(n));
+    std::iota(nb.begin(), nb.end(), 0);
+  } else if (kind == B2_TOPO_RING) {
+    nb = {(rank + n - 1) % n, rank, (rank + 1) % n};
+    std::sort(nb.begin(), nb.end());
+    nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+  } else if (kind == B2_TOPO_RANDOM) {
+    std::mt19937_64 rng(seed ^ (0x9e3779b97f4a7c15ULL * (round + 1)));
+    std::vector<int> perm(static_cast<size_t>(n));
+    std::iota(perm.begin(), perm.end(), 0);
+    std::shuffle(perm.begin(), perm.end(), rng);
+    int peer = rank;
+    for (int i = 0; i + 1 < n; i += 2) {
+      if (perm[i] == rank) peer = perm[i + 1];
+      if (perm[i + 1] == rank) peer = perm[i];
+    }
+    nb = {rank};
+    if (peer != rank) nb.push_back(peer);
+    std::sort(nb.begin(), nb.end());
+  } else {
+    set_error("topology: unknown kind");
+    return -1;
+  }
+  std::copy(nb.begin(), nb.end(), out);
+  return static_cast<int>(nb.size());
+}
+
+int b2_comm_create(int world, int rank, int device, b2_allgather_fn allgather, void* user,
+                   b2_comm_t* out) {
+  B2_REQUIRE(out, "null output handle");
+  B2_REQUIRE(world >= 1 && world <= B2_MAX_RANKS, "world size %d outside [1, %d]", world,
+             B2_MAX_RANKS);
+  B2_REQUIRE(rank >= 0 && rank < world, "rank %d outside [0, %d)", rank, world);
+  B2_REQUIRE(world == 1 || allgather, "world > 1 needs an allgather bootstrap");
+  DeviceGuard dg(device);
+  int coop = 0;
+  B2_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+  B2_REQUIRE(coop, "device %d does not support cooperative launch", device);
+  b2_comm* c = new b2_comm();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  c->allgather = allgather;
+  c->user = user;
+  if (cudaHostAlloc(&c->status_h, sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(&c->status_d, c->status_h, 0) != cudaSuccess) {
+    set_error("status word allocation failed: %s", cudaGetErrorString(cudaGetLastError()));
+    delete c;
+    return B2_ERR_CUDA;
+  }
+  *c->status_h = 0;
+  *out = c;
+  return B2_OK;
+}
+
+int b2_comm_destroy(b2_comm_t c) {
+  if (!c) return B2_OK;
+  DeviceGuard dg(c->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : c->wins) free_window(c, kv.second);
+  if (c->status_h) cudaFreeHost(c->status_h);
+  delete c;
+  return B2_OK;
+}
+
+int b2_comm_rank(b2_comm_t c) { return c ? c->rank : -1; }
+int b2_comm_world(b2_comm_t c) { return c ? c->world : -1; }
+uint64_t b2_comm_launches(b2_comm_t c) { return c ? c->launches : 0; }
+
+int b2_comm_set_timeout_ms(b2_comm_t c, uint64_t ms) {
+  B2_REQUIRE(c, "null communicator");
+  c->timeout_ns = static_cast<unsigned long long>(ms) * 1000000ull;
+  return B2_OK;
+}
+
+int b2_comm_poll(b2_comm_t c) {
+  B2_REQUIRE(c, "null communicator");
+  const int s = __atomic_exchange_n(c->status_h, 0, __ATOMIC_SEQ_CST);
+  if (s & kStatusTimeout) {
+    set_error("rendezvous timeout: a peer did not arrive");
+    return B2_ERR_TIMEOUT;
+  }
+  if (s & kStatusNonFinite) {
+    set_error("encode: non-finite input value");
+    return B2_ERR_NONFINITE;
+  }
+  return B2_OK;
+}
+
+int b2_comm_sync(b2_comm_t c, void* stream) {
+  B2_REQUIRE(c, "null communicator");
+  DeviceGuard dg(c->device);
+  B2_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return b2_comm_poll(c);
+}
+
+static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite, float* delta,
+                   size_t delta_len, float* eps, size_t eps_len, uint32_t bucket, void* stream) {
+  int rc = check_comm(c, x, n);
+  if (rc) return rc;
+  B2_REQUIRE((delta == nullptr) == (eps == nullptr), "delta and eps must both be set or both null");
+  const size_t own = b2_owned_partition_len(n, c->world, c->rank);
+  if (delta) {  // collectives.cpp:102-107
+    B2_REQUIRE(delta_len == n, "c_lp_s: delta length does not match bucket length");
+    B2_REQUIRE(eps_len == own, "c_lp_s: epsilon length does not match owned partition");
+    B2_REQUIRE((reinterpret_cast<uintptr_t>(delta) & 15) == 0, "delta must be 16-byte aligned");
+  }
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  Window* w = nullptr;
+  rc = get_window(c, bucket, kCentral, n, codec == B2_CODEC_UNIFORM8 ? 1 : 4, &w);
+  if (rc) return rc;
+  CentralArgs a{};
+  a.x = x;
+  a.n = n;
+  a.g = c->world;
+  a.me = c->rank;
+  a.check_finite = check_finite;
+  a.epoch = ++w->epoch;
+  a.delta = delta;
+  a.eps = eps;
+  for (int j = 0; j < c->world; ++j) a.win[j] = w->peer[j];
+  a.off_recv1 = w->off_recv1;
+  a.slot_stride = w->slot_stride;
+  a.off_out2 = w->off_out2;
+  a.partials = w->partials;
+  a.cta_done = w->cta_done;
+  a.scratch = w->scratch;
+  a.status = c->status_d;
+  a.timeout_ns = c->timeout_ns;
+  rc = launch_central(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity, delta != nullptr,
+                      static_cast<cudaStream_t>(stream));
+  if (rc == B2_OK) ++c->launches;
+  return rc;
+}
+
+int b2_c_fp_s(b2_comm_t c, float* x, size_t n, uint32_t bucket, void* stream) {
+  int rc = check_comm(c, x, n);
+  if (rc) return rc;
+  if (c->world == 1) return B2_OK;  // collectives.cpp:49: x untouched
+  return central(c, x, n, B2_CODEC_IDENTITY, 0, nullptr, 0, nullptr, 0, bucket, stream);
+}
+
+int b2_c_lp_s(b2_comm_t c, float* x, size_t n, int codec, float* delta, size_t delta_len,
+              float* eps, size_t eps_len, uint32_t bucket, void* stream) {
+  if (codec == B2_CODEC_ONEBIT) {
+    set_error("c_lp_s: onebit codec is not implemented on the B200 path");
+    return B2_ERR_UNSUPPORTED;
+  }
+  B2_REQUIRE(codec == B2_CODEC_UNIFORM8 || codec == B2_CODEC_IDENTITY, "unknown codec %d", codec);
+  return central(c, x, n, codec, 1, delta, delta_len, eps, eps_len, bucket, stream);
+}
+
+static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbrs, int codec,
+                     int check_finite, int mode, uint32_t bucket, void* stream) {
+  int rc = check_comm(c, x, n);
+  if (rc) return rc;
+  B2_REQUIRE(nbrs && n_nbrs >= 1 && n_nbrs <= c->world, "neighbour list of size %d invalid", n_nbrs);
+  B2_REQUIRE(mode == B2_REDUCE_SUM || mode == B2_REDUCE_AVERAGE, "unknown reduce mode %d", mode);
+  bool has_self = false;
+  for (int i = 0; i < n_nbrs; ++i) {
+    B2_REQUIRE(nbrs[i] >= 0 && nbrs[i] < c->world, "neighbour %d out of range", nbrs[i]);
+    B2_REQUIRE(i == 0 || nbrs[i] > nbrs[i - 1], "neighbour list must be sorted and unique");
+    has_self |= nbrs[i] == c->rank;
+  }
+  B2_REQUIRE(has_self, "neighbour list must include the calling rank");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  Window* w = nullptr;
+  rc = get_window(c, bucket, kDecentral, n, codec == B2_CODEC_UNIFORM8 ? 1 : 4, &w);
+  if (rc) return rc;
+  DecentArgs a{};
+  a.x = x;
+  a.n = n;
+  a.me = c->rank;
+  a.nnb = n_nbrs;
+  for (int i = 0; i < n_nbrs; ++i) a.nbrs[i] = nbrs[i];
+  a.check_finite = check_finite;
+  a.epoch = ++w->epoch;
+  a.parity = static_cast<int>(a.epoch & 1);
+  a.expected_reads = w->exp_reads[a.parity];
+  a.inv = mode == B2_REDUCE_AVERAGE ? 1.0 / static_cast<double>(n_nbrs) : 1.0;
+  for (int j = 0; j < c->world; ++j) a.win[j] = w->peer[j];
+  a.off_dbuf = w->off_dbuf[a.parity];
+  a.partials = w->partials;
+  a.cta_done = w->cta_done;
+  a.status = c->status_d;
+  a.timeout_ns = c->timeout_ns;
+  rc = launch_decent(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity,
+                     static_cast<cudaStream_t>(stream));
+  if (rc == B2_OK) {
+    w->exp_reads[a.parity] += static_cast<unsigned long long>(n_nbrs - 1);
+    ++c->launches;
+  }
+  return rc;
+}
+
+int b2_d_fp_s(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbrs, int mode,
+              uint32_t bucket, void* stream) {
+  return decentral(c, x, n, nbrs, n_nbrs, B2_CODEC_IDENTITY, 0, mode, bucket, stream);
+}
+
+int b2_d_lp_s(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbrs, int codec, int mode,
+              uint32_t bucket, void* stream) {
+  if (codec == B2_CODEC_ONEBIT) {
+    set_error("d_lp_s: onebit codec is not implemented on the B200 path");
+    return B2_ERR_UNSUPPORTED;
+  }
+  B2_REQUIRE(codec == B2_CODEC_UNIFORM8 || codec == B2_CODEC_IDENTITY, "unknown codec %d", codec);
+  return decentral(c, x, n, nbrs, n_nbrs, codec, 1, mode, bucket, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,199 @@
+"""Multi-GPU parity driver: one process per GPU (torchrun), every primitive
+against the CPU oracle on identical, deterministically generated inputs.
+
+    python -m torch.distributed.run --nproc-per-node G --master-addr 127.0.0.1 \
+        --master-port 29511 tests/mp_parity.py [--quick] [--large]
+
+Each rank regenerates every rank's input from the shared seeds (synthetic
+splitmix64 generator, identical on host and device), computes the oracle
+result for ITSELF and compares bit for bit.  For large buckets each rank
+checks its own partition with the partition-local restatement
+and all ranks compare digests of their full outputs (every rank must hold the
+identical bucket after C_*).  Rank 0 prints one JSON line; exit code 1 on
+any mismatch.
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import sys
+import time
+import traceback
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_2107_01499_b200 as b2  # noqa: E402
+from oracle import Oracle  # noqa: E402  (test infrastructure: the checker)
+
+U8 = b2.Codec(b2.CodecKind.uniform8)
+ID = b2.Codec(b2.CodecKind.identity)
+
+
+def bits(a):
+    return np.asarray(a, np.float32).view(np.uint32)
+
+
+class Checker:
+    def __init__(self, rank):
+        self.rank = rank
+        self.fail: list[str] = []
+        self.passed = 0
+
+    def eq(self, name, got, want):
+        if np.array_equal(bits(got), bits(want)):
+            self.passed += 1
+        else:
+            bad = np.flatnonzero(bits(got) != bits(want))
+            self.fail.append(f"rank{self.rank} {name}: {bad.size} mismatches, first at {bad[:5].tolist()} "
+                             f"got {np.asarray(got).ravel()[bad[:3]].tolist()} "
+                             f"want {np.asarray(want).ravel()[bad[:3]].tolist()}")
+
+
+def run(args):
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dev = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(dev)
+    orc = Oracle()
+    ep = b2.B200Endpoint(rank, world, dev)
+    ck = Checker(rank)
+    g = world
+
+    sizes = [1, 3, 5, 37, 1000, 4097, 65536 + 7, 1_000_003]
+    if not args.quick:
+        sizes += [4_000_000, 25_000_000]
+    bucket = 0
+    for n in sizes:
+        bucket += 1
+        xs = [orc.synth(n, 2026 + r) for r in range(g)]
+        # ---- C_LP_S uint8 (stateless), repeated calls on one bucket (epoch protocol)
+        for it in range(3):
+            xs_it = [orc.synth(n, 7000 + 31 * it + r) for r in range(g)]
+            want = [x.copy() for x in xs_it]
+            orc.c_lp_s(want, codec=1)
+            t = torch.as_tensor(xs_it[rank]).cuda()
+            b2.c_lp_s(ep, 0.0, t, U8, None, bucket=bucket)
+            ck.eq(f"c_lp_s u8 n={n} it={it}", t.cpu().numpy(), want[rank])
+        # ---- C_LP_S identity == C_FP_S fp64 ordered sum
+        want = [x.copy() for x in xs]
+        orc.c_lp_s(want, codec=0)
+        t = torch.as_tensor(xs[rank]).cuda()
+        b2.c_lp_s(ep, 0.0, t, ID, None, bucket=bucket)
+        ck.eq(f"c_lp_s identity n={n}", t.cpu().numpy(), want[rank])
+        want = [x.copy() for x in xs]
+        orc.c_fp_s(want)
+        for it in range(2):
+            t = torch.as_tensor(xs[rank]).cuda()
+            b2.c_fp_s(ep, 0.0, t, bucket=bucket)
+            ck.eq(f"c_fp_s n={n} it={it}", t.cpu().numpy(), want[rank])
+        # ---- D_FP_S / D_LP_S over ring, full, random
+        for kind in (b2.TopologyKind.ring, b2.TopologyKind.full, b2.TopologyKind.random):
+            topo = b2.Topology(kind, g, 123)
+            for rnd in range(3):
+                nb = topo.neighbors(rank, rnd)
+                for mode in (b2.ReduceMode.average, b2.ReduceMode.sum):
+                    t = torch.as_tensor(xs[rank]).cuda()
+                    b2.d_fp_s(ep, 0.0, t, topo, rnd, mode, bucket=bucket)
+                    ck.eq(f"d_fp_s {kind.name} r{rnd} {mode.name} n={n}", t.cpu().numpy(),
+                          orc.d_fp_s_rank([xs[j] for j in nb], int(mode)))
+                    t = torch.as_tensor(xs[rank]).cuda()
+                    b2.d_lp_s(ep, 0.0, t, topo, rnd, U8, mode, bucket=bucket)
+                    ck.eq(f"d_lp_s {kind.name} r{rnd} {mode.name} n={n}", t.cpu().numpy(),
+                          orc.d_lp_s_rank([xs[j] for j in nb], 1, int(mode)))
+        t = torch.as_tensor(xs[rank]).cuda()
+        topo = b2.Topology(b2.TopologyKind.ring, g, 0)
+        b2.d_lp_s(ep, 0.0, t, topo, 0, ID, b2.ReduceMode.average, bucket=bucket)
+        ck.eq(f"d_lp_s identity n={n}", t.cpu().numpy(),
+              orc.d_fp_s_rank([xs[j] for j in topo.neighbors(rank, 0)], 1))
+
+    # ---- C_LP_S uint8 + error feedback, acceptance c4 style (many rounds, state carried)
+    for n, rounds in ((37, 200), (100_003, 10)):
+        bucket += 1
+        own = b2.owned_partition_len(n, g, rank)
+        es = b2.ErrorState(n, own)
+        deltas = [np.zeros(n, np.float32) for _ in range(g)]
+        eps = [np.zeros(b2.owned_partition_len(n, g, r), np.float32) for r in range(g)]
+        for t_ in range(rounds):
+            grads = [orc.synth(n, 7000 + 1000 * r + t_) for r in range(g)]
+            want = [x.copy() for x in grads]
+            orc.c_lp_s(want, codec=1, deltas=deltas, eps=eps)
+            t = torch.as_tensor(grads[rank]).cuda()
+            b2.c_lp_s(ep, 0.0, t, U8, es, bucket=bucket)
+            ck.eq(f"c_lp_s+EC n={n} round={t_} x", t.cpu().numpy(), want[rank])
+            ck.eq(f"c_lp_s+EC n={n} round={t_} delta", es.delta.cpu().numpy(), deltas[rank])
+            ck.eq(f"c_lp_s+EC n={n} round={t_} eps", es.epsilon.cpu().numpy(), eps[rank])
+
+    # ---- interleaved buckets, non-blocking issue, one sync (overlap of buckets)
+    bucket += 1
+    n = 300_001
+    xs = [[orc.synth(n, 50 + 10 * b + r) for r in range(g)] for b in range(3)]
+    ts = [torch.as_tensor(xs[b][rank]).cuda() for b in range(3)]
+    for b in range(3):
+        b2.c_lp_s(ep, 0.0, ts[b], U8, None, bucket=bucket + b, blocking=False)
+    ep.sync()
+    for b in range(3):
+        want = [x.copy() for x in xs[b]]
+        orc.c_lp_s(want, codec=1)
+        ck.eq(f"interleaved bucket {b}", ts[b].cpu().numpy(), want[rank])
+
+    # ---- large: owner-partition restatement + identical-replica digest
+    if args.large:
+        for n in (100_000_000,):
+            bucket += 10
+            t = torch.empty(n, device="cuda")
+            b2.lib.b2_fill_synthetic(t.data_ptr(), n, 2026 + rank, 0, torch.cuda.current_stream().cuda_stream)
+            b2.c_lp_s(ep, 0.0, t, U8, None, bucket=bucket)
+            lo, sz = b2.partition_range(n, g, rank)
+            parts = [orc.synth(sz, 2026 + r, lo) for r in range(g)]
+            # partition-local restatement: D(Q2((float) sum_j D(Q1(x_j|k))))
+            acc = np.zeros(sz, np.float64)
+            for p in parts:
+                l1, h1, c1 = orc.encode(p)
+                acc += orc.decode(l1, h1, c1).astype(np.float64)
+            s = acc.astype(np.float32)
+            l2, h2, c2 = orc.encode(s)
+            ck.eq(f"c_lp_s n={n} own partition", t[lo:lo + sz].cpu().numpy(), orc.decode(l2, h2, c2))
+            digest = hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest()
+            allv = [None] * g
+            dist.all_gather_object(allv, digest)
+            if len(set(allv)) != 1:
+                ck.fail.append(f"rank{rank} c_lp_s n={n}: replicas differ {allv}")
+            else:
+                ck.passed += 1
+
+    return ck, ep.launches()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--large", action="store_true")
+    args = ap.parse_args()
+    dist.init_process_group("gloo")
+    t0 = time.time()
+    try:
+        ck, launches = run(args)
+        fails, passed = ck.fail, ck.passed
+    except Exception:
+        fails, passed, launches = [f"rank{dist.get_rank()} exception: {traceback.format_exc()}"], 0, 0
+    allres = [None] * dist.get_world_size()
+    dist.all_gather_object(allres, (passed, fails, launches))
+    if dist.get_rank() == 0:
+        total_pass = sum(p for p, _, _ in allres)
+        all_fail = [f for _, fs, _ in allres for f in fs]
+        print(json.dumps({"world": dist.get_world_size(), "passed": total_pass, "failed": len(all_fail),
+                          "launches": [l for _, _, l in allres], "seconds": round(time.time() - t0, 1),
+                          "failures": all_fail[:40]}))
+    ok = all(not fs for _, fs, _ in allres)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()

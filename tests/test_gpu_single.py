@@ -1,0 +1,146 @@
+"""GPU parity of the primitives at world size 1 (one GPU), through the C ABI.
+
+g = 1 still runs the whole C_LP_S pipeline (both quantizations,
+collectives.cpp:89-90); C_FP_S leaves x untouched (collectives.cpp:49);
+D_* reduce over the singleton neighbourhood.  Bit-exact against the oracle.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2107_01499_b200 as b2  # noqa: E402
+
+
+def bits(a):
+    return np.asarray(a, np.float32).view(np.uint32)
+
+
+@pytest.fixture(scope="module")
+def ep():
+    e = b2.B200Endpoint(0, 1, 0)
+    yield e
+    e.close()
+
+
+U8 = b2.Codec(b2.CodecKind.uniform8)
+ID = b2.Codec(b2.CodecKind.identity)
+
+
+@pytest.mark.parametrize("n", [1, 5, 37, 4096, 1_000_003, 4_000_000])
+def test_c_lp_s_g1(ep, oracle, n):
+    x = oracle.synth(n, 2026)
+    want = x.copy()
+    oracle.c_lp_s([want], codec=1)
+    t = torch.as_tensor(x).cuda()
+    b2.c_lp_s(ep, 0.0, t, U8, None)
+    assert np.array_equal(bits(t.cpu().numpy()), bits(want))
+
+
+def test_c_lp_s_g1_identity_and_ec(ep, oracle):
+    n = 1001
+    x = oracle.synth(n, 7)
+    want = x.copy()
+    oracle.c_lp_s([want], codec=0)
+    t = torch.as_tensor(x).cuda()
+    b2.c_lp_s(ep, 0.0, t, ID, None, bucket=3)
+    assert np.array_equal(bits(t.cpu().numpy()), bits(want))
+    # error feedback, several rounds, state carried on the device
+    es = b2.ErrorState(n, n)
+    d_or = [np.zeros(n, np.float32)]
+    e_or = [np.zeros(n, np.float32)]
+    for r in range(5):
+        g = oracle.synth(n, 100 + r)
+        w = g.copy()
+        oracle.c_lp_s([w], codec=1, deltas=d_or, eps=e_or)
+        t = torch.as_tensor(g).cuda()
+        b2.c_lp_s(ep, 0.0, t, U8, es, bucket=4)
+        assert np.array_equal(bits(t.cpu().numpy()), bits(w))
+        assert np.array_equal(bits(es.delta.cpu().numpy()), bits(d_or[0]))
+        assert np.array_equal(bits(es.epsilon.cpu().numpy()), bits(e_or[0]))
+
+
+def test_c_fp_s_g1_untouched(ep):
+    x = np.array([-0.0, 1.0, 2.5], np.float32)
+    t = torch.as_tensor(x).cuda()
+    b2.c_fp_s(ep, 0.0, t)
+    assert np.array_equal(bits(t.cpu().numpy()), bits(x))
+
+
+def test_d_primitives_g1(ep, oracle):
+    n = 5003
+    x = oracle.synth(n, 9)
+    topo = b2.Topology(b2.TopologyKind.ring, 1, 0)
+    for mode in (b2.ReduceMode.sum, b2.ReduceMode.average):
+        t = torch.as_tensor(x).cuda()
+        b2.d_fp_s(ep, 0.0, t, topo, 0, mode)
+        assert np.array_equal(bits(t.cpu().numpy()), bits(oracle.d_fp_s_rank([x], int(mode))))
+        t = torch.as_tensor(x).cuda()
+        b2.d_lp_s(ep, 0.0, t, topo, 0, U8, mode)
+        assert np.array_equal(bits(t.cpu().numpy()), bits(oracle.d_lp_s_rank([x], 1, int(mode))))
+
+
+def test_nonfinite_bucket_raises(ep):
+    x = torch.ones(1000, device="cuda")
+    x[500] = float("nan")
+    with pytest.raises(b2.Error):
+        b2.c_lp_s(ep, 0.0, x, U8, None, bucket=9)
+    y = torch.ones(1000, device="cuda")
+    y[3] = float("inf")
+    with pytest.raises(b2.Error):
+        b2.d_lp_s(ep, 0.0, y, b2.Topology(b2.TopologyKind.ring, 1), 0, U8, b2.ReduceMode.average, bucket=9)
+
+
+def test_argument_errors(ep):
+    x = torch.ones(10, device="cuda")
+    with pytest.raises(b2.Error):
+        b2.c_lp_s(ep, 0.0, x, U8, b2.ErrorState(3, 1))  # collectives.cpp:102-107
+    with pytest.raises(b2.Error):
+        b2.d_fp_s(ep, 0.0, x, b2.Topology(b2.TopologyKind.full, 5), 0, b2.ReduceMode.sum)
+
+
+def test_host_buffer_path(ep, oracle):
+    x = oracle.synth(4099, 31)
+    want = x.copy()
+    oracle.c_lp_s([want], codec=1)
+    y = x.copy()
+    b2.c_lp_s(ep, 0.0, y, U8, None, bucket=11)  # numpy in place, staged through the GPU
+    assert np.array_equal(bits(y), bits(want))
+
+
+def test_flatten_aliasing_and_collective(ep, oracle):
+    # test_tensor.cpp:10-60 on device memory, then a collective on the arena
+    t1 = b2.FlatTensor("t1", [2], [1.0, 2.0])
+    t2 = b2.FlatTensor("t2", [1], [3.0])
+    arena = b2.BucketArena.flatten([t1, t2])
+    assert arena.size() == 3 and arena.data().cpu().tolist() == [1.0, 2.0, 3.0]
+    assert [(m.offset, m.length) for m in arena.members()] == [(0, 2), (2, 1)]
+    arena.data()[2] = 9.0
+    assert float(t2[0]) == 9.0
+    t1[1] = -4.0
+    assert float(arena.data()[1]) == -4.0
+    flat = arena.as_flat()
+    flat[0] = 11.0
+    assert float(t1[0]) == 11.0
+    with pytest.raises(b2.Error):
+        b2.BucketArena.flatten([b2.FlatTensor("x", [1], [1.0]), b2.FlatTensor("x", [1], [2.0])])
+    with pytest.raises(b2.Error):
+        b2.BucketArena.flatten([])
+    # many members (> one 64-member launch), then C_LP_S on the arena aliases back
+    rng = np.random.default_rng(99)
+    vals = [rng.uniform(-100, 100, int(rng.integers(1, 50))).astype(np.float32) for _ in range(150)]
+    ts = [b2.FlatTensor(f"p{i}", [v.size], v) for i, v in enumerate(vals)]
+    a = b2.BucketArena.flatten(ts)
+    cat = np.concatenate(vals)
+    assert np.array_equal(a.data().cpu().numpy(), cat)
+    want = cat.copy()
+    oracle.c_lp_s([want], codec=1)
+    b2.c_lp_s(ep, 0.0, a, U8, None, bucket=12)
+    off = 0
+    for t, v in zip(ts, vals):
+        assert np.array_equal(bits(t.data().cpu().numpy()), bits(want[off:off + v.size]))
+        off += v.size
