@@ -38,6 +38,7 @@ struct CentralArgs {
   size_t off_recv1, slot_stride, off_out2;
   float2* partials;             // local workspace [(kMaxRanks + 1) * grid]
   unsigned* cta_done;           // local workspace [kMaxRanks + 2]
+  unsigned* gridbar;            // local workspace [2]: consumer grid barrier
   float* scratch;               // local, owned-len y2 cache, or null (recompute)
   int* status;                  // mapped host status word
   unsigned long long timeout_ns;
@@ -58,6 +59,7 @@ struct DecentArgs {
   size_t off_dbuf;              // offset of dbuf[parity]
   float2* partials;
   unsigned* cta_done;
+  unsigned* gridbar;
   int* status;
   unsigned long long timeout_ns;
 };

@@ -134,8 +134,8 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
       cudaMemset(w->local, 0, 256) != cudaSuccess ||
       cudaMalloc(&w->partials, sizeof(float2) * (kMaxRanks + 1) * max_persistent_grid()) !=
           cudaSuccess ||
-      cudaMalloc(&w->cta_done, sizeof(unsigned) * (kMaxRanks + 2)) != cudaSuccess ||
-      cudaMemset(w->cta_done, 0, sizeof(unsigned) * (kMaxRanks + 2)) != cudaSuccess) {
+      cudaMalloc(&w->cta_done, sizeof(unsigned) * (kMaxRanks + 4)) != cudaSuccess ||
+      cudaMemset(w->cta_done, 0, sizeof(unsigned) * (kMaxRanks + 4)) != cudaSuccess) {
     set_error("window allocation of %zu bytes failed: %s", w->bytes,
               cudaGetErrorString(cudaGetLastError()));
     return fail(B2_ERR_CUDA);
@@ -387,6 +387,7 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   a.off_out2 = w->off_out2;
   a.partials = w->partials;
   a.cta_done = w->cta_done;
+  a.gridbar = w->cta_done + kMaxRanks + 2;
   a.scratch = w->scratch;
   a.status = c->status_d;
   a.timeout_ns = c->timeout_ns;
@@ -446,6 +447,7 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
   a.off_dbuf = w->off_dbuf[a.parity];
   a.partials = w->partials;
   a.cta_done = w->cta_done;
+  a.gridbar = w->cta_done + kMaxRanks + 2;
   a.status = c->status_d;
   a.timeout_ns = c->timeout_ns;
   rc = launch_decent(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity,

@@ -1,0 +1,220 @@
+// ring.cuh -- warp-specialized TMA streaming for the persistent collective
+// kernels: one producer warp issues cp.async.bulk copies (global -- local
+// HBM or a peer GPU's window over NVLink -- into shared memory) into a ring
+// of kStages x kStageBytes stages guarded by mbarriers; kConsumerWarps
+// consumer warps compute from shared memory.  Memory-level parallelism is the
+// ring size (192 KB per SM in flight), independent of register count.
+//
+// A "pass" streams an element range [s, s+n) of up to kMaxRanks equally
+// shaped sources; its 16-element-aligned body is cut into tiles of
+// tile_units * 16 elements handed to CTAs round-robin.  The (< 16 element)
+// unaligned head and tail are processed by the consumers of the last CTA
+// with plain loads.  Producer and consumers walk identical tile sequences,
+// so the ring cursor (stage, phase) stays in lock step across passes.
+#pragma once
+
+#include <cstdint>
+
+#include "b2_device.cuh"
+
+namespace b2 {
+
+constexpr int kConsumerWarps = 16;
+constexpr int kConsumers = 32 * kConsumerWarps;          // 512 consumer threads
+constexpr int kRingThreads = kConsumers + 32;             // + 1 producer warp
+constexpr int kStages = 6;
+constexpr int kStageBytes = 32768;
+constexpr int kRingSmem = 256 + kStages * kStageBytes;    // barriers + ring
+constexpr int kConsumerBar = 1;                           // named barrier id
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// global (local HBM or peer-mapped NVLink address) -> shared, completes tx on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// Order this thread's generic-proxy global writes before later async-proxy
+// (TMA) reads of the same bytes, on this or another GPU.
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync %0, %1;" ::"n"(kConsumerBar), "n"(kConsumers) : "memory");
+}
+
+struct PassDesc {
+  size_t s = 0, n = 0;                  // element range
+  int nsrc = 1, eb = 4;                 // sources, bytes per element
+  const uint8_t* base[kMaxRanks] = {};  // address of element e of source i = base[i] + eb * e
+  const unsigned long long* wait_flag = nullptr;  // producer: wait *flag >= target before loading
+  unsigned long long wait_target = 0;
+  __host__ __device__ int tile_units() const { return kStageBytes / (nsrc * 16 * eb); }
+  __host__ __device__ size_t u0() const { return (s + 15) >> 4; }
+  __host__ __device__ size_t u1() const { return (s + n) >> 4; }
+  __host__ __device__ size_t nunits() const { return u1() > u0() ? u1() - u0() : 0; }
+  __host__ __device__ size_t body_begin() const { return nunits() ? 16 * u0() : s + n; }
+  __host__ __device__ size_t body_end() const { return nunits() ? 16 * u1() : s + n; }
+};
+
+struct Ring {
+  uint64_t* full;
+  uint64_t* empty;
+  uint8_t* buf;
+  int stage = 0;
+  unsigned phase = 0;
+  bool producer;
+  int ct;  // consumer thread index 0..kConsumers-1 (producer: -1)
+  int* status;
+  unsigned long long timeout_ns;
+
+  __device__ void init(uint8_t* smem, int* st, unsigned long long to) {
+    full = reinterpret_cast<uint64_t*>(smem);
+    empty = full + kStages;
+    buf = smem + 256;
+    producer = threadIdx.x < 32;
+    ct = producer ? -1 : int(threadIdx.x) - 32;
+    status = st;
+    timeout_ns = to;
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < kStages; ++i) {
+        mbar_init(full + i, 1);
+        mbar_init(empty + i, kConsumerWarps);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  __device__ __forceinline__ void advance() {
+    if (++stage == kStages) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+
+  // Stream one pass.  consume(stage_ptr, first_element, units, tile_units)
+  // runs on every consumer thread for every tile this CTA owns.
+  template <class F>
+  __device__ void run(const PassDesc& p, F&& consume) {
+    const size_t u0 = p.u0(), nun = p.nunits();
+    const int T = p.tile_units();
+    const size_t ntiles = (nun + T - 1) / T;
+    if (producer) {
+      if ((threadIdx.x & 31) != 0) return;
+      bool waited = p.wait_flag == nullptr;
+      for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        if (!waited) {
+          wait_geq(p.wait_flag, p.wait_target, timeout_ns, status);
+          fence_proxy_async();
+          waited = true;
+        }
+        mbar_wait(empty + stage, phase ^ 1u);
+        const size_t units = (nun - t * T) < size_t(T) ? (nun - t * T) : size_t(T);
+        const unsigned bytes = unsigned(units * 16 * p.eb);
+        mbar_expect_tx(full + stage, bytes * p.nsrc);
+        uint8_t* dst = buf + size_t(stage) * kStageBytes;
+        const size_t off = size_t(p.eb) * 16 * (u0 + t * T);
+        for (int i = 0; i < p.nsrc; ++i)
+          bulk_g2s(dst + size_t(i) * T * 16 * p.eb, p.base[i] + off, bytes, full + stage);
+        advance();
+      }
+      return;
+    }
+    for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(full + stage, phase);
+      const size_t units = (nun - t * T) < size_t(T) ? (nun - t * T) : size_t(T);
+      consume(buf + size_t(stage) * kStageBytes, 16 * (u0 + t * T), units, T);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(empty + stage);
+      advance();
+    }
+  }
+
+  // Unaligned head/tail elements of a pass (consumer warp 0 of the last CTA).
+  template <class F>
+  __device__ void edges(const PassDesc& p, F&& fn) const {
+    if (producer || blockIdx.x != gridDim.x - 1 || ct >= 32) return;
+    const size_t b0 = p.body_begin(), b1 = p.body_end(), e1 = p.s + p.n;
+    for (size_t e = p.s + ct; e < b0; e += 32) fn(e);
+    for (size_t e = b1 + ct; e < e1; e += 32) fn(e);
+  }
+};
+
+// (lo, hi) over the consumer threads of the CTA; result valid in all consumers.
+__device__ __forceinline__ float2 consumer_minmax(float lo, float hi, float2* smem /*[32]*/) {
+  lo = warp_min_nan(lo);
+  hi = warp_max_nan(hi);
+  const int w = (threadIdx.x >> 5) - 1, l = threadIdx.x & 31;
+  consumer_sync();
+  if (l == 0) smem[w] = make_float2(lo, hi);
+  consumer_sync();
+  const float2 v = l < kConsumerWarps ? smem[l] : smem[0];
+  lo = warp_min_nan(v.x);
+  hi = warp_max_nan(v.y);
+  return make_float2(lo, hi);
+}
+
+// Grid-wide barrier among the CONSUMER threads of every CTA (the producer
+// warps keep prefetching across it).  ws[0] = arrival count, ws[1] = generation.
+__device__ __forceinline__ void consumer_grid_sync(unsigned* ws) {
+  __threadfence();
+  consumer_sync();
+  if (threadIdx.x == 32) {
+    volatile unsigned* gen = ws + 1;
+    const unsigned g0 = *gen;
+    if (atomicAdd(ws, 1u) == gridDim.x - 1) {
+      atomicExch(ws, 0u);
+      __threadfence();
+      atomicAdd(ws + 1, 1u);
+    } else {
+      while (*gen == g0) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  consumer_sync();
+}
+
+// Fence this CTA's (consumer) writes at system scope -- including making them
+// visible to TMA readers -- and report whether this CTA arrived last at ctr
+// (ctr is then reset for the next call).
+__device__ __forceinline__ bool consumer_arrive(unsigned* ctr, int* flag_smem) {
+  fence_proxy_async();
+  __threadfence_system();
+  consumer_sync();
+  if (threadIdx.x == 32) {
+    const unsigned old = atomicAdd(ctr, 1u);
+    const int last = old == gridDim.x - 1;
+    if (last) {
+      atomicExch(ctr, 0u);
+      __threadfence_system();
+    }
+    *flag_smem = last;
+  }
+  consumer_sync();
+  return *flag_smem != 0;
+}
+
+}  // namespace b2
