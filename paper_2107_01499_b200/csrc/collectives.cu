@@ -40,6 +40,10 @@
 // a slow neighbour is still reading.
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "b2_host.h"
 #include "collectives.cuh"
 #include "ring.cuh"
@@ -642,17 +646,25 @@ __global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
       if (a.nbrs[i] != me) red_release_sys_add(&hdr_of(a.win[a.nbrs[i]])->dreads[p], 1ull);
 }
 
+// The 192 KB ring exceeds the default 48 KB dynamic-smem limit: opt in once
+// per (kernel, device).
+cudaError_t ensure_ring_smem(const void* fn) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({fn, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingSmem);
+  if (e == cudaSuccess) done.insert({fn, dev});
+  return e;
+}
+
 template <typename K, typename A>
 int launch_ring(K kernel, const A& args, cudaStream_t s) {
   static_assert(sizeof(A) < 4000, "kernel argument block too large");
-  static unsigned long long attr_set = 0;  // per instantiation, bit per device
-  int dev = 0;
-  B2_CUDA_TRY(cudaGetDevice(&dev));
-  if (dev >= 64 || !(attr_set & (1ull << dev))) {
-    B2_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kRingSmem));
-    if (dev < 64) attr_set |= 1ull << dev;
-  }
+  B2_CUDA_TRY(ensure_ring_smem(reinterpret_cast<const void*>(kernel)));
   const int grid = sm_count();  // one persistent CTA per SM; all co-resident
   A copy = args;
   void* params[] = {&copy};
