@@ -1,0 +1,70 @@
+"""Live cross-check of the C restatement against the compiled reference
+(oracle/_ref), on inputs the fixtures do not cover.  Skipped where the
+reference library was not built (it is built from /root/reference)."""
+import numpy as np
+import pytest
+
+
+def bits(a):
+    return np.asarray(a, np.float32).view(np.uint32)
+
+
+@pytest.mark.parametrize("g", [1, 2, 3, 8])
+@pytest.mark.parametrize("n", [5, 37, 100_003])
+def test_c_primitives_match_reference(oracle, ref, g, n):
+    xs = [ref.synth(n, 2026 + r) for r in range(g)]
+    for codec in (0, 1):
+        a = [x.copy() for x in xs]
+        b = [x.copy() for x in xs]
+        oracle.c_lp_s(a, codec=codec)
+        ref.c_lp_s(b, codec=codec)
+        assert all(np.array_equal(bits(p), bits(q)) for p, q in zip(a, b))
+    a = [x.copy() for x in xs]
+    b = [x.copy() for x in xs]
+    oracle.c_fp_s(a)
+    ref.c_fp_s(b)
+    assert all(np.array_equal(bits(p), bits(q)) for p, q in zip(a, b))
+
+
+@pytest.mark.parametrize("g", [2, 4, 8])
+def test_d_primitives_match_reference(oracle, ref, g):
+    n = 50_001
+    xs = [ref.synth(n, 99 + r) for r in range(g)]
+    for kind, seed in ((0, 0), (1, 5), (2, 0)):
+        for mode in (0, 1):
+            b = [x.copy() for x in xs]
+            ref.d_lp_s(b, topo_kind=kind, seed=seed, round_=2, codec=1, mode=mode)
+            c = [x.copy() for x in xs]
+            ref.d_fp_s(c, topo_kind=kind, seed=seed, round_=2, mode=mode)
+            for r in range(g):
+                nb = ref.neighbors(kind, g, seed, r, 2)
+                assert np.array_equal(bits(oracle.d_lp_s_rank([xs[j] for j in nb], 1, mode)), bits(b[r]))
+                assert np.array_equal(bits(oracle.d_fp_s_rank([xs[j] for j in nb], mode)), bits(c[r]))
+
+
+def test_ec_rounds_match_reference(oracle, ref):
+    g, n = 3, 1001
+    da = [np.zeros(n, np.float32) for _ in range(g)]
+    db = [np.zeros(n, np.float32) for _ in range(g)]
+    ea = [np.zeros(oracle.partition_range(n, g, r)[1], np.float32) for r in range(g)]
+    eb = [e.copy() for e in ea]
+    for t in range(5):
+        xs = [ref.synth(n, 500 + 10 * t + r) for r in range(g)]
+        a = [x.copy() for x in xs]
+        b = [x.copy() for x in xs]
+        oracle.c_lp_s(a, codec=1, deltas=da, eps=ea)
+        ref.c_lp_s(b, codec=1, deltas=db, eps=eb)
+        assert all(np.array_equal(bits(p), bits(q)) for p, q in zip(a, b))
+        assert all(np.array_equal(bits(p), bits(q)) for p, q in zip(da, db))
+        assert all(np.array_equal(bits(p), bits(q)) for p, q in zip(ea, eb))
+
+
+def test_wire_counts_match_reference(ref):
+    # bytes on the wire per worker: 2(g-1)/g * 4N for c_fp_s
+    g, n = 8, 80_000
+    xs = [ref.synth(n, r) for r in range(g)]
+    b, m = ref.c_fp_s([x.copy() for x in xs])
+    assert all(v == 2 * (g - 1) for v in m)
+    assert all(v == 4 * n * 2 * (g - 1) // g for v in b)
+    bl = ref.c_lp_s([x.copy() for x in xs], codec=1)
+    assert all(v == 2 * (g - 1) * (8 + n // g) for v in bl)
