@@ -205,6 +205,19 @@ def run_b200(args, rank: int, world: int):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ems = float(t.item())
 
+    trace = None
+    if args.trace:
+        ep.enable_trace(True)
+        barrier()
+        b2.c_lp_s(ep, 0.0, x, codec, None)
+        trace = ep.read_trace()
+        ep.enable_trace(False)
+        if world > 1:
+            allt = [None] * world
+            dist.all_gather_object(allt, trace)
+            trace = allt
+        barrier()
+
     hbm_peak, peak_kind = measured_peaks()
     hbm_b, nvl_b = algorithmic_bytes(n, g)
     t_s = ms / 1e3
@@ -247,6 +260,8 @@ def run_b200(args, rank: int, world: int):
                                           f"(reference SimCluster harness, {backend} kernels)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+        if trace is not None:
+            print(json.dumps({"phase_trace_us(median,max)": trace}), file=sys.stderr, flush=True)
     ep.close()
 
 
@@ -261,6 +276,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=25_000_000)
     ap.add_argument("--ref-sample", type=int, default=25_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--trace", action="store_true", help="print per-phase device timestamps (stderr)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes/launch from an ncu --set full capture (profiles/)")
     args = ap.parse_args()

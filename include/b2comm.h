@@ -128,6 +128,12 @@ int b2_comm_poll(b2_comm_t comm);
 int b2_comm_set_timeout_ms(b2_comm_t comm, uint64_t ms);
 /* Number of kernel launches this communicator has issued (evidence counter). */
 uint64_t b2_comm_launches(b2_comm_t comm);
+/* Phase tracing (the multi-GPU stand-in for ncu, which cannot replay kernels
+ * that rendezvous across GPUs): when enabled every primitive launch records
+ * %globaltimer stamps (ns) per CTA at its phase boundaries; read_trace copies
+ * the last launch's stamps, max_ctas x n_slots uint64 (0 = not reached). */
+int b2_comm_enable_trace(b2_comm_t comm, int on);
+int b2_comm_read_trace(b2_comm_t comm, uint64_t* out, int max_ctas, int* n_slots);
 
 /* --------------------------------------------------- the primitives
  * x: this rank's bucket (device, n floats, 16-byte aligned), updated in place.

@@ -171,6 +171,32 @@ class B200Endpoint:
     def launches(self) -> int:
         return int(lib.b2_comm_launches(self._h))
 
+    # -- phase tracing (ncu cannot replay kernels that rendezvous across GPUs)
+    TRACE_POINTS = ("start", "p1_first_minmax", "p1_first_push", "p1_done", "p2_ready", "p2_minmax",
+                    "p2_done", "p3_first", "end")
+
+    def enable_trace(self, on: bool = True) -> None:
+        check(lib.b2_comm_enable_trace(self._h, int(on)))
+
+    def read_trace(self):
+        """-> {point: (median, max) microseconds after the earliest CTA start}
+        for the last primitive launched (synchronizes the device)."""
+        import numpy as _np
+        torch.cuda.synchronize(self.device)
+        grid = torch.cuda.get_device_properties(self.device).multi_processor_count
+        buf = (C.c_uint64 * (grid * 16))()
+        n = C.c_int()
+        check(lib.b2_comm_read_trace(self._h, buf, grid, C.byref(n)))
+        t = _np.ctypeslib.as_array(buf).reshape(grid, n.value).astype(_np.float64)
+        t0 = t[:, 0].min()
+        out = {}
+        for i, name in enumerate(self.TRACE_POINTS):
+            col = t[:, i]
+            col = col[col > 0]
+            if col.size:
+                out[name] = (round(float(_np.median(col) - t0) / 1e3, 2), round(float(col.max() - t0) / 1e3, 2))
+        return out
+
     @property
     def handle(self):
         return self._h

@@ -87,6 +87,11 @@ __device__ __forceinline__ float4 add0(float4 v) {  // (float)(0.0 + (double)v),
 
 __device__ __forceinline__ WinHdr* hdr_of(uint8_t* w) { return reinterpret_cast<WinHdr*>(w); }
 
+#define B2_TRACE(pt)                                                                   \
+  do {                                                                                 \
+    if (a.trace && ct == 0) a.trace[size_t(blockIdx.x) * kTraceSlots + (pt)] = globaltimer(); \
+  } while (0)
+
 // Per-CTA smem gate: the producer waits for it before streaming data that
 // other CTAs of this grid wrote in an earlier pass (after a grid barrier).
 __device__ __forceinline__ void gate_wait(volatile int* gate, int target) {
@@ -147,6 +152,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   float4* x4 = reinterpret_cast<float4*>(a.x);
   float4* dl4 = reinterpret_cast<float4*>(a.delta);
   int bad = 0;
+  B2_TRACE(kTrStart);
 
   auto xpass = [&](size_t lo, size_t sz) {
     PassDesc p;
@@ -193,6 +199,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     U8Params p1{};
     if (cons) {
       mm1 = finish_minmax(0);
+      B2_TRACE(kTrP1FirstA);
       p1 = u8_params(mm1.x, mm1.y);
       if (blockIdx.x == 0 && ct == 0 && a.n && !(finite_f(mm1.x) && finite_f(mm1.y)))
         latch(a.status, kStatusNonFinite);
@@ -232,6 +239,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       if (ct == 0) a.partials[size_t(1) * G + blockIdx.x] = mm;
       fence_proxy_async();
       const float2 mm2 = finish_minmax(1);  // includes the grid barrier
+      B2_TRACE(kTrP1Done);
       p2 = u8_params(mm2.x, mm2.y);
       if (blockIdx.x == 0 && ct == 0) {
         hdr_of(a.win[0])->hdr2 = mm2;
@@ -264,6 +272,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       a.x[e] = d2;
       if (EC) a.eps[e] = __fsub_rn(y2, d2);
     });
+    B2_TRACE(kTrEnd);
     return;
   }
 
@@ -280,6 +289,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       U8Params p{};
       if (cons) {
         const float2 mm = finish_minmax(k);
+        if (i == 0) B2_TRACE(kTrP1FirstA);
         p = u8_params(mm.x, mm.y);
         if (blockIdx.x == 0 && ct == 0) {
           hdr_of(a.win[k])->hdr1[me] = mm;  // remote 8-byte store into owner k's header
@@ -327,9 +337,11 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
         if (EC) a.delta[e] = __fsub_rn(y, y);
       });
     }
+    if (i == 0) B2_TRACE(kTrP1FirstB);
     if (cons && consumer_arrive(a.cta_done + k, &s_flag) && ct == 0)
       red_release_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);
   }
+  B2_TRACE(kTrP1Done);
 
   // ------------------------------------------------------ phase 2: owner reduce
   size_t mlo, msz;
@@ -347,6 +359,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   pf.wait_target = (unsigned long long)g * a.epoch;
   if (cons) {
     if (ct == 0) wait_geq(&mine->arrive1, pf.wait_target, a.timeout_ns, a.status);
+    B2_TRACE(kTrP2Ready);
     consumer_sync();
     if (CODEC == kU8 && ct < g) {
       const float2 h = __ldcg(&mine->hdr1[ct]);
@@ -389,6 +402,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       if (ct == 0) a.partials[size_t(kMaxRanks) * G + blockIdx.x] = mm0;
       fence_proxy_async();
       const float2 mm = finish_minmax(kMaxRanks);
+      B2_TRACE(kTrP2A);
       p = u8_params(mm.x, mm.y);
       if (blockIdx.x == 0 && ct == 0) {
         mine->hdr2 = mm;
@@ -461,9 +475,13 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     });
   }
   if (bad) latch(a.status, kStatusNonFinite);
-  if (g == 1) return;
+  if (g == 1) {
+    B2_TRACE(kTrEnd);
+    return;
+  }
   if (cons && consumer_arrive(a.cta_done + kMaxRanks, &s_flag) && ct == 0)
     st_release_sys(&mine->ready2, a.epoch);
+  B2_TRACE(kTrP2Done);
 
   // ------------------------------------------------------ phase 3: pull + decode
   for (int i = 0; i + 1 < g; ++i) {
@@ -483,6 +501,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     if (cons) {
       if (ct == 0) {
         wait_geq(&hk->ready2, a.epoch, a.timeout_ns, a.status);
+        if (i == 0) B2_TRACE(kTrP3First);
         if (CODEC == kU8) {
           const float2 h = ld_peer_f2(&hk->hdr2);
           s_lo[0] = h.x;
@@ -509,6 +528,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     }
     if (cons) consumer_sync();  // s_lo/s_step are reused by the next owner
   }
+  B2_TRACE(kTrEnd);
 }
 
 // ---------------------------------------------------------------- D_* kernel
@@ -526,6 +546,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
   uint8_t* mybuf = a.win[me] + a.off_dbuf;
   float4* x4 = reinterpret_cast<float4*>(a.x);
   int bad = 0;
+  B2_TRACE(kTrStart);
 
   PassDesc px;
   px.s = 0;
@@ -548,6 +569,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
       if (ct == 0) a.partials[blockIdx.x] = m0;
       consumer_grid_sync(a.gridbar);
       const float2 mm = reduce_partials(a.partials, G, red, ct);
+      B2_TRACE(kTrP1FirstA);
       q8 = u8_params(mm.x, mm.y);
       // the neighbours of two rounds ago must be done reading this buffer
       if (ct == 0) {
@@ -584,6 +606,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
     });
   }
   if (cons && consumer_arrive(a.cta_done + 0, &s_flag) && ct == 0) st_release_sys(&mine->dready[p], a.epoch);
+  B2_TRACE(kTrP1Done);
 
   // ----- gather: every neighbour's buffer (self included), ascending order
   PassDesc pg;
@@ -601,6 +624,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
     if (ct == 0)
       for (int i = 0; i < a.nnb; ++i)
         wait_geq(&hdr_of(a.win[a.nbrs[i]])->dready[p], a.epoch, a.timeout_ns, a.status);
+    B2_TRACE(kTrP2Ready);
     consumer_sync();
     if (CODEC == kU8 && ct < a.nnb) {
       const float2 h = ld_peer_f2(&hdr_of(a.win[a.nbrs[ct]])->dhdr[p]);
@@ -644,6 +668,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
   if (cons && consumer_arrive(a.cta_done + 1, &s_flag) && ct == 0)
     for (int i = 0; i < a.nnb; ++i)
       if (a.nbrs[i] != me) red_release_sys_add(&hdr_of(a.win[a.nbrs[i]])->dreads[p], 1ull);
+  B2_TRACE(kTrEnd);
 }
 
 // The 192 KB ring exceeds the default 48 KB dynamic-smem limit: opt in once

@@ -25,6 +25,22 @@ static_assert(sizeof(WinHdr) <= 256, "window header exceeds 256 bytes");
 
 enum Codec : int { kIdentity = 0, kU8 = 1 };
 
+// Per-CTA phase timestamps (%globaltimer, ns) written by consumer thread 0
+// when tracing is enabled -- the multi-GPU replacement for ncu, which cannot
+// replay kernels that rendezvous with other GPUs.
+constexpr int kTraceSlots = 16;
+enum TracePoint : int {
+  kTrStart = 0,
+  kTrP1FirstA = 1,   // phase 1: first chunk's (min,max) final
+  kTrP1FirstB = 2,   // phase 1: first chunk pushed
+  kTrP1Done = 3,     // phase 1: all chunks pushed (g==1: pass B done)
+  kTrP2Ready = 4,    // phase 2: all contributions arrived
+  kTrP2A = 5,        // phase 2: second (min,max) final
+  kTrP2Done = 6,     // phase 2: payload published
+  kTrP3First = 7,    // phase 3: first owner's payload ready
+  kTrEnd = 8,
+};
+
 // Centralized ScatterReduce (C_FP_S, C_LP_S).
 struct CentralArgs {
   float* x;
@@ -42,6 +58,7 @@ struct CentralArgs {
   float* scratch;               // local, owned-len y2 cache, or null (recompute)
   int* status;                  // mapped host status word
   unsigned long long timeout_ns;
+  unsigned long long* trace;    // [grid * kTraceSlots] globaltimer stamps, or null
 };
 
 // Decentralized neighbourhood reduce (D_FP_S, D_LP_S).
@@ -62,6 +79,7 @@ struct DecentArgs {
   unsigned* gridbar;
   int* status;
   unsigned long long timeout_ns;
+  unsigned long long* trace;
 };
 
 }  // namespace b2

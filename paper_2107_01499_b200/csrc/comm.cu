@@ -71,6 +71,8 @@ struct b2_comm {
   int* status_d = nullptr;
   unsigned long long timeout_ns = 20000ull * 1000000ull;
   unsigned long long launches = 0;
+  unsigned long long* trace = nullptr;  // device [max grid * kTraceSlots], when enabled
+  int trace_grid = 0;
   std::mutex mu;
 };
 
@@ -320,8 +322,34 @@ int b2_comm_destroy(b2_comm_t c) {
   DeviceGuard dg(c->device);
   cudaDeviceSynchronize();
   for (auto& kv : c->wins) free_window(c, kv.second);
+  if (c->trace) cudaFree(c->trace);
   if (c->status_h) cudaFreeHost(c->status_h);
   delete c;
+  return B2_OK;
+}
+
+int b2_comm_enable_trace(b2_comm_t c, int on) {
+  B2_REQUIRE(c, "null communicator");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  if (on && !c->trace) {
+    c->trace_grid = max_persistent_grid();
+    B2_CUDA_TRY(cudaMalloc(&c->trace, sizeof(unsigned long long) * kTraceSlots * c->trace_grid));
+    B2_CUDA_TRY(cudaMemset(c->trace, 0, sizeof(unsigned long long) * kTraceSlots * c->trace_grid));
+  } else if (!on && c->trace) {
+    cudaFree(c->trace);
+    c->trace = nullptr;
+  }
+  return B2_OK;
+}
+
+int b2_comm_read_trace(b2_comm_t c, uint64_t* out, int max_ctas, int* n_slots) {
+  B2_REQUIRE(c && out && n_slots, "null argument");
+  B2_REQUIRE(c->trace, "tracing is not enabled");
+  DeviceGuard dg(c->device);
+  const int n = std::min(max_ctas, c->trace_grid);
+  B2_CUDA_TRY(cudaMemcpy(out, c->trace, sizeof(uint64_t) * kTraceSlots * n, cudaMemcpyDeviceToHost));
+  *n_slots = kTraceSlots;
   return B2_OK;
 }
 
@@ -391,6 +419,7 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   a.scratch = w->scratch;
   a.status = c->status_d;
   a.timeout_ns = c->timeout_ns;
+  a.trace = c->trace;
   rc = launch_central(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity, delta != nullptr,
                       static_cast<cudaStream_t>(stream));
   if (rc == B2_OK) ++c->launches;
@@ -450,6 +479,7 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
   a.gridbar = w->cta_done + kMaxRanks + 2;
   a.status = c->status_d;
   a.timeout_ns = c->timeout_ns;
+  a.trace = c->trace;
   rc = launch_decent(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity,
                      static_cast<cudaStream_t>(stream));
   if (rc == B2_OK) {
