@@ -105,6 +105,8 @@ __device__ __forceinline__ float4 dequant4(uint32_t c, float lo, float step) {
 // Codec parameters from a (min, max) header (codec.cpp:61,66,106).
 struct U8Params {
   float lo, inv, step;
+  float c23;        // -(2^23 * step), exact: lets one FFMA produce fl32(q * step)
+  bool fastdec;     // c23 and (2^23 + 255) * step are finite -> dequant via FFMA
   bool degenerate;  // range == 0: all codes 0 (codec.cpp:62-64)
 };
 __device__ __forceinline__ U8Params u8_params(float lo, float hi) {
@@ -114,8 +116,31 @@ __device__ __forceinline__ U8Params u8_params(float lo, float hi) {
   p.degenerate = (range == 0.0f);
   p.inv = p.degenerate ? 0.0f : __fdiv_rn(255.0f, range);
   p.step = __fdiv_rn(range, 255.0f);
+  p.c23 = __fmul_rn(-8388608.0f, p.step);
+  p.fastdec = fabsf(p.step) < 0x1p100f;  // also false for NaN / Inf
   return p;
 }
+
+// dequant with the parameters above.  Fast form: (2^23 + q) is the magic
+// float m (PRMT only); fma(m, step, -2^23 step) = round((2^23 + q) step -
+// 2^23 step) = round(q * step) -- the exact product rounded ONCE, i.e. the
+// reference's rounded multiply -- then the rounded add.  3 ops per element.
+template <int K>
+__device__ __forceinline__ float magic_q(uint32_t codes) {
+  return __uint_as_float(__byte_perm(codes, 0x4B000000u, 0x7440 | K));
+}
+__device__ __forceinline__ float4 dequant4_fast(uint32_t c, float lo, float step, float c23) {
+  float4 r;
+  r.x = __fadd_rn(lo, __fmaf_rn(magic_q<0>(c), step, c23));
+  r.y = __fadd_rn(lo, __fmaf_rn(magic_q<1>(c), step, c23));
+  r.z = __fadd_rn(lo, __fmaf_rn(magic_q<2>(c), step, c23));
+  r.w = __fadd_rn(lo, __fmaf_rn(magic_q<3>(c), step, c23));
+  return r;
+}
+__device__ __forceinline__ float4 dequant4(uint32_t c, const U8Params& p) {
+  return p.fastdec ? dequant4_fast(c, p.lo, p.step, p.c23) : dequant4(c, p.lo, p.step);
+}
+__device__ __forceinline__ float dequant1(uint8_t q, const U8Params& p) { return dequant1(q, p.lo, p.step); }
 
 __device__ __forceinline__ float4 sub4(float4 a, float4 b) {
   return make_float4(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y), __fsub_rn(a.z, b.z),

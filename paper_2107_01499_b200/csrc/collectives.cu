@@ -46,6 +46,7 @@
 
 #include "b2_host.h"
 #include "collectives.cuh"
+#include "fold.cuh"
 #include "ring.cuh"
 
 namespace b2 {
@@ -113,34 +114,14 @@ __device__ __forceinline__ void set_eps4(float* eps, size_t e, size_t lo, float4
   p[3] = v.w;
 }
 
-// fp64 ascending fold of nsrc decoded contributions of one group
-template <int CODEC>
-__device__ __forceinline__ float4 fold_group(const uint8_t* st, int gi, int nsrc, int T, const float* lo,
-                                             const float* step) {
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  for (int j = 0; j < nsrc; ++j) {
-    float4 d;
-    if (CODEC == kU8) {
-      const uint32_t c = reinterpret_cast<const uint32_t*>(st + size_t(j) * T * 16)[gi];
-      d = dequant4(c, lo[j], step[j]);
-    } else {
-      d = reinterpret_cast<const float4*>(st + size_t(j) * T * 64)[gi];
-    }
-    a0 = __dadd_rn(a0, double(d.x));
-    a1 = __dadd_rn(a1, double(d.y));
-    a2 = __dadd_rn(a2, double(d.z));
-    a3 = __dadd_rn(a3, double(d.w));
-  }
-  return make_float4(__double2float_rn(a0), __double2float_rn(a1), __double2float_rn(a2),
-                     __double2float_rn(a3));
-}
-
 // ---------------------------------------------------------------- C_* kernel
 template <int CODEC, bool EC>
 __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float2 red[32];
   __shared__ float s_lo[kMaxRanks], s_step[kMaxRanks];
+  __shared__ SrcDec s_dec[kMaxRanks];
+  __shared__ int s_fast;
   __shared__ int s_flag;
   __shared__ volatile int s_gate;
   Ring r;
@@ -215,7 +196,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
         const uint32_t q = quantize4(y, p1.lo, p1.inv);
         const size_t e = e0 + 4 * size_t(gi);
         *reinterpret_cast<uint32_t*>(codes + e) = q;
-        const float4 d = dequant4(q, p1.lo, p1.step);
+        const float4 d = dequant4(q, p1);
         if (EC) dl4[e >> 2] = sub4(y, d);
         float4 y2 = add0(d);
         if (EC) y2 = sub4(y2, eps4(a.eps, e, 0));
@@ -258,9 +239,9 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
       for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
         const size_t e = e0 + 4 * size_t(gi);
-        float4 y2 = add0(dequant4(cs[gi], p1.lo, p1.step));
+        float4 y2 = add0(dequant4(cs[gi], p1));
         if (EC) y2 = sub4(y2, eps4(a.eps, e, 0));
-        const float4 d2 = dequant4(quantize4(y2, p2.lo, p2.inv), p2.lo, p2.step);
+        const float4 d2 = dequant4(quantize4(y2, p2.lo, p2.inv), p2);
         __stcs(x4 + (e >> 2), d2);
         if (EC) set_eps4(a.eps, e, 0, sub4(y2, d2));
       }
@@ -305,7 +286,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
           const uint32_t q = quantize4(y, p.lo, p.inv);
           const size_t e = e0 + 4 * size_t(gi);
           *reinterpret_cast<uint32_t*>(dst + (e - ebase)) = q;
-          if (EC) dl4[e >> 2] = sub4(y, dequant4(q, p.lo, p.step));
+          if (EC) dl4[e >> 2] = sub4(y, dequant4(q, p));
         }
       });
       r.edges(px, [&](size_t e) {
@@ -361,18 +342,34 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     if (ct == 0) wait_geq(&mine->arrive1, pf.wait_target, a.timeout_ns, a.status);
     B2_TRACE(kTrP2Ready);
     consumer_sync();
+    if (ct == 0) s_fast = 1;
+    consumer_sync();
     if (CODEC == kU8 && ct < g) {
       const float2 h = __ldcg(&mine->hdr1[ct]);
-      s_lo[ct] = h.x;
-      s_step[ct] = __fdiv_rn(__fsub_rn(h.y, h.x), 255.0f);
+      const U8Params q = u8_params(h.x, h.y);
+      s_dec[ct] = SrcDec{q.lo, q.step, q.c23};
+      if (!(q.fastdec && fold_fast_ok(q.lo, q.step))) s_fast = 0;
     }
     consumer_sync();
   }
+  const bool fast = s_fast != 0;
+  // pairs of aligned groups through the fold (8 fp64 chains per thread)
+  auto fold_pairs = [&](const uint8_t* st, size_t units, int T, auto&& body) {
+    const int ng = int(units * 4);
+    for (int gi = ct; gi < ng; gi += 2 * kConsumers) {
+      const int g1 = gi + kConsumers;
+      const bool has1 = g1 < ng;
+      float4 y0, y1;
+      fold2<CODEC>(g, fast, st, gi, has1 ? g1 : gi, T, s_dec, 1.0, y0, y1);
+      body(gi, y0);
+      if (has1) body(g1, y1);
+    }
+  };
   auto fold1 = [&](size_t e) -> float {
     double acc = 0.0;
     for (int j = 0; j < g; ++j) {
       const uint8_t* slot = a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride;
-      const float d = CODEC == kU8 ? dequant1(__ldcg(slot + (e - mbase)), s_lo[j], s_step[j])
+      const float d = CODEC == kU8 ? dequant1(__ldcg(slot + (e - mbase)), s_dec[j].lo, s_dec[j].step)
                                    : __ldcg(reinterpret_cast<const float*>(slot) + (e - mbase));
       acc = __dadd_rn(acc, double(d));
     }
@@ -382,13 +379,12 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   if (CODEC == kU8) {
     float lo = kInf, hi = -kInf;
     r.run(pf, [&](const uint8_t* st, size_t e0, size_t units, int T) {
-      for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
+      fold_pairs(st, units, T, [&](int gi, float4 y) {
         const size_t e = e0 + 4 * size_t(gi);
-        float4 y = fold_group<kU8>(st, gi, g, T, s_lo, s_step);
         if (EC) y = sub4(y, eps4(a.eps, e, mlo));
         if (a.scratch) *reinterpret_cast<float4*>(a.scratch + (e - mbase)) = y;
         mm_acc(lo, hi, y);
-      }
+      });
     });
     r.edges(pf, [&](size_t e) {
       float y = fold1(e);
@@ -413,7 +409,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     auto emit = [&](size_t e, float4 y) {
       const uint32_t q = quantize4(y, p.lo, p.inv);
       *reinterpret_cast<uint32_t*>(out2 + (e - mbase)) = q;
-      const float4 d = dequant4(q, p.lo, p.step);
+      const float4 d = dequant4(q, p);
       __stcs(x4 + (e >> 2), d);
       if (EC) set_eps4(a.eps, e, mlo, sub4(y, d));
     };
@@ -439,12 +435,11 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       r.edges(ps, [&](size_t e) { emit1(e, a.scratch[e - mbase]); });
     } else {
       r.run(pf, [&](const uint8_t* st, size_t e0, size_t units, int T) {
-        for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
+        fold_pairs(st, units, T, [&](int gi, float4 y) {
           const size_t e = e0 + 4 * size_t(gi);
-          float4 y = fold_group<kU8>(st, gi, g, T, s_lo, s_step);
           if (EC) y = sub4(y, eps4(a.eps, e, mlo));
           emit(e, y);
-        }
+        });
       });
       r.edges(pf, [&](size_t e) {
         float y = fold1(e);
@@ -455,15 +450,14 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   } else {
     float* outf = reinterpret_cast<float*>(out2);
     r.run(pf, [&](const uint8_t* st, size_t e0, size_t units, int T) {
-      for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
+      fold_pairs(st, units, T, [&](int gi, float4 y) {
         const size_t e = e0 + 4 * size_t(gi);
-        float4 y = fold_group<kIdentity>(st, gi, g, T, nullptr, nullptr);
         if (EC) y = sub4(y, eps4(a.eps, e, mlo));
         if (a.check_finite) bad |= !finite4(y);
         if (EC) set_eps4(a.eps, e, mlo, sub4(y, y));
         if (g > 1) *reinterpret_cast<float4*>(outf + (e - mbase)) = y;
         __stcs(x4 + (e >> 2), y);
-      }
+      });
     });
     r.edges(pf, [&](size_t e) {
       float y = fold1(e);
@@ -504,21 +498,28 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
         if (i == 0) B2_TRACE(kTrP3First);
         if (CODEC == kU8) {
           const float2 h = ld_peer_f2(&hk->hdr2);
-          s_lo[0] = h.x;
-          s_step[0] = __fdiv_rn(__fsub_rn(h.y, h.x), 255.0f);
+          const U8Params q = u8_params(h.x, h.y);
+          s_dec[0] = SrcDec{q.lo, q.step, q.c23};
+          s_fast = q.fastdec;
         }
       }
       consumer_sync();
     }
-    const float klo = s_lo[0], kstep = s_step[0];
+    const SrcDec kd = s_dec[0];
+    const bool kfast = s_fast != 0;
     const uint8_t* src = a.win[k] + a.off_out2;
     if (CODEC == kU8) {
       r.run(pp, [&](const uint8_t* st, size_t e0, size_t units, int) {
         const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
-        for (int gi = ct; gi < int(units * 4); gi += kConsumers)
-          __stcs(x4 + ((e0 >> 2) + gi), dequant4(cs[gi], klo, kstep));
+        if (kfast) {
+          for (int gi = ct; gi < int(units * 4); gi += kConsumers)
+            __stcs(x4 + ((e0 >> 2) + gi), dequant4_fast(cs[gi], kd.lo, kd.step, kd.c23));
+        } else {
+          for (int gi = ct; gi < int(units * 4); gi += kConsumers)
+            __stcs(x4 + ((e0 >> 2) + gi), dequant4(cs[gi], kd.lo, kd.step));
+        }
       });
-      r.edges(pp, [&](size_t e) { a.x[e] = dequant1(__ldcg(src + (e - kbase)), klo, kstep); });
+      r.edges(pp, [&](size_t e) { a.x[e] = dequant1(__ldcg(src + (e - kbase)), kd.lo, kd.step); });
     } else {
       r.run(pp, [&](const uint8_t* st, size_t e0, size_t units, int) {
         const float4* fs = reinterpret_cast<const float4*>(st);
@@ -526,7 +527,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       });
       r.edges(pp, [&](size_t e) { a.x[e] = __ldcg(reinterpret_cast<const float*>(src) + (e - kbase)); });
     }
-    if (cons) consumer_sync();  // s_lo/s_step are reused by the next owner
+    if (cons) consumer_sync();  // s_dec/s_fast are reused by the next owner
   }
   B2_TRACE(kTrEnd);
 }
@@ -536,7 +537,8 @@ template <int CODEC>
 __global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float2 red[32];
-  __shared__ float s_lo[kMaxRanks], s_step[kMaxRanks];
+  __shared__ SrcDec s_dec[kMaxRanks];
+  __shared__ int s_fast;
   __shared__ int s_flag;
   Ring r;
   r.init(smem, a.status, a.timeout_ns);
@@ -625,39 +627,34 @@ __global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
       for (int i = 0; i < a.nnb; ++i)
         wait_geq(&hdr_of(a.win[a.nbrs[i]])->dready[p], a.epoch, a.timeout_ns, a.status);
     B2_TRACE(kTrP2Ready);
+    if (ct == 0) s_fast = 1;
     consumer_sync();
     if (CODEC == kU8 && ct < a.nnb) {
       const float2 h = ld_peer_f2(&hdr_of(a.win[a.nbrs[ct]])->dhdr[p]);
-      s_lo[ct] = h.x;
-      s_step[ct] = __fdiv_rn(__fsub_rn(h.y, h.x), 255.0f);
+      const U8Params q = u8_params(h.x, h.y);
+      s_dec[ct] = SrcDec{q.lo, q.step, q.c23};
+      if (!(q.fastdec && fold_fast_ok(q.lo, q.step))) s_fast = 0;
     }
     consumer_sync();
   }
   const double inv = a.inv;
+  const bool fast = s_fast != 0;
   r.run(pg, [&](const uint8_t* st, size_t e0, size_t units, int T) {
-    for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      for (int j = 0; j < a.nnb; ++j) {
-        float4 d;
-        if (CODEC == kU8)
-          d = dequant4(reinterpret_cast<const uint32_t*>(st + size_t(j) * T * 16)[gi], s_lo[j], s_step[j]);
-        else
-          d = reinterpret_cast<const float4*>(st + size_t(j) * T * 64)[gi];
-        a0 = __dadd_rn(a0, double(d.x));
-        a1 = __dadd_rn(a1, double(d.y));
-        a2 = __dadd_rn(a2, double(d.z));
-        a3 = __dadd_rn(a3, double(d.w));
-      }
-      __stcs(x4 + ((e0 >> 2) + gi),
-             make_float4(__double2float_rn(__dmul_rn(a0, inv)), __double2float_rn(__dmul_rn(a1, inv)),
-                         __double2float_rn(__dmul_rn(a2, inv)), __double2float_rn(__dmul_rn(a3, inv))));
+    const int ng = int(units * 4);
+    for (int gi = ct; gi < ng; gi += 2 * kConsumers) {
+      const int g1 = gi + kConsumers;
+      const bool has1 = g1 < ng;
+      float4 y0, y1;
+      fold2<CODEC>(a.nnb, fast, st, gi, has1 ? g1 : gi, T, s_dec, inv, y0, y1);
+      __stcs(x4 + ((e0 >> 2) + gi), y0);
+      if (has1) __stcs(x4 + ((e0 >> 2) + g1), y1);
     }
   });
   r.edges(pg, [&](size_t e) {
     double acc = 0.0;
     for (int j = 0; j < a.nnb; ++j) {
       const uint8_t* buf = a.win[a.nbrs[j]] + a.off_dbuf;
-      const float d = CODEC == kU8 ? dequant1(__ldcg(buf + e), s_lo[j], s_step[j])
+      const float d = CODEC == kU8 ? dequant1(__ldcg(buf + e), s_dec[j].lo, s_dec[j].step)
                                    : __ldcg(reinterpret_cast<const float*>(buf) + e);
       acc = __dadd_rn(acc, double(d));
     }
