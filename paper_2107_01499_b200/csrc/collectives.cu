@@ -116,7 +116,7 @@ __device__ __forceinline__ void set_eps4(float* eps, size_t e, size_t lo, float4
 
 // ---------------------------------------------------------------- C_* kernel
 template <int CODEC, bool EC>
-__global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a) {
+__global__ void __maxnreg__(120) central_kernel(CentralArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float2 red[32];
   __shared__ float s_lo[kMaxRanks], s_step[kMaxRanks];
@@ -258,6 +258,41 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   }
 
   // ------------------------------------------------------ phase 1: encode + push
+  // uint8: A(k0) | B(k0)+A(k1) | B(k1)+A(k2) | ... | B(k_last), one consumer
+  // grid barrier after each segment to finalise the next chunk's (min, max).
+  float mlo_ = kInf, mhi_ = -kInf;  // running (min, max) of the chunk in pass A
+  auto mm_consume = [&](const uint8_t* st, size_t, size_t units, int T) {
+    const float4* xs = reinterpret_cast<const float4*>(st);
+    const float4* ds = reinterpret_cast<const float4*>(st + size_t(T) * 64);
+    for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
+      float4 v = xs[gi];
+      if (EC) v = sub4(v, ds[gi]);
+      mm_acc(mlo_, mhi_, v);
+    }
+  };
+  auto mm_edges = [&](const PassDesc& p) {
+    r.edges(p, [&](size_t e) {
+      float v = a.x[e];
+      if (EC) v = __fsub_rn(v, a.delta[e]);
+      mm_acc1(mlo_, mhi_, v);
+    });
+  };
+  auto mm_publish = [&](int slot) {  // per-CTA partial of the finished pass A
+    if (cons) {
+      const float2 mm = consumer_minmax(mlo_, mhi_, red);
+      if (ct == 0) a.partials[size_t(slot) * G + blockIdx.x] = mm;
+    }
+    mlo_ = kInf;
+    mhi_ = -kInf;
+  };
+  if (CODEC == kU8) {
+    size_t lo0, sz0;
+    part_range(a.n, g, (me + 1) % g, lo0, sz0);
+    const PassDesc p0 = xpass(lo0, sz0);
+    r.run(p0, mm_consume);
+    mm_edges(p0);
+    mm_publish((me + 1) % g);
+  }
   for (int i = 0; i < g; ++i) {
     const int k = (me + 1 + i) % g;
     size_t lo, sz;
@@ -266,7 +301,6 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     uint8_t* dst = a.win[k] + a.off_recv1 + size_t(me) * a.slot_stride;
     const size_t ebase = lo & ~size_t(15);  // slot element index = e - ebase
     if (CODEC == kU8) {
-      minmax_pass(px, k);
       U8Params p{};
       if (cons) {
         const float2 mm = finish_minmax(k);
@@ -277,7 +311,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
           if (sz && !(finite_f(mm.x) && finite_f(mm.y))) latch(a.status, kStatusNonFinite);
         }
       }
-      r.run(px, [&](const uint8_t* st, size_t e0, size_t units, int T) {
+      auto push = [&](const uint8_t* st, size_t e0, size_t units, int T) {
         const float4* xs = reinterpret_cast<const float4*>(st);
         const float4* ds = reinterpret_cast<const float4*>(st + size_t(T) * 64);
         for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
@@ -288,7 +322,18 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
           *reinterpret_cast<uint32_t*>(dst + (e - ebase)) = q;
           if (EC) dl4[e >> 2] = sub4(y, dequant4(q, p));
         }
-      });
+      };
+      if (i + 1 < g) {  // B(k) interleaved with A(next chunk)
+        const int kn = (me + 2 + i) % g;
+        size_t lon, szn;
+        part_range(a.n, g, kn, lon, szn);
+        const PassDesc pn = xpass(lon, szn);
+        r.run2(px, push, pn, mm_consume);
+        mm_edges(pn);
+        mm_publish(kn);
+      } else {
+        r.run(px, push);
+      }
       r.edges(px, [&](size_t e) {
         float y = a.x[e];
         if (EC) y = __fsub_rn(y, a.delta[e]);
@@ -534,7 +579,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
 
 // ---------------------------------------------------------------- D_* kernel
 template <int CODEC>
-__global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
+__global__ void __maxnreg__(120) decent_kernel(DecentArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float2 red[32];
   __shared__ SrcDec s_dec[kMaxRanks];

@@ -153,6 +153,46 @@ struct Ring {
     }
   }
 
+  // Stream two passes with their tiles interleaved (a0 b0 a1 b1 ...), so e.g.
+  // an NVLink-bound push pass overlaps an HBM-bound min/max pass.
+  template <class FA, class FB>
+  __device__ void run2(const PassDesc& pa, FA&& fa, const PassDesc& pb, FB&& fb) {
+    const int Ta = pa.tile_units(), Tb = pb.tile_units();
+    const size_t na = (pa.nunits() + Ta - 1) / Ta, nb = (pb.nunits() + Tb - 1) / Tb;
+    const size_t ma = na > blockIdx.x ? (na - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const size_t mb = nb > blockIdx.x ? (nb - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const size_t m = ma > mb ? ma : mb;
+    for (size_t i = 0; i < m; ++i) {
+      if (i < ma) tile(pa, blockIdx.x + i * gridDim.x, fa);
+      if (i < mb) tile(pb, blockIdx.x + i * gridDim.x, fb);
+    }
+  }
+
+  // One tile of a pass (producer lane 0 issues, consumers consume).
+  template <class F>
+  __device__ __forceinline__ void tile(const PassDesc& p, size_t t, F&& consume) {
+    const size_t u0 = p.u0(), nun = p.nunits();
+    const int T = p.tile_units();
+    const size_t units = (nun - t * T) < size_t(T) ? (nun - t * T) : size_t(T);
+    if (producer) {
+      if ((threadIdx.x & 31) != 0) return;
+      mbar_wait(empty + stage, phase ^ 1u);
+      const unsigned bytes = unsigned(units * 16 * p.eb);
+      mbar_expect_tx(full + stage, bytes * p.nsrc);
+      uint8_t* dst = buf + size_t(stage) * kStageBytes;
+      const size_t off = size_t(p.eb) * 16 * (u0 + t * T);
+      for (int i = 0; i < p.nsrc; ++i)
+        bulk_g2s(dst + size_t(i) * T * 16 * p.eb, p.base[i] + off, bytes, full + stage);
+      advance();
+      return;
+    }
+    mbar_wait(full + stage, phase);
+    consume(buf + size_t(stage) * kStageBytes, 16 * (u0 + t * T), units, T);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(empty + stage);
+    advance();
+  }
+
   // Unaligned head/tail elements of a pass (consumer warp 0 of the last CTA).
   template <class F>
   __device__ void edges(const PassDesc& p, F&& fn) const {

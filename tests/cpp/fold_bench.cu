@@ -31,11 +31,14 @@ __global__ void __launch_bounds__(kRingThreads, 1) fold_kernel(const uint8_t* co
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float s_lo[kMaxRanks], s_step[kMaxRanks];
   __shared__ double s_tab[kMaxRanks * 256];
+  __shared__ SrcDec s_dec[kMaxRanks];
   Ring r;
   r.init(smem, status, 1000000000ull);
   if (threadIdx.x < kMaxRanks) {
     s_lo[threadIdx.x] = -1.0f + 0.01f * threadIdx.x;
     s_step[threadIdx.x] = __fdiv_rn(__fsub_rn(1.0f, s_lo[threadIdx.x]), 255.0f);
+    const U8Params q = u8_params(s_lo[threadIdx.x], 1.0f);
+    s_dec[threadIdx.x] = SrcDec{q.lo, q.step, q.c23};
   }
   __syncthreads();
   for (int i = threadIdx.x; i < g * 256; i += blockDim.x)
@@ -58,7 +61,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) fold_kernel(const uint8_t* co
         if (VAR == 1)
           fold_group2<kU8>(st, gi, g1, g, T, s_lo, s_step, a, b);
         else
-          fold_group2_fast<kU8>(st, gi, g1, g, T, s_lo, s_step, a, b);
+          fold2<kU8>(g, true, st, gi, g1, T, s_dec, 1.0, a, b);
         __stcs(x4 + (e0 >> 2) + gi, a);
         if (g1 != gi) __stcs(x4 + (e0 >> 2) + g1, b);
       }
