@@ -116,7 +116,7 @@ __device__ __forceinline__ void set_eps4(float* eps, size_t e, size_t lo, float4
 
 // ---------------------------------------------------------------- C_* kernel
 template <int CODEC, bool EC>
-__global__ void __maxnreg__(120) central_kernel(CentralArgs a) {
+__global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float2 red[32];
   __shared__ float s_lo[kMaxRanks], s_step[kMaxRanks];
@@ -579,7 +579,7 @@ __global__ void __maxnreg__(120) central_kernel(CentralArgs a) {
 
 // ---------------------------------------------------------------- D_* kernel
 template <int CODEC>
-__global__ void __maxnreg__(120) decent_kernel(DecentArgs a) {
+__global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float2 red[32];
   __shared__ SrcDec s_dec[kMaxRanks];

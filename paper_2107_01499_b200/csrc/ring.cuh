@@ -19,8 +19,8 @@
 
 namespace b2 {
 
-constexpr int kConsumerWarps = 16;
-constexpr int kConsumers = 32 * kConsumerWarps;          // 512 consumer threads
+constexpr int kConsumerWarps = 19;  // 20 warps = 5 per SM sub-partition at 96 regs
+constexpr int kConsumers = 32 * kConsumerWarps;          // 608 consumer threads
 constexpr int kRingThreads = kConsumers + 32;             // + 1 producer warp
 constexpr int kStages = 6;
 constexpr int kStageBytes = 32768;
