@@ -25,12 +25,14 @@
 //           its LOCAL window, decode, fold them in ascending rank order in
 //           fp64 (kernels.cpp add_f64) and round once; second (min, max),
 //           quantize, decode its own payload straight into x, publish ready2.
-//           (g >= 4 caches y2 in a scratch chunk instead of re-folding.)
+//           The fold is issue-bound, so it runs once: y2 is cached in x's own
+//           chunk (dead after phase 1) and re-streamed for the second Q.
 //  phase 3  PULL every other owner's payload with TMA from its window over
 //           NVLink, decode into x (owners visited in staggered order).
-//  g == 1   the single-term fold is exact in fp32 ((float)(0.0 + d) == d + 0.0f),
-//           so the pipeline fuses to three passes: minmax(x) | Q1(x) -> codes,
-//           minmax(D(Q1)) | D(Q2(D(Q1))) -> x  (14 N bytes of HBM traffic).
+//  g == 1   stateless: the output is a function of the first code alone
+//           (see the g == 1 branch), two passes, 12 N bytes = the algorithmic
+//           minimum.  With error feedback the single-term fold is exact in fp32
+//           ((float)(0.0 + d) == d + 0.0f) and three passes remain.
 //
 // D_* dataflow: encode (or stage) the whole bucket into my window's parity
 // buffer, publish dready; pull every neighbour's buffer (self included) with
@@ -172,8 +174,45 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     return reduce_partials(a.partials + size_t(slot) * G, G, red, ct);
   };
 
+  if (CODEC == kU8 && g == 1 && !EC) {
+    // ------------------------------------------- single rank, stateless
+    // D1(q) = lo1 + q*step1 is monotone in q and codes 0 and 255 always occur
+    // (0 at the minimum element, 255 at the maximum; all 0 when degenerate),
+    // so the second header is (D1(0), D1(qmax)) without a pass and the output
+    // D2(Q2(D1(q1))) is a function of q1 alone: two passes, 12 N bytes.
+    const PassDesc px = xpass(0, a.n);
+    minmax_pass(px, 0);
+    U8Params p1{}, p2{};
+    if (cons) {
+      const float2 mm1 = finish_minmax(0);
+      B2_TRACE(kTrP1FirstA);
+      p1 = u8_params(mm1.x, mm1.y);
+      const float lo2 = __fadd_rn(dequant1(uint8_t(0), p1), 0.0f);
+      const float hi2 = __fadd_rn(dequant1(uint8_t(p1.degenerate ? 0 : 255), p1), 0.0f);
+      p2 = u8_params(lo2, hi2);
+      if (blockIdx.x == 0 && ct == 0) {
+        hdr_of(a.win[0])->hdr1[0] = mm1;
+        hdr_of(a.win[0])->hdr2 = make_float2(lo2, hi2);
+        if (a.n && !(finite_f(mm1.x) && finite_f(mm1.y) && finite_f(lo2) && finite_f(hi2)))
+          latch(a.status, kStatusNonFinite);
+      }
+    }
+    r.run(px, [&](const uint8_t* st, size_t e0, size_t units, int) {
+      const float4* xs = reinterpret_cast<const float4*>(st);
+      for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
+        const float4 d1 = add0(dequant4(quantize4(xs[gi], p1.lo, p1.inv), p1));
+        __stcs(x4 + ((e0 >> 2) + gi), dequant4(quantize4(d1, p2.lo, p2.inv), p2));
+      }
+    });
+    r.edges(px, [&](size_t e) {
+      const float d1 = __fadd_rn(dequant1(quantize1(a.x[e], p1.lo, p1.inv), p1), 0.0f);
+      a.x[e] = dequant1(quantize1(d1, p2.lo, p2.inv), p2);
+    });
+    B2_TRACE(kTrEnd);
+    return;
+  }
   if (CODEC == kU8 && g == 1) {
-    // ------------------------------------------------ fused single-rank path
+    // ------------------------------------------------ single rank, error feedback
     const PassDesc px = xpass(0, a.n);
     minmax_pass(px, 0);
     float2 mm1 = make_float2(0.f, 0.f);
@@ -421,20 +460,23 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     return __double2float_rn(acc);
   };
   uint8_t* out2 = a.win[me] + a.off_out2;
+  // g >= 2: one fold pass, y2 cached in x's own chunk (the fold is issue-bound,
+  // re-reading 4N/g bytes is cheaper than re-folding N contributions)
+  const bool cache = g >= 2;
   if (CODEC == kU8) {
     float lo = kInf, hi = -kInf;
     r.run(pf, [&](const uint8_t* st, size_t e0, size_t units, int T) {
       fold_pairs(st, units, T, [&](int gi, float4 y) {
         const size_t e = e0 + 4 * size_t(gi);
         if (EC) y = sub4(y, eps4(a.eps, e, mlo));
-        if (a.scratch) *reinterpret_cast<float4*>(a.scratch + (e - mbase)) = y;
+        if (cache) x4[e >> 2] = y;  // x's own chunk is dead after phase 1: cache y2 there
         mm_acc(lo, hi, y);
       });
     });
     r.edges(pf, [&](size_t e) {
       float y = fold1(e);
       if (EC) y = __fsub_rn(y, a.eps[e - mlo]);
-      if (a.scratch) a.scratch[e - mbase] = y;
+      if (cache) a.x[e] = y;
       mm_acc1(lo, hi, y);
     });
     U8Params p{};
@@ -465,19 +507,15 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       a.x[e] = d;
       if (EC) a.eps[e - mlo] = __fsub_rn(y, d);
     };
-    if (a.scratch) {
-      PassDesc ps;
-      ps.s = mlo;
-      ps.n = msz;
-      ps.eb = 4;
+    if (cache) {
+      PassDesc ps = xpass(mlo, msz);
       ps.nsrc = 1;
-      ps.base[0] = reinterpret_cast<const uint8_t*>(a.scratch) - 4 * mbase;
       if (r.producer && (threadIdx.x & 31) == 0) gate_wait(&s_gate, 1);
       r.run(ps, [&](const uint8_t* st, size_t e0, size_t units, int) {
         const float4* ys = reinterpret_cast<const float4*>(st);
         for (int gi = ct; gi < int(units * 4); gi += kConsumers) emit(e0 + 4 * size_t(gi), ys[gi]);
       });
-      r.edges(ps, [&](size_t e) { emit1(e, a.scratch[e - mbase]); });
+      r.edges(ps, [&](size_t e) { emit1(e, a.x[e]); });
     } else {
       r.run(pf, [&](const uint8_t* st, size_t e0, size_t units, int T) {
         fold_pairs(st, units, T, [&](int gi, float4 y) {

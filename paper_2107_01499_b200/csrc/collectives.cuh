@@ -55,7 +55,6 @@ struct CentralArgs {
   float2* partials;             // local workspace [(kMaxRanks + 1) * grid]
   unsigned* cta_done;           // local workspace [kMaxRanks + 2]
   unsigned* gridbar;            // local workspace [2]: consumer grid barrier
-  float* scratch;               // local, owned-len y2 cache, or null (recompute)
   int* status;                  // mapped host status word
   unsigned long long timeout_ns;
   unsigned long long* trace;    // [grid * kTraceSlots] globaltimer stamps, or null

@@ -47,7 +47,6 @@ struct Window {
   unsigned long long exp_reads[2] = {0, 0};
   float2* partials = nullptr;
   unsigned* cta_done = nullptr;
-  float* scratch = nullptr;
 };
 
 struct Blob {  // what each rank publishes about one window
@@ -97,7 +96,6 @@ void free_window(b2_comm* c, Window* w) {
   if (w->local) cudaFree(w->local);
   if (w->partials) cudaFree(w->partials);
   if (w->cta_done) cudaFree(w->cta_done);
-  if (w->scratch) cudaFree(w->scratch);
   delete w;
   (void)c;
 }
@@ -141,15 +139,6 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
     set_error("window allocation of %zu bytes failed: %s", w->bytes,
               cudaGetErrorString(cudaGetLastError()));
     return fail(B2_ERR_CUDA);
-  }
-  // Cache the owner's y2 in scratch when that costs fewer HBM bytes than
-  // re-folding the g contributions (4N/g written+read vs N re-read): g >= 4.
-  if (family == kCentral && elem == 1 && g >= 4) {
-    const size_t maxchunk = (n + g - 1) / g;
-    if (cudaMalloc(&w->scratch, sizeof(float) * (maxchunk + 8)) != cudaSuccess) {
-      set_error("scratch allocation failed");
-      return fail(B2_ERR_CUDA);
-    }
   }
   if (cudaDeviceSynchronize() != cudaSuccess) {
     set_error("window init failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -416,7 +405,6 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   a.partials = w->partials;
   a.cta_done = w->cta_done;
   a.gridbar = w->cta_done + kMaxRanks + 2;
-  a.scratch = w->scratch;
   a.status = c->status_d;
   a.timeout_ns = c->timeout_ns;
   a.trace = c->trace;

@@ -144,3 +144,34 @@ def test_flatten_aliasing_and_collective(ep, oracle):
     for t, v in zip(ts, vals):
         assert np.array_equal(bits(t.data().cpu().numpy()), bits(want[off:off + v.size]))
         off += v.size
+
+
+@pytest.mark.parametrize("case", ["constant", "two_levels", "tiny_range", "signed_zeros", "huge_finite",
+                                  "overflow_range", "subnormal"])
+def test_c_lp_s_g1_edge_inputs(ep, oracle, case):
+    """Edge inputs for the single-rank path (its second header is derived
+    from the first, so degenerate / extreme ranges are pinned explicitly)."""
+    n = 4099
+    rng = np.random.default_rng(7)
+    x = {
+        "constant": np.full(n, 3.25, np.float32),
+        "two_levels": np.where(rng.random(n) < 0.5, -1.5, 2.0).astype(np.float32),
+        "tiny_range": (1.0 + rng.random(n) * 1e-6).astype(np.float32),
+        "signed_zeros": np.where(rng.random(n) < 0.5, 0.0, -0.0).astype(np.float32),
+        "huge_finite": (rng.standard_normal(n) * 1e37).astype(np.float32),
+        "overflow_range": np.where(rng.random(n) < 0.5, -3e38, 3e38).astype(np.float32),
+        "subnormal": (rng.standard_normal(n) * 1e-40).astype(np.float32),
+    }[case]
+    want = x.copy()
+    try:
+        oracle.c_lp_s([want], codec=1)
+        ref_err = False
+    except ValueError:
+        ref_err = True
+    t = torch.as_tensor(x).cuda()
+    if ref_err:
+        with pytest.raises(b2.Error):
+            b2.c_lp_s(ep, 0.0, t, U8, None, bucket=20)
+    else:
+        b2.c_lp_s(ep, 0.0, t, U8, None, bucket=20)
+        assert np.array_equal(bits(t.cpu().numpy()), bits(want))
