@@ -173,14 +173,15 @@ class B200Endpoint:
 
     # -- phase tracing (ncu cannot replay kernels that rendezvous across GPUs)
     TRACE_POINTS = ("start", "p1_first_minmax", "p1_first_push", "p1_done", "p2_ready", "p2_minmax",
-                    "p2_done", "p3_first", "end")
+                    "p2_done", "p3_first", "end", "p2_pass", "p2_fproxy", "p2_fgpu", "p2_sync")
 
     def enable_trace(self, on: bool = True) -> None:
         check(lib.b2_comm_enable_trace(self._h, int(on)))
 
-    def read_trace(self):
+    def read_trace(self, raw: bool = False):
         """-> {point: (median, max) microseconds after the earliest CTA start}
-        for the last primitive launched (synchronizes the device)."""
+        for the last primitive launched (synchronizes the device); raw=True
+        returns the [CTA, point] array in microseconds instead."""
         import numpy as _np
         torch.cuda.synchronize(self.device)
         grid = torch.cuda.get_device_properties(self.device).multi_processor_count
@@ -189,6 +190,8 @@ class B200Endpoint:
         check(lib.b2_comm_read_trace(self._h, buf, grid, C.byref(n)))
         t = _np.ctypeslib.as_array(buf).reshape(grid, n.value).astype(_np.float64)
         t0 = t[:, 0].min()
+        if raw:
+            return _np.where(t > 0, (t - t0) / 1e3, _np.nan)
         out = {}
         for i, name in enumerate(self.TRACE_POINTS):
             col = t[:, i]

@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       });
     }
     if (i == 0) B2_TRACE(kTrP1FirstB);
-    if (cons && consumer_arrive(a.cta_done + k, &s_flag) && ct == 0)
+    if (cons && consumer_arrive<true>(a.cta_done + k, &s_flag) && ct == 0)
       red_release_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);
   }
   B2_TRACE(kTrP1Done);
@@ -463,6 +463,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   // g >= 2: one fold pass, y2 cached in x's own chunk (the fold is issue-bound,
   // re-reading 4N/g bytes is cheaper than re-folding N contributions)
   const bool cache = g >= 2;
+  U8Params own{};  // parameters of the owner's phase-2 payload (decoded in phase 3)
   if (CODEC == kU8) {
     float lo = kInf, hi = -kInf;
     r.run(pf, [&](const uint8_t* st, size_t e0, size_t units, int T) {
@@ -493,43 +494,28 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       }
       if (ct == 0) s_gate = 1;
     }
+    // second Q: only the payload is written here, so ready2 can be published
+    // as early as possible; the owner's own chunk of x is decoded from it in
+    // phase 3, in the shadow of the NVLink pulls.
     auto emit = [&](size_t e, float4 y) {
       const uint32_t q = quantize4(y, p.lo, p.inv);
       *reinterpret_cast<uint32_t*>(out2 + (e - mbase)) = q;
-      const float4 d = dequant4(q, p);
-      __stcs(x4 + (e >> 2), d);
-      if (EC) set_eps4(a.eps, e, mlo, sub4(y, d));
+      if (EC) set_eps4(a.eps, e, mlo, sub4(y, dequant4(q, p)));
     };
     auto emit1 = [&](size_t e, float y) {
       const uint8_t q = quantize1(y, p.lo, p.inv);
       out2[e - mbase] = q;
-      const float d = dequant1(q, p.lo, p.step);
-      a.x[e] = d;
-      if (EC) a.eps[e - mlo] = __fsub_rn(y, d);
+      if (EC) a.eps[e - mlo] = __fsub_rn(y, dequant1(q, p.lo, p.step));
     };
-    if (cache) {
-      PassDesc ps = xpass(mlo, msz);
-      ps.nsrc = 1;
-      if (r.producer && (threadIdx.x & 31) == 0) gate_wait(&s_gate, 1);
-      r.run(ps, [&](const uint8_t* st, size_t e0, size_t units, int) {
-        const float4* ys = reinterpret_cast<const float4*>(st);
-        for (int gi = ct; gi < int(units * 4); gi += kConsumers) emit(e0 + 4 * size_t(gi), ys[gi]);
-      });
-      r.edges(ps, [&](size_t e) { emit1(e, a.x[e]); });
-    } else {
-      r.run(pf, [&](const uint8_t* st, size_t e0, size_t units, int T) {
-        fold_pairs(st, units, T, [&](int gi, float4 y) {
-          const size_t e = e0 + 4 * size_t(gi);
-          if (EC) y = sub4(y, eps4(a.eps, e, mlo));
-          emit(e, y);
-        });
-      });
-      r.edges(pf, [&](size_t e) {
-        float y = fold1(e);
-        if (EC) y = __fsub_rn(y, a.eps[e - mlo]);
-        emit1(e, y);
-      });
-    }
+    PassDesc ps = xpass(mlo, msz);  // the y2 cached in x's own chunk
+    ps.nsrc = 1;
+    if (r.producer && (threadIdx.x & 31) == 0) gate_wait(&s_gate, 1);
+    r.run(ps, [&](const uint8_t* st, size_t e0, size_t units, int) {
+      const float4* ys = reinterpret_cast<const float4*>(st);
+      for (int gi = ct; gi < int(units * 4); gi += kConsumers) emit(e0 + 4 * size_t(gi), ys[gi]);
+    });
+    r.edges(ps, [&](size_t e) { emit1(e, a.x[e]); });
+    own = p;
   } else {
     float* outf = reinterpret_cast<float*>(out2);
     r.run(pf, [&](const uint8_t* st, size_t e0, size_t units, int T) {
@@ -538,8 +524,10 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
         if (EC) y = sub4(y, eps4(a.eps, e, mlo));
         if (a.check_finite) bad |= !finite4(y);
         if (EC) set_eps4(a.eps, e, mlo, sub4(y, y));
-        if (g > 1) *reinterpret_cast<float4*>(outf + (e - mbase)) = y;
-        __stcs(x4 + (e >> 2), y);
+        if (g > 1)
+          *reinterpret_cast<float4*>(outf + (e - mbase)) = y;
+        else
+          __stcs(x4 + (e >> 2), y);
       });
     });
     r.edges(pf, [&](size_t e) {
@@ -547,8 +535,10 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       if (EC) y = __fsub_rn(y, a.eps[e - mlo]);
       if (a.check_finite) bad |= !finite_f(y);
       if (EC) a.eps[e - mlo] = __fsub_rn(y, y);
-      if (g > 1) outf[e - mbase] = y;
-      a.x[e] = y;
+      if (g > 1)
+        outf[e - mbase] = y;
+      else
+        a.x[e] = y;
     });
   }
   if (bad) latch(a.status, kStatusNonFinite);
@@ -556,7 +546,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     B2_TRACE(kTrEnd);
     return;
   }
-  if (cons && consumer_arrive(a.cta_done + kMaxRanks, &s_flag) && ct == 0)
+  B2_TRACE(kTrP2Pass);
+  if (cons && consumer_arrive<false>(a.cta_done + kMaxRanks, &s_flag, a.trace ? a.trace + size_t(blockIdx.x) * kTraceSlots + 10 : nullptr) && ct == 0)
     st_release_sys(&mine->ready2, a.epoch);
   B2_TRACE(kTrP2Done);
 
@@ -591,8 +582,17 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     const SrcDec kd = s_dec[0];
     const bool kfast = s_fast != 0;
     const uint8_t* src = a.win[k] + a.off_out2;
+    // the owner's own payload, decoded into x's own chunk (first owner only)
+    PassDesc po;
+    po.s = mlo;
+    po.n = i == 0 ? msz : 0;
+    po.eb = pp.eb;
+    po.nsrc = 1;
+    po.base[0] = out2 - size_t(po.eb) * mbase;
+    po.wait_flag = &mine->ready2;  // every CTA's payload writes are fenced
+    po.wait_target = a.epoch;
     if (CODEC == kU8) {
-      r.run(pp, [&](const uint8_t* st, size_t e0, size_t units, int) {
+      auto pull = [&](const uint8_t* st, size_t e0, size_t units, int) {
         const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
         if (kfast) {
           for (int gi = ct; gi < int(units * 4); gi += kConsumers)
@@ -601,14 +601,22 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
           for (int gi = ct; gi < int(units * 4); gi += kConsumers)
             __stcs(x4 + ((e0 >> 2) + gi), dequant4(cs[gi], kd.lo, kd.step));
         }
-      });
+      };
+      auto mine_dec = [&](const uint8_t* st, size_t e0, size_t units, int) {
+        const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
+        for (int gi = ct; gi < int(units * 4); gi += kConsumers) __stcs(x4 + ((e0 >> 2) + gi), dequant4(cs[gi], own));
+      };
+      r.run2(pp, pull, po, mine_dec);
       r.edges(pp, [&](size_t e) { a.x[e] = dequant1(__ldcg(src + (e - kbase)), kd.lo, kd.step); });
+      r.edges(po, [&](size_t e) { a.x[e] = dequant1(__ldcg(out2 + (e - mbase)), own.lo, own.step); });
     } else {
-      r.run(pp, [&](const uint8_t* st, size_t e0, size_t units, int) {
+      auto pull = [&](const uint8_t* st, size_t e0, size_t units, int) {
         const float4* fs = reinterpret_cast<const float4*>(st);
         for (int gi = ct; gi < int(units * 4); gi += kConsumers) __stcs(x4 + ((e0 >> 2) + gi), fs[gi]);
-      });
+      };
+      r.run2(pp, pull, po, pull);
       r.edges(pp, [&](size_t e) { a.x[e] = __ldcg(reinterpret_cast<const float*>(src) + (e - kbase)); });
+      r.edges(po, [&](size_t e) { a.x[e] = __ldcg(reinterpret_cast<const float*>(out2) + (e - mbase)); });
     }
     if (cons) consumer_sync();  // s_dec/s_fast are reused by the next owner
   }
@@ -690,7 +698,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
       if (a.check_finite) bad |= !finite_f(a.x[e]);
     });
   }
-  if (cons && consumer_arrive(a.cta_done + 0, &s_flag) && ct == 0) st_release_sys(&mine->dready[p], a.epoch);
+  if (cons && consumer_arrive<false>(a.cta_done + 0, &s_flag) && ct == 0) st_release_sys(&mine->dready[p], a.epoch);
   B2_TRACE(kTrP1Done);
 
   // ----- gather: every neighbour's buffer (self included), ascending order
@@ -745,7 +753,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
   });
   if (bad) latch(a.status, kStatusNonFinite);
   // ----- acknowledge the reads so each neighbour may reuse its buffer
-  if (cons && consumer_arrive(a.cta_done + 1, &s_flag) && ct == 0)
+  if (cons && consumer_arrive<false>(a.cta_done + 1, &s_flag) && ct == 0)
     for (int i = 0; i < a.nnb; ++i)
       if (a.nbrs[i] != me) red_release_sys_add(&hdr_of(a.win[a.nbrs[i]])->dreads[p], 1ull);
   B2_TRACE(kTrEnd);

@@ -39,6 +39,7 @@ enum TracePoint : int {
   kTrP2Done = 6,     // phase 2: payload published
   kTrP3First = 7,    // phase 3: first owner's payload ready
   kTrEnd = 8,
+  kTrP2Pass = 9,     // phase 2: second pass done, before the publication fence
 };
 
 // Centralized ScatterReduce (C_FP_S, C_LP_S).

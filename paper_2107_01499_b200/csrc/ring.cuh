@@ -162,20 +162,27 @@ struct Ring {
     const size_t ma = na > blockIdx.x ? (na - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     const size_t mb = nb > blockIdx.x ? (nb - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     const size_t m = ma > mb ? ma : mb;
+    bool wa = pa.wait_flag == nullptr, wb = pb.wait_flag == nullptr;
     for (size_t i = 0; i < m; ++i) {
-      if (i < ma) tile(pa, blockIdx.x + i * gridDim.x, fa);
-      if (i < mb) tile(pb, blockIdx.x + i * gridDim.x, fb);
+      if (i < ma) tile(pa, blockIdx.x + i * gridDim.x, fa, wa);
+      if (i < mb) tile(pb, blockIdx.x + i * gridDim.x, fb, wb);
     }
   }
 
-  // One tile of a pass (producer lane 0 issues, consumers consume).
+  // One tile of a pass (producer lane 0 issues, consumers consume).  The
+  // producer honours the pass's wait flag before its first tile (`waited`).
   template <class F>
-  __device__ __forceinline__ void tile(const PassDesc& p, size_t t, F&& consume) {
+  __device__ __forceinline__ void tile(const PassDesc& p, size_t t, F&& consume, bool& waited) {
     const size_t u0 = p.u0(), nun = p.nunits();
     const int T = p.tile_units();
     const size_t units = (nun - t * T) < size_t(T) ? (nun - t * T) : size_t(T);
     if (producer) {
       if ((threadIdx.x & 31) != 0) return;
+      if (!waited) {
+        wait_geq(p.wait_flag, p.wait_target, timeout_ns, status);
+        fence_proxy_async();
+        waited = true;
+      }
       mbar_wait(empty + stage, phase ^ 1u);
       const unsigned bytes = unsigned(units * 16 * p.eb);
       mbar_expect_tx(full + stage, bytes * p.nsrc);
@@ -237,20 +244,33 @@ __device__ __forceinline__ void consumer_grid_sync(unsigned* ws) {
   consumer_sync();
 }
 
-// Fence this CTA's (consumer) writes at system scope -- including making them
-// visible to TMA readers -- and report whether this CTA arrived last at ctr
-// (ctr is then reset for the next call).
-__device__ __forceinline__ bool consumer_arrive(unsigned* ctr, int* flag_smem) {
-  fence_proxy_async();
-  __threadfence_system();
-  consumer_sync();
+// Fence this CTA's (consumer) writes and report whether this CTA arrived
+// last at ctr (ctr is then reset for the next call).  SYS = true for writes
+// that went to a PEER's memory (phase-1 pushes): they must be performed at
+// system scope before the owner is signalled.  Writes to local memory that
+// peers later read through this GPU's L2 need only gpu scope; the flag itself
+// is released at system scope by the caller.  The proxy fence makes the data
+// visible to TMA (async-proxy) readers.
+template <bool SYS>
+__device__ __forceinline__ bool consumer_arrive(unsigned* ctr, int* flag_smem,
+                                                unsigned long long* tr = nullptr) {
+  fence_proxy_async();  // every writer: generic -> async-proxy (TMA readers)
+  consumer_sync();      // all consumer writes happen-before thread 32's fence
   if (threadIdx.x == 32) {
+    if (tr) tr[0] = globaltimer();
+    // one cumulative fence per CTA (the cooperative-groups grid-sync pattern)
+    if (SYS)
+      __threadfence_system();
+    else
+      __threadfence();
+    if (tr) tr[1] = globaltimer();
     const unsigned old = atomicAdd(ctr, 1u);
     const int last = old == gridDim.x - 1;
     if (last) {
       atomicExch(ctr, 0u);
       __threadfence_system();
     }
+    if (tr) tr[2] = globaltimer();
     *flag_smem = last;
   }
   consumer_sync();

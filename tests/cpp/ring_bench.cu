@@ -87,6 +87,27 @@ float run(float* x, uint8_t* c, size_t n, float2* out, int* st, int nsm, int rep
   return ms / reps;
 }
 
+template <int MODE>
+float run_coop(float* x, uint8_t* c, size_t n, float2* out, int* st, int nsm, int reps) {
+  CK(cudaFuncSetAttribute(ring_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingSmem));
+  void* args[] = {&x, &c, &n, &out, &st};
+  auto go = [&] {
+    CK(cudaLaunchCooperativeKernel((const void*)ring_kernel<MODE>, dim3(nsm), dim3(kRingThreads), args, kRingSmem, 0));
+  };
+  go();
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  CK(cudaEventRecord(a));
+  for (int i = 0; i < reps; ++i) go();
+  CK(cudaEventRecord(b));
+  CK(cudaEventSynchronize(b));
+  float ms;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  return ms / reps;
+}
+
 int main() {
   int nsm;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
@@ -100,6 +121,10 @@ int main() {
   CK(cudaMalloc(&out, 8 * 1024));
   CK(cudaMalloc(&st, 4));
   CK(cudaMemset(x, 0, nmax * 4));
+  for (size_t n : {size_t(1000), size_t(100000000)}) {
+    printf("launch n=%zu: regular %.1f us, cooperative %.1f us\n", n, run<0>(x, c, n, out, st, nsm, 20) * 1e3,
+           run_coop<0>(x, c, n, out, st, nsm, 20) * 1e3);
+  }
   for (size_t n : {size_t(12500000), size_t(25000000), size_t(50000000), size_t(100000000)}) {
     const double mb = n * 4.0 / 1e6;
     float t0 = run<0>(x, c, n, out, st, nsm, 10);
