@@ -197,7 +197,9 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
           latch(a.status, kStatusNonFinite);
       }
     }
-    r.run(px, [&](const uint8_t* st, size_t e0, size_t units, int) {
+    PassDesc pb = px;
+    pb.reverse = true;  // the tail of x that pass A just read is still in L2
+    r.run(pb, [&](const uint8_t* st, size_t e0, size_t units, int) {
       const float4* xs = reinterpret_cast<const float4*>(st);
       for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
         const float4 d1 = add0(dequant4(quantize4(xs[gi], p1.lo, p1.inv), p1));
@@ -336,7 +338,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     const int k = (me + 1 + i) % g;
     size_t lo, sz;
     part_range(a.n, g, k, lo, sz);
-    const PassDesc px = xpass(lo, sz);
+    PassDesc px = xpass(lo, sz);
+    px.reverse = CODEC == kU8;  // re-read chunk k backwards: its tail is L2-resident
     uint8_t* dst = a.win[k] + a.off_recv1 + size_t(me) * a.slot_stride;
     const size_t ebase = lo & ~size_t(15);  // slot element index = e - ebase
     if (CODEC == kU8) {
@@ -509,6 +512,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     };
     PassDesc ps = xpass(mlo, msz);  // the y2 cached in x's own chunk
     ps.nsrc = 1;
+    ps.reverse = true;
     if (r.producer && (threadIdx.x & 31) == 0) gate_wait(&s_gate, 1);
     r.run(ps, [&](const uint8_t* st, size_t e0, size_t units, int) {
       const float4* ys = reinterpret_cast<const float4*>(st);

@@ -72,6 +72,8 @@ struct PassDesc {
   const uint8_t* base[kMaxRanks] = {};  // address of element e of source i = base[i] + eb * e
   const unsigned long long* wait_flag = nullptr;  // producer: wait *flag >= target before loading
   unsigned long long wait_target = 0;
+  bool reverse = false;  // walk this CTA's tiles backwards: re-reads the tail of a
+                         // range that was streamed forwards just before from L2
   __host__ __device__ int tile_units() const { return kStageBytes / (nsrc * 16 * eb); }
   __host__ __device__ size_t u0() const { return (s + 15) >> 4; }
   __host__ __device__ size_t u1() const { return (s + n) >> 4; }
@@ -119,38 +121,14 @@ struct Ring {
   // runs on every consumer thread for every tile this CTA owns.
   template <class F>
   __device__ void run(const PassDesc& p, F&& consume) {
-    const size_t u0 = p.u0(), nun = p.nunits();
     const int T = p.tile_units();
-    const size_t ntiles = (nun + T - 1) / T;
-    if (producer) {
-      if ((threadIdx.x & 31) != 0) return;
-      bool waited = p.wait_flag == nullptr;
-      for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        if (!waited) {
-          wait_geq(p.wait_flag, p.wait_target, timeout_ns, status);
-          fence_proxy_async();
-          waited = true;
-        }
-        mbar_wait(empty + stage, phase ^ 1u);
-        const size_t units = (nun - t * T) < size_t(T) ? (nun - t * T) : size_t(T);
-        const unsigned bytes = unsigned(units * 16 * p.eb);
-        mbar_expect_tx(full + stage, bytes * p.nsrc);
-        uint8_t* dst = buf + size_t(stage) * kStageBytes;
-        const size_t off = size_t(p.eb) * 16 * (u0 + t * T);
-        for (int i = 0; i < p.nsrc; ++i)
-          bulk_g2s(dst + size_t(i) * T * 16 * p.eb, p.base[i] + off, bytes, full + stage);
-        advance();
-      }
-      return;
-    }
-    for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      mbar_wait(full + stage, phase);
-      const size_t units = (nun - t * T) < size_t(T) ? (nun - t * T) : size_t(T);
-      consume(buf + size_t(stage) * kStageBytes, 16 * (u0 + t * T), units, T);
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive(empty + stage);
-      advance();
-    }
+    const size_t ntiles = (p.nunits() + T - 1) / T;
+    const size_t m = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    bool waited = p.wait_flag == nullptr;
+    for (size_t i = 0; i < m; ++i) tile(p, tile_index(p, i, m), consume, waited);
+  }
+  __device__ __forceinline__ size_t tile_index(const PassDesc& p, size_t i, size_t m) const {
+    return blockIdx.x + (p.reverse ? m - 1 - i : i) * gridDim.x;
   }
 
   // Stream two passes with their tiles interleaved (a0 b0 a1 b1 ...), so e.g.
@@ -164,8 +142,8 @@ struct Ring {
     const size_t m = ma > mb ? ma : mb;
     bool wa = pa.wait_flag == nullptr, wb = pb.wait_flag == nullptr;
     for (size_t i = 0; i < m; ++i) {
-      if (i < ma) tile(pa, blockIdx.x + i * gridDim.x, fa, wa);
-      if (i < mb) tile(pb, blockIdx.x + i * gridDim.x, fb, wb);
+      if (i < ma) tile(pa, tile_index(pa, i, ma), fa, wa);
+      if (i < mb) tile(pb, tile_index(pb, i, mb), fb, wb);
     }
   }
 
