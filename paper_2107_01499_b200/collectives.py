@@ -173,7 +173,8 @@ class B200Endpoint:
 
     # -- phase tracing (ncu cannot replay kernels that rendezvous across GPUs)
     TRACE_POINTS = ("start", "p1_first_minmax", "p1_first_push", "p1_done", "p2_ready", "p2_minmax",
-                    "p2_done", "p3_first", "end", "p2_pass", "p2_fproxy", "p2_fgpu", "p2_sync")
+                    "p2_done", "p3_first", "end", "p2_pass", "p1_step0", "p1_step1", "p1_step2", "p1_step3", "p1_step4",
+                    "p1_step5")
 
     def enable_trace(self, on: bool = True) -> None:
         check(lib.b2_comm_enable_trace(self._h, int(on)))

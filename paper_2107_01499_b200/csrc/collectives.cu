@@ -301,6 +301,20 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   // ------------------------------------------------------ phase 1: encode + push
   // uint8: A(k0) | B(k0)+A(k1) | B(k1)+A(k2) | ... | B(k_last), one consumer
   // grid barrier after each segment to finalise the next chunk's (min, max).
+  // Step i pushes to owner me+1+i, a permutation across ranks -- but only if
+  // the ranks stay aligned: skew lets two pushers share one owner's ingress.
+  // lockstep(i) is a light cross-rank barrier (peers post their step counter
+  // into my window header; CTAs poll locally) run before each push step.
+  auto lockstep = [&](int i) {  // consumers only
+    const unsigned long long v = (a.epoch << 4) | unsigned(i);
+    if (blockIdx.x == 0 && ct == 0)
+      for (int j = 0; j < g; ++j)
+        if (j != me) st_release_sys(&hdr_of(a.win[j])->step[me], v);
+    if (ct == 0)
+      for (int j = 0; j < g; ++j)
+        if (j != me) wait_geq(&hdr_of(a.win[me])->step[j], v, a.timeout_ns, a.status);
+    consumer_sync();
+  };
   float mlo_ = kInf, mhi_ = -kInf;  // running (min, max) of the chunk in pass A
   auto mm_consume = [&](const uint8_t* st, size_t, size_t units, int T) {
     const float4* xs = reinterpret_cast<const float4*>(st);
@@ -348,6 +362,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
         const float2 mm = finish_minmax(k);
         if (i == 0) B2_TRACE(kTrP1FirstA);
         p = u8_params(mm.x, mm.y);
+        if (g >= 3 && i + 1 < g) lockstep(i);
         if (blockIdx.x == 0 && ct == 0) {
           hdr_of(a.win[k])->hdr1[me] = mm;  // remote 8-byte store into owner k's header
           if (sz && !(finite_f(mm.x) && finite_f(mm.y))) latch(a.status, kStatusNonFinite);
@@ -406,6 +421,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       });
     }
     if (i == 0) B2_TRACE(kTrP1FirstB);
+    if (i < 6) B2_TRACE(kTrP1Step + i);
     if (cons && consumer_arrive<true>(a.cta_done + k, &s_flag) && ct == 0)
       red_release_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);
   }
@@ -466,7 +482,6 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   // g >= 2: one fold pass, y2 cached in x's own chunk (the fold is issue-bound,
   // re-reading 4N/g bytes is cheaper than re-folding N contributions)
   const bool cache = g >= 2;
-  U8Params own{};  // parameters of the owner's phase-2 payload (decoded in phase 3)
   if (CODEC == kU8) {
     float lo = kInf, hi = -kInf;
     r.run(pf, [&](const uint8_t* st, size_t e0, size_t units, int T) {
@@ -519,7 +534,6 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       for (int gi = ct; gi < int(units * 4); gi += kConsumers) emit(e0 + 4 * size_t(gi), ys[gi]);
     });
     r.edges(ps, [&](size_t e) { emit1(e, a.x[e]); });
-    own = p;
   } else {
     float* outf = reinterpret_cast<float*>(out2);
     r.run(pf, [&](const uint8_t* st, size_t e0, size_t units, int T) {
@@ -551,78 +565,76 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     return;
   }
   B2_TRACE(kTrP2Pass);
-  if (cons && consumer_arrive<false>(a.cta_done + kMaxRanks, &s_flag, a.trace ? a.trace + size_t(blockIdx.x) * kTraceSlots + 10 : nullptr) && ct == 0)
+  if (cons && consumer_arrive<false>(a.cta_done + kMaxRanks, &s_flag) && ct == 0)
     st_release_sys(&mine->ready2, a.epoch);
   B2_TRACE(kTrP2Done);
 
   // ------------------------------------------------------ phase 3: pull + decode
-  for (int i = 0; i + 1 < g; ++i) {
-    const int k = (me + 1 + i) % g;
-    size_t lo, sz;
-    part_range(a.n, g, k, lo, sz);
-    const size_t kbase = lo & ~size_t(15);
-    WinHdr* hk = hdr_of(a.win[k]);
-    PassDesc pp;
-    pp.s = lo;
-    pp.n = sz;
-    pp.eb = CODEC == kU8 ? 1 : 4;
-    pp.nsrc = 1;
-    pp.base[0] = a.win[k] + a.off_out2 - size_t(pp.eb) * kbase;
-    pp.wait_flag = &hk->ready2;
-    pp.wait_target = a.epoch;
+  // Every other owner's payload is pulled with TMA over NVLink, all owners at
+  // once with tiles interleaved round-robin (balanced fan-in whatever the rank
+  // skew), plus the owner's own payload decoded into its own chunk.
+  {
+    PassDesc pp[kMaxRanks];
+    size_t plo[kMaxRanks], pbase[kMaxRanks];
+    int powner[kMaxRanks];
+    for (int i = 0; i < g; ++i) {
+      const int k = (me + 1 + i) % g;  // i == g-1: self (local)
+      size_t lo, sz;
+      part_range(a.n, g, k, lo, sz);
+      powner[i] = k;
+      plo[i] = lo;
+      pbase[i] = lo & ~size_t(15);
+      pp[i].s = lo;
+      pp[i].n = sz;
+      pp[i].eb = CODEC == kU8 ? 1 : 4;
+      pp[i].nsrc = 1;
+      pp[i].base[0] = a.win[k] + a.off_out2 - size_t(pp[i].eb) * pbase[i];
+      pp[i].wait_flag = &hdr_of(a.win[k])->ready2;
+      pp[i].wait_target = a.epoch;
+    }
     if (cons) {
-      if (ct == 0) {
+      if (ct < g) {  // one consumer thread per owner: wait, then its header
+        const int k = powner[ct];
+        WinHdr* hk = hdr_of(a.win[k]);
         wait_geq(&hk->ready2, a.epoch, a.timeout_ns, a.status);
-        if (i == 0) B2_TRACE(kTrP3First);
         if (CODEC == kU8) {
-          const float2 h = ld_peer_f2(&hk->hdr2);
+          const float2 h = k == me ? mine->hdr2 : ld_peer_f2(&hk->hdr2);
           const U8Params q = u8_params(h.x, h.y);
-          s_dec[0] = SrcDec{q.lo, q.step, q.c23};
-          s_fast = q.fastdec;
+          s_dec[ct] = SrcDec{q.lo, q.step, q.c23};
+          s_lo[ct] = q.fastdec ? 1.0f : 0.0f;  // per-owner fast-decode flag
         }
       }
       consumer_sync();
+      B2_TRACE(kTrP3First);
     }
-    const SrcDec kd = s_dec[0];
-    const bool kfast = s_fast != 0;
-    const uint8_t* src = a.win[k] + a.off_out2;
-    // the owner's own payload, decoded into x's own chunk (first owner only)
-    PassDesc po;
-    po.s = mlo;
-    po.n = i == 0 ? msz : 0;
-    po.eb = pp.eb;
-    po.nsrc = 1;
-    po.base[0] = out2 - size_t(po.eb) * mbase;
-    po.wait_flag = &mine->ready2;  // every CTA's payload writes are fenced
-    po.wait_target = a.epoch;
     if (CODEC == kU8) {
-      auto pull = [&](const uint8_t* st, size_t e0, size_t units, int) {
+      r.run_multi(pp, g, [&](int i, const uint8_t* st, size_t e0, size_t units, int) {
         const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
-        if (kfast) {
+        const SrcDec kd = s_dec[i];
+        if (s_lo[i] != 0.0f) {
           for (int gi = ct; gi < int(units * 4); gi += kConsumers)
             __stcs(x4 + ((e0 >> 2) + gi), dequant4_fast(cs[gi], kd.lo, kd.step, kd.c23));
         } else {
           for (int gi = ct; gi < int(units * 4); gi += kConsumers)
             __stcs(x4 + ((e0 >> 2) + gi), dequant4(cs[gi], kd.lo, kd.step));
         }
-      };
-      auto mine_dec = [&](const uint8_t* st, size_t e0, size_t units, int) {
-        const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
-        for (int gi = ct; gi < int(units * 4); gi += kConsumers) __stcs(x4 + ((e0 >> 2) + gi), dequant4(cs[gi], own));
-      };
-      r.run2(pp, pull, po, mine_dec);
-      r.edges(pp, [&](size_t e) { a.x[e] = dequant1(__ldcg(src + (e - kbase)), kd.lo, kd.step); });
-      r.edges(po, [&](size_t e) { a.x[e] = dequant1(__ldcg(out2 + (e - mbase)), own.lo, own.step); });
+      });
+      for (int i = 0; i < g; ++i) {
+        const uint8_t* src = a.win[powner[i]] + a.off_out2;
+        const SrcDec kd = s_dec[i];
+        r.edges(pp[i], [&](size_t e) { a.x[e] = dequant1(__ldcg(src + (e - pbase[i])), kd.lo, kd.step); });
+      }
     } else {
-      auto pull = [&](const uint8_t* st, size_t e0, size_t units, int) {
+      r.run_multi(pp, g, [&](int, const uint8_t* st, size_t e0, size_t units, int) {
         const float4* fs = reinterpret_cast<const float4*>(st);
         for (int gi = ct; gi < int(units * 4); gi += kConsumers) __stcs(x4 + ((e0 >> 2) + gi), fs[gi]);
-      };
-      r.run2(pp, pull, po, pull);
-      r.edges(pp, [&](size_t e) { a.x[e] = __ldcg(reinterpret_cast<const float*>(src) + (e - kbase)); });
-      r.edges(po, [&](size_t e) { a.x[e] = __ldcg(reinterpret_cast<const float*>(out2) + (e - mbase)); });
+      });
+      for (int i = 0; i < g; ++i) {
+        const float* src = reinterpret_cast<const float*>(a.win[powner[i]] + a.off_out2);
+        r.edges(pp[i], [&](size_t e) { a.x[e] = __ldcg(src + (e - pbase[i])); });
+      }
     }
-    if (cons) consumer_sync();  // s_dec/s_fast are reused by the next owner
+    (void)plo;
   }
   B2_TRACE(kTrEnd);
 }

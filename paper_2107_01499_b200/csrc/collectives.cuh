@@ -17,6 +17,7 @@ struct WinHdr {
   unsigned long long dready[2]; // decentral: epoch of my published buffer, per parity
   unsigned long long dreads[2]; // decentral: #neighbour reads of my buffer completed (cumulative)
   unsigned long long pad0[2];
+  unsigned long long step[kMaxRanks];  // central: phase-1 step counter posted by rank j (lockstep)
   float2 hdr1[kMaxRanks];       // central uint8: (min,max) of my chunk as encoded by rank j
   float2 hdr2;                  // central uint8: (min,max) of my phase-2 payload
   float2 dhdr[2];               // decentral uint8: (min,max) of my bucket, per parity
@@ -40,6 +41,7 @@ enum TracePoint : int {
   kTrP3First = 7,    // phase 3: first owner's payload ready
   kTrEnd = 8,
   kTrP2Pass = 9,     // phase 2: second pass done, before the publication fence
+  kTrP1Step = 10,    // 10..15: phase-1 step i (chunk me+1+i) pushed, before its fence
 };
 
 // Centralized ScatterReduce (C_FP_S, C_LP_S).

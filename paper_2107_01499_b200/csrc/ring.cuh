@@ -147,6 +147,28 @@ struct Ring {
     }
   }
 
+  // Stream np passes with their tiles interleaved round-robin (pass 0 tile 0,
+  // pass 1 tile 0, ..., pass 0 tile 1, ...): e.g. pull every owner's payload
+  // at once, which keeps NVLink fan-in balanced whatever the rank skew.
+  template <class F>
+  __device__ void run_multi(const PassDesc* ps, int np, F&& consume) {
+    size_t mm[kMaxRanks];
+    bool w[kMaxRanks];
+    size_t m = 0;
+    for (int i = 0; i < np; ++i) {
+      const int T = ps[i].tile_units();
+      const size_t nt = (ps[i].nunits() + T - 1) / T;
+      mm[i] = nt > blockIdx.x ? (nt - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+      m = mm[i] > m ? mm[i] : m;
+      w[i] = ps[i].wait_flag == nullptr;
+    }
+    for (size_t t = 0; t < m; ++t)
+      for (int i = 0; i < np; ++i)
+        if (t < mm[i])
+          tile(ps[i], tile_index(ps[i], t, mm[i]),
+               [&](const uint8_t* st, size_t e0, size_t units, int T) { consume(i, st, e0, units, T); }, w[i]);
+  }
+
   // One tile of a pass (producer lane 0 issues, consumers consume).  The
   // producer honours the pass's wait flag before its first tile (`waited`).
   template <class F>
