@@ -301,20 +301,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   // ------------------------------------------------------ phase 1: encode + push
   // uint8: A(k0) | B(k0)+A(k1) | B(k1)+A(k2) | ... | B(k_last), one consumer
   // grid barrier after each segment to finalise the next chunk's (min, max).
-  // Step i pushes to owner me+1+i, a permutation across ranks -- but only if
-  // the ranks stay aligned: skew lets two pushers share one owner's ingress.
-  // lockstep(i) is a light cross-rank barrier (peers post their step counter
-  // into my window header; CTAs poll locally) run before each push step.
-  auto lockstep = [&](int i) {  // consumers only
-    const unsigned long long v = (a.epoch << 4) | unsigned(i);
-    if (blockIdx.x == 0 && ct == 0)
-      for (int j = 0; j < g; ++j)
-        if (j != me) st_release_sys(&hdr_of(a.win[j])->step[me], v);
-    if (ct == 0)
-      for (int j = 0; j < g; ++j)
-        if (j != me) wait_geq(&hdr_of(a.win[me])->step[j], v, a.timeout_ns, a.status);
-    consumer_sync();
-  };
+  // Step i pushes to owner me+1+i: a permutation of destinations across ranks.
   float mlo_ = kInf, mhi_ = -kInf;  // running (min, max) of the chunk in pass A
   auto mm_consume = [&](const uint8_t* st, size_t, size_t units, int T) {
     const float4* xs = reinterpret_cast<const float4*>(st);
@@ -362,7 +349,6 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
         const float2 mm = finish_minmax(k);
         if (i == 0) B2_TRACE(kTrP1FirstA);
         p = u8_params(mm.x, mm.y);
-        if (g >= 3 && i + 1 < g) lockstep(i);
         if (blockIdx.x == 0 && ct == 0) {
           hdr_of(a.win[k])->hdr1[me] = mm;  // remote 8-byte store into owner k's header
           if (sz && !(finite_f(mm.x) && finite_f(mm.y))) latch(a.status, kStatusNonFinite);

@@ -17,7 +17,6 @@ struct WinHdr {
   unsigned long long dready[2]; // decentral: epoch of my published buffer, per parity
   unsigned long long dreads[2]; // decentral: #neighbour reads of my buffer completed (cumulative)
   unsigned long long pad0[2];
-  unsigned long long step[kMaxRanks];  // central: phase-1 step counter posted by rank j (lockstep)
   float2 hdr1[kMaxRanks];       // central uint8: (min,max) of my chunk as encoded by rank j
   float2 hdr2;                  // central uint8: (min,max) of my phase-2 payload
   float2 dhdr[2];               // decentral uint8: (min,max) of my bucket, per parity
