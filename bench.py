@@ -52,9 +52,32 @@ def measured_peaks():
         return HBM_FALLBACK_GBS, "fallback"
 
 
-def algorithmic_bytes(n: int, g: int):
-    """HBM bytes 11N + N/g, NVLink ingress 2N(g-1)/g per GPU."""
-    return 11 * n + n // g, 2 * n * (g - 1) // g
+PRIMS = {  # name -> (default elements, reference time_primitive id, metric label)
+    "c_lp_s": (100_000_000, 2, "C_LP_S allreduce"),
+    "c_fp_s": (25_000_000, 1, "C_FP_S allreduce"),
+    "d_fp_s": (25_000_000, 3, "D_FP_S ring averaging"),
+    "d_lp_s": (25_000_000, 4, "D_LP_S ring averaging"),
+    "codec": (4_000_000, 0, "MinMaxUInt8 compress+decompress"),
+}
+
+
+def ring_nbrs(g: int) -> int:
+    """|N(i)| of the ring topology, self included (collectives.cpp:187-192)."""
+    return min(g, 3)
+
+
+def algorithmic_bytes(prim: str, n: int, g: int):
+    """Per-GPU algorithmic (HBM, NVLink-ingress) bytes, SURVEY.md 8d."""
+    nb = ring_nbrs(g)
+    if prim == "c_lp_s":
+        return 11 * n + n // g, 2 * n * (g - 1) // g
+    if prim == "c_fp_s":
+        return 4 * n + 4 * n // g + 8 * n * (g - 1) // g, 8 * n * (g - 1) // g
+    if prim == "d_fp_s":
+        return 4 * n * nb + 4 * n, 4 * n * (nb - 1)
+    if prim == "d_lp_s":
+        return 4 * n + n + n * nb + 4 * n, n * (nb - 1)
+    return 10 * n, 0  # codec: read x, write codes, read codes, write x
 
 
 class ClockSampler:
@@ -103,11 +126,11 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_reference_gbs(g: int, n_sample: int, reps: int):
-    """The unmodified reference (oracle/_ref) C_LP_S through its SimCluster harness."""
+def cpu_reference_gbs(prim_id: int, g: int, n_sample: int, reps: int):
+    """The unmodified reference (oracle/_ref) primitive through its SimCluster harness."""
     from oracle import Reference  # test/baseline infrastructure only
     r = Reference()
-    secs = r.time_primitive(2, g, n_sample, reps)
+    secs = r.time_primitive(prim_id, g, n_sample, reps)
     return secs, r.backend()
 
 
@@ -116,17 +139,20 @@ def run_reference(args, rank: int, world: int):
         return
     g = world
     n_sample = min(args.n, args.ref_sample)
-    secs, backend = cpu_reference_gbs(g, n_sample, args.warmup + args.steps)
+    prim_id, label = PRIMS[args.prim][1], PRIMS[args.prim][2]
+    if args.prim == "codec":
+        g = 1
+    secs, backend = cpu_reference_gbs(prim_id, g, n_sample, args.warmup + args.steps)
     timed = secs[args.warmup:] or secs
     t = statistics.median(timed)
     value = g * 4 * n_sample / t / 1e9
     line = {
-        "metric": "effective gradient GB/s for C_LP_S allreduce", "value": round(value, 4), "unit": "GB/s",
+        "metric": f"effective gradient GB/s for {label}", "value": round(value, 4), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+u8", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": f"C_LP_S uint8 (no EC) allreduce, {n_sample} fp32 elements per worker (bounded "
-                               f"sample of the {args.n}-element bucket), {g} worker threads on SimCluster",
+        "config": {"workload": f"{label}, {n_sample} fp32 elements per worker (bounded sample of the "
+                               f"{args.n}-element bucket), {g} worker threads on SimCluster",
                    "elements": n_sample, "workers": g},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": g, "kind": "reference",
                          "sample": f"{n_sample} elements x {g} workers, median of {len(timed)} calls, "
@@ -145,11 +171,35 @@ def run_b200(args, rank: int, world: int):
     torch.cuda.set_device(dev)
     g = world
     n = args.n
+    prim = args.prim
     ep = b2.B200Endpoint(rank, world, dev)
     codec = b2.Codec(b2.CodecKind.uniform8)
     stream = torch.cuda.current_stream()
     x = torch.empty(n, dtype=torch.float32, device="cuda")
     b2._lib.check(b2.lib.b2_fill_synthetic(x.data_ptr(), n, 2026 + rank, 0, stream.cuda_stream))
+    ring = b2.Topology(b2.TopologyKind.ring, g, 0)
+    if prim == "codec":  # one GPU, the standalone codec kernels
+        codes = torch.empty(n + 64, dtype=torch.uint8, device="cuda")
+        hdr = torch.empty(4, dtype=torch.float32, device="cuda")
+        launches_box = [0]
+
+    def step(buf):
+        if prim == "c_lp_s":
+            b2.c_lp_s(ep, 0.0, buf, codec, None, blocking=False)
+        elif prim == "c_fp_s":
+            b2.c_fp_s(ep, 0.0, buf, blocking=False)
+        elif prim == "d_fp_s":
+            b2.d_fp_s(ep, 0.0, buf, ring, 0, b2.ReduceMode.average, blocking=False)
+        elif prim == "d_lp_s":
+            b2.d_lp_s(ep, 0.0, buf, ring, 0, codec, b2.ReduceMode.average, blocking=False)
+        else:
+            s_ = torch.cuda.current_stream().cuda_stream
+            b2._lib.check(b2.lib.b2_u8_encode(buf.data_ptr(), n, codes.data_ptr(), hdr.data_ptr(), s_))
+            b2._lib.check(b2.lib.b2_u8_decode(codes.data_ptr(), hdr.data_ptr(), n, buf.data_ptr(), s_))
+            launches_box[0] += 4  # init keys, minmax, quantize, decode
+
+    def n_launches():
+        return launches_box[0] if prim == "codec" else ep.launches()
 
     def barrier():
         if world > 1:
@@ -158,19 +208,19 @@ def run_b200(args, rank: int, world: int):
 
     # ---------------- device-resident timing (value)
     for _ in range(args.warmup):
-        b2.c_lp_s(ep, 0.0, x, codec, None, blocking=False)
+        step(x)
     ep.sync()
-    launches0 = ep.launches()
+    launches0 = n_launches()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            b2.c_lp_s(ep, 0.0, x, codec, None, blocking=False)
+            step(x)
         ev1.record(stream)
         ev1.synchronize()
     ep.sync()
-    launches = ep.launches() - launches0
+    launches = n_launches() - launches0
     ms_local = ev0.elapsed_time(ev1) / args.steps
     ms = ms_local
     if world > 1:
@@ -185,7 +235,7 @@ def run_b200(args, rank: int, world: int):
     xd = torch.empty_like(x)
     for _ in range(max(1, args.warmup // 2)):
         xd.copy_(host, non_blocking=True)
-        b2.c_lp_s(ep, 0.0, xd, codec, None, blocking=False)
+        step(xd)
         host.copy_(xd, non_blocking=True)
     ep.sync()
     barrier()
@@ -194,7 +244,7 @@ def run_b200(args, rank: int, world: int):
     e0.record(stream)
     for _ in range(e_steps):
         xd.copy_(host, non_blocking=True)
-        b2.c_lp_s(ep, 0.0, xd, codec, None, blocking=False)
+        step(xd)
         host.copy_(xd, non_blocking=True)
     e1.record(stream)
     e1.synchronize()
@@ -206,10 +256,10 @@ def run_b200(args, rank: int, world: int):
         ems = float(t.item())
 
     trace = None
-    if args.trace:
+    if args.trace and prim != "codec":
         ep.enable_trace(True)
         barrier()
-        b2.c_lp_s(ep, 0.0, x, codec, None)
+        step(x)
         trace = ep.read_trace()
         ep.enable_trace(False)
         if world > 1:
@@ -219,7 +269,7 @@ def run_b200(args, rank: int, world: int):
         barrier()
 
     hbm_peak, peak_kind = measured_peaks()
-    hbm_b, nvl_b = algorithmic_bytes(n, g)
+    hbm_b, nvl_b = algorithmic_bytes(prim, n, g)
     t_s = ms / 1e3
     t_roof_hbm = hbm_b / (hbm_peak * 1e9)
     t_roof_nvl = nvl_b / (NVL_PEER_GBS * 1e9)
@@ -233,16 +283,22 @@ def run_b200(args, rank: int, world: int):
     roof["traffic"] = args.traffic
     roof["algorithmic_bytes"] = {"hbm": hbm_b, "nvlink_ingress": nvl_b}
     roof["t_roof_us"] = round(max(t_roof_hbm, t_roof_nvl) * 1e6, 1)
-    roof["kernel"] = "central_kernel<uint8> (one fused launch per step)"
+    roof["kernel"] = {"c_lp_s": "central_kernel<uint8> (one fused launch per step)",
+                      "c_fp_s": "central_kernel<identity> (one fused launch per step)",
+                      "d_fp_s": "decent_kernel<identity> (one fused launch per step)",
+                      "d_lp_s": "decent_kernel<uint8> (one fused launch per step)",
+                      "codec": "minmax_keys_kernel + quantize_kernel + decode_kernel"}[prim]
 
     per_gpu = 4 * n / t_s / 1e9
+    label = PRIMS[prim][2]
     line = {
-        "metric": "effective gradient GB/s for C_LP_S allreduce", "value": round(g * per_gpu, 2), "unit": "GB/s",
+        "metric": f"effective gradient GB/s for {label}", "value": round(g * per_gpu, 2), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+u8",
         "data": "synthetic (splitmix64 uniform [-1,1), seed 2026+rank)",
-        "config": {"workload": f"C_LP_S ByteGrad MinMaxUInt8 allreduce of {n} fp32 gradients per GPU (VGG16-sized), "
-                               f"g={g}", "elements_per_gpu": n, "parallelism": f"dp{g}",
+        "config": {"workload": (f"C_LP_S ByteGrad MinMaxUInt8 allreduce of {n} fp32 gradients per GPU "
+                                f"(VGG16-sized), g={g}" if prim == "c_lp_s" else f"{label} of {n} fp32 elements "
+                                f"per GPU, g={g}"), "primitive": prim, "elements_per_gpu": n, "parallelism": f"dp{g}",
                    "per_gpu_gbs": round(per_gpu, 2), "l2": "inputs 400 MB/GPU > 126 MB L2, no flush"},
         "roofline": roof,
         "e2e": {"value": round(g * 4 * n / (ems / 1e3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
@@ -250,13 +306,13 @@ def run_b200(args, rank: int, world: int):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and prim != "c_fp_s":
         n_sample = min(n, args.cpu_sample)
-        secs, backend = cpu_reference_gbs(1, n_sample, 3)
+        secs, backend = cpu_reference_gbs(PRIMS[prim][1], 1, n_sample, 3)
         tc = statistics.median(secs)
         line["cpu_baseline"] = {"value": round(4 * n_sample / tc / 1e9, 4), "unit": "GB/s", "cores": 1,
                                 "kind": "reference",
-                                "sample": f"C_LP_S g=1 over {n_sample} elements, median of 3 calls "
+                                "sample": f"{label} g=1 over {n_sample} elements, median of 3 calls "
                                           f"(reference SimCluster harness, {backend} kernels)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -271,7 +327,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=N_ELEMS)
+    ap.add_argument("--prim", default="c_lp_s", choices=sorted(PRIMS))
+    ap.add_argument("--n", type=int, default=None, help="elements per GPU (default: the BASELINE config size)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-sample", type=int, default=25_000_000)
     ap.add_argument("--ref-sample", type=int, default=25_000_000)
@@ -281,6 +338,8 @@ def main():
                     help="dram bytes/launch from an ncu --set full capture (profiles/)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.n is None:
+        args.n = PRIMS[args.prim][0]
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
