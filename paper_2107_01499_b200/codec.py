@@ -93,7 +93,7 @@ class Codec:
         n = out.numel()
         if n == 0:
             return out
-        c = codes if codes.data_ptr() % 4 == 0 else codes.clone()
+        c = codes if codes.data_ptr() % 16 == 0 else codes.clone()
         o = out if _aligned(out) and out.is_contiguous() else torch.empty_like(out)
         check(lib.b2_u8_decode(c.data_ptr(), hdr.data_ptr(), n, o.data_ptr(), _stream(out.device)))
         if o is not out:

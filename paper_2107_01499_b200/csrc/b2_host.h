@@ -34,5 +34,7 @@ void set_error(const char* fmt, ...);
 // Persistent-grid size for a kernel: SMs x resident CTAs per SM.
 int persistent_grid(const void* func, int threads, size_t smem = 0);
 int sm_count();
+// Opt a ring kernel into the 192 KB dynamic shared memory (once per device).
+cudaError_t ensure_ring_smem(const void* fn);
 
 }  // namespace b2

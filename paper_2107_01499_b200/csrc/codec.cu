@@ -16,13 +16,16 @@
 #include <mutex>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "b2_device.cuh"
 #include "b2_host.h"
+#include "ring.cuh"
 
 namespace b2 {
 namespace {
 
-constexpr int U = 4;  // 4 x 16-byte loads in flight per thread per iteration
+namespace cg = cooperative_groups;
 
 __device__ __forceinline__ unsigned key_of(float f) {
   const unsigned b = __float_as_uint(f);
@@ -32,147 +35,121 @@ __device__ __forceinline__ float float_of(unsigned k) {
   return __uint_as_float((k & 0x80000000u) ? (k ^ 0x80000000u) : ~k);
 }
 
-// Pass 1: per-CTA (min, max) of y = x (- delta), folded into keys[0..1].
+// Encode = ONE cooperative launch on the TMA ring (ring.cuh): pass A streams
+// x (- delta) and reduces a NaN-propagating (min, max) per CTA into two
+// order-preserving u32 keys (one atomicMin/atomicMax per CTA, hdr scratch
+// words); a grid barrier finalises the header; pass B re-streams x in REVERSE
+// tile order (its tail is still in L2, all of it when the chunk fits) and
+// writes 4 codes per 32-bit store (+ delta / decoded with error feedback).
 template <bool EC>
-__global__ void __launch_bounds__(kThreads) minmax_keys_kernel(const float* __restrict__ x,
-                                                               const float* __restrict__ delta,
-                                                               size_t n, unsigned* keys) {
+__global__ void __launch_bounds__(kRingThreads, 1) encode_ring_kernel(const float* __restrict__ x,
+                                                                      float* __restrict__ delta, size_t n,
+                                                                      uint8_t* __restrict__ codes, float* hdr,
+                                                                      float* __restrict__ decoded) {
+  extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float2 red[32];
-  const Span sp = make_span(0, n);
-  float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
-  const size_t stride = size_t(gridDim.x) * blockDim.x;
-  const float4* x4 = reinterpret_cast<const float4*>(x);
-  const float4* d4 = reinterpret_cast<const float4*>(delta);
-  for (size_t base = sp.g0 + size_t(blockIdx.x) * blockDim.x + threadIdx.x; base < sp.g1;
-       base += stride * U) {
-    float4 v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const size_t gi = base + u * stride;
-      if (gi < sp.g1) {
-        v[u] = ld_stream(x4 + gi);
-        if (EC) v[u] = sub4(v[u], ld_stream(d4 + gi));
-      } else {
-        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (base + u * stride < sp.g1) {
-        lo = fmin_nan(lo, fmin_nan(fmin_nan(v[u].x, v[u].y), fmin_nan(v[u].z, v[u].w)));
-        hi = fmax_nan(hi, fmax_nan(fmax_nan(v[u].x, v[u].y), fmax_nan(v[u].z, v[u].w)));
-      }
-    }
-  }
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x < 8) {  // unaligned head / tail
-    const size_t e = threadIdx.x < 4 ? sp.s + threadIdx.x : sp.tail_begin + (threadIdx.x - 4);
-    const bool in = threadIdx.x < 4 ? e < sp.head_end : e < sp.s + sp.n;
-    if (in) {
-      float v = x[e];
-      if (EC) v = __fsub_rn(v, delta[e]);
-      lo = fmin_nan(lo, v);
-      hi = fmax_nan(hi, v);
-    }
-  }
-  const float2 r = block_minmax(lo, hi, red);
-  if (threadIdx.x == 0) {
-    if (r.x != r.x || r.y != r.y) {
-      atomicMax(keys + 1, 0xffffffffu);  // NaN -> the max key decodes to NaN
-    } else {
-      atomicMin(keys + 0, key_of(r.x));
-      atomicMax(keys + 1, key_of(r.y));
-    }
-  }
-}
-
-// Pass 2: codes = Q(y); with EC also delta = y - D(Q(y)) and decoded.
-template <bool EC>
-__global__ void __launch_bounds__(kThreads) quantize_kernel(const float* __restrict__ x,
-                                                            float* __restrict__ delta, size_t n,
-                                                            uint8_t* __restrict__ codes, float* hdr,
-                                                            float* __restrict__ decoded) {
-  const unsigned* keys = reinterpret_cast<const unsigned*>(hdr + 2);
-  const float lo = float_of(__ldcg(keys + 0)), hi = float_of(__ldcg(keys + 1));
+  cg::grid_group grid = cg::this_grid();
+  Ring r;
+  r.init(smem, nullptr, 0);
+  unsigned* keys = reinterpret_cast<unsigned*>(hdr + 2);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    hdr[0] = lo;
-    hdr[1] = hi;
+    keys[0] = 0xffffffffu;
+    keys[1] = 0u;
   }
-  const U8Params p = u8_params(lo, hi);
-  const Span sp = make_span(0, n);
-  const size_t stride = size_t(gridDim.x) * blockDim.x;
-  const float4* x4 = reinterpret_cast<const float4*>(x);
-  float4* d4 = reinterpret_cast<float4*>(delta);
-  uint32_t* c4 = reinterpret_cast<uint32_t*>(codes);
-  for (size_t base = sp.g0 + size_t(blockIdx.x) * blockDim.x + threadIdx.x; base < sp.g1;
-       base += stride * U) {
-    float4 v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const size_t gi = base + u * stride;
-      if (gi < sp.g1) {
-        v[u] = ld_stream(x4 + gi);
-        if (EC) v[u] = sub4(v[u], d4[gi]);
+  grid.sync();
+  PassDesc p;
+  p.s = 0;
+  p.n = n;
+  p.eb = 4;
+  p.nsrc = EC ? 2 : 1;
+  p.base[0] = reinterpret_cast<const uint8_t*>(x);
+  if (EC) p.base[1] = reinterpret_cast<const uint8_t*>(delta);
+  const int ct = r.ct;
+  float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
+  r.run(p, [&](const uint8_t* st, size_t, size_t units, int T) {
+    const float4* xs = reinterpret_cast<const float4*>(st);
+    const float4* ds = reinterpret_cast<const float4*>(st + size_t(T) * 64);
+    for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
+      float4 v = xs[gi];
+      if (EC) v = sub4(v, ds[gi]);
+      lo = fmin_nan(lo, fmin_nan(fmin_nan(v.x, v.y), fmin_nan(v.z, v.w)));
+      hi = fmax_nan(hi, fmax_nan(fmax_nan(v.x, v.y), fmax_nan(v.z, v.w)));
+    }
+  });
+  r.edges(p, [&](size_t e) {
+    float v = x[e];
+    if (EC) v = __fsub_rn(v, delta[e]);
+    lo = fmin_nan(lo, v);
+    hi = fmax_nan(hi, v);
+  });
+  if (!r.producer) {
+    const float2 m = consumer_minmax(lo, hi, red);
+    if (ct == 0) {
+      if (m.x != m.x || m.y != m.y) {
+        atomicMax(keys + 1, 0xffffffffu);  // NaN -> the max key decodes to NaN
+      } else {
+        atomicMin(keys + 0, key_of(m.x));
+        atomicMax(keys + 1, key_of(m.y));
       }
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const size_t gi = base + u * stride;
-      if (gi < sp.g1) {
-        const uint32_t q = quantize4(v[u], p.lo, p.inv);
-        st_stream(c4 + gi, q);
-        if (EC) {
-          const float4 d = dequant4(q, p.lo, p.step);
-          d4[gi] = sub4(v[u], d);
-          if (decoded) st_stream(reinterpret_cast<float4*>(decoded) + gi, d);
-        }
-      }
-    }
   }
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x < 8) {
-    const size_t e = threadIdx.x < 4 ? sp.s + threadIdx.x : sp.tail_begin + (threadIdx.x - 4);
-    const bool in = threadIdx.x < 4 ? e < sp.head_end : e < sp.s + sp.n;
-    if (in) {
-      float v = x[e];
-      if (EC) v = __fsub_rn(v, delta[e]);
-      const uint8_t q = quantize1(v, p.lo, p.inv);
-      codes[e] = q;
+  grid.sync();
+  const float mlo = float_of(__ldcg(keys + 0)), mhi = float_of(__ldcg(keys + 1));
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    hdr[0] = mlo;
+    hdr[1] = mhi;
+  }
+  const U8Params q = u8_params(mlo, mhi);
+  p.reverse = true;
+  r.run(p, [&](const uint8_t* st, size_t e0, size_t units, int T) {
+    const float4* xs = reinterpret_cast<const float4*>(st);
+    const float4* ds = reinterpret_cast<const float4*>(st + size_t(T) * 64);
+    uint32_t* c32 = reinterpret_cast<uint32_t*>(codes + e0);
+    for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
+      float4 y = xs[gi];
+      if (EC) y = sub4(y, ds[gi]);
+      const uint32_t c = quantize4(y, q.lo, q.inv);
+      __stcs(c32 + gi, c);
       if (EC) {
-        const float d = dequant1(q, p.lo, p.step);
-        delta[e] = __fsub_rn(v, d);
-        if (decoded) decoded[e] = d;
+        const float4 d = dequant4(c, q);
+        reinterpret_cast<float4*>(delta)[(e0 >> 2) + gi] = sub4(y, d);
+        if (decoded) __stcs(reinterpret_cast<float4*>(decoded) + (e0 >> 2) + gi, d);
       }
     }
-  }
+  });
+  r.edges(p, [&](size_t e) {
+    float y = x[e];
+    if (EC) y = __fsub_rn(y, delta[e]);
+    const uint8_t c = quantize1(y, q.lo, q.inv);
+    codes[e] = c;
+    if (EC) {
+      const float d = dequant1(c, q.lo, q.step);
+      delta[e] = __fsub_rn(y, d);
+      if (decoded) decoded[e] = d;
+    }
+  });
 }
 
-__global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restrict__ codes,
-                                                          const float* hdr, size_t n,
-                                                          float* __restrict__ out) {
-  const float lo = hdr[0], hi = hdr[1];
-  const float step = __fdiv_rn(__fsub_rn(hi, lo), 255.0f);
-  const Span sp = make_span(0, n);
-  const size_t stride = size_t(gridDim.x) * blockDim.x;
-  const uint32_t* c4 = reinterpret_cast<const uint32_t*>(codes);
+__global__ void __launch_bounds__(kRingThreads, 1) decode_ring_kernel(const uint8_t* __restrict__ codes,
+                                                                      const float* hdr, size_t n,
+                                                                      float* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  Ring r;
+  r.init(smem, nullptr, 0);
+  const U8Params q = u8_params(hdr[0], hdr[1]);
+  PassDesc p;
+  p.s = 0;
+  p.n = n;
+  p.eb = 1;
+  p.nsrc = 1;
+  p.base[0] = codes;
+  const int ct = r.ct;
   float4* o4 = reinterpret_cast<float4*>(out);
-  for (size_t base = sp.g0 + size_t(blockIdx.x) * blockDim.x + threadIdx.x; base < sp.g1;
-       base += stride * U) {
-    uint32_t c[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const size_t gi = base + u * stride;
-      c[u] = gi < sp.g1 ? ld_stream(c4 + gi) : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const size_t gi = base + u * stride;
-      if (gi < sp.g1) st_stream(o4 + gi, dequant4(c[u], lo, step));
-    }
-  }
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x < 8) {
-    const size_t e = threadIdx.x < 4 ? sp.s + threadIdx.x : sp.tail_begin + (threadIdx.x - 4);
-    const bool in = threadIdx.x < 4 ? e < sp.head_end : e < sp.s + sp.n;
-    if (in) out[e] = dequant1(codes[e], lo, step);
-  }
+  r.run(p, [&](const uint8_t* st, size_t e0, size_t units, int) {
+    const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
+    for (int gi = ct; gi < int(units * 4); gi += kConsumers) __stcs(o4 + (e0 >> 2) + gi, dequant4(cs[gi], q));
+  });
+  r.edges(p, [&](size_t e) { out[e] = dequant1(codes[e], q.lo, q.step); });
 }
 
 __global__ void init_keys_kernel(float* hdr, size_t n) {
@@ -305,22 +282,27 @@ extern "C" {
 
 const char* b2_last_error(void) { return b2::last_error(); }
 
+static int launch_encode(const float* x, float* delta, size_t n, uint8_t* codes, float* hdr, float* decoded,
+                         cudaStream_t s) {
+  if (n == 0) {  // empty input: header (0, 0), codec.cpp:52-57
+    init_keys_kernel<<<1, 1, 0, s>>>(hdr, n);
+    B2_CUDA_TRY(cudaGetLastError());
+    return B2_OK;
+  }
+  const void* fn = delta ? reinterpret_cast<const void*>(encode_ring_kernel<true>)
+                         : reinterpret_cast<const void*>(encode_ring_kernel<false>);
+  B2_CUDA_TRY(ensure_ring_smem(fn));
+  void* params[] = {&x, &delta, &n, &codes, &hdr, &decoded};
+  B2_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(sm_count()), dim3(kRingThreads), params, kRingSmem, s));
+  return B2_OK;
+}
+
 int b2_u8_encode(const float* x, size_t n, uint8_t* codes, float* hdr, void* stream) {
   B2_REQUIRE(hdr, "b2_u8_encode: hdr is null");
   B2_REQUIRE(n == 0 || (x && codes), "b2_u8_encode: null buffer");
   B2_REQUIRE(n == 0 || aligned16(x), "b2_u8_encode: x must be 16-byte aligned");
-  B2_REQUIRE(n == 0 || (reinterpret_cast<uintptr_t>(codes) & 3) == 0,
-             "b2_u8_encode: codes must be 4-byte aligned");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  init_keys_kernel<<<1, 1, 0, s>>>(hdr, n);
-  if (n) {
-    minmax_keys_kernel<false><<<grid_for((const void*)minmax_keys_kernel<false>), kThreads, 0, s>>>(
-        x, nullptr, n, reinterpret_cast<unsigned*>(hdr + 2));
-    quantize_kernel<false><<<grid_for((const void*)quantize_kernel<false>), kThreads, 0, s>>>(
-        x, nullptr, n, codes, hdr, nullptr);
-  }
-  B2_CUDA_TRY(cudaGetLastError());
-  return B2_OK;
+  B2_REQUIRE(n == 0 || aligned16(codes), "b2_u8_encode: codes must be 16-byte aligned");
+  return launch_encode(x, nullptr, n, codes, hdr, nullptr, static_cast<cudaStream_t>(stream));
 }
 
 int b2_u8_decode(const uint8_t* codes, const float* hdr, size_t n, float* out, void* stream) {
@@ -328,10 +310,10 @@ int b2_u8_decode(const uint8_t* codes, const float* hdr, size_t n, float* out, v
   if (n == 0) return B2_OK;
   B2_REQUIRE(codes && out, "b2_u8_decode: null buffer");
   B2_REQUIRE(aligned16(out), "b2_u8_decode: out must be 16-byte aligned");
-  B2_REQUIRE((reinterpret_cast<uintptr_t>(codes) & 3) == 0,
-             "b2_u8_decode: codes must be 4-byte aligned");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  decode_kernel<<<grid_for((const void*)decode_kernel), kThreads, 0, s>>>(codes, hdr, n, out);
+  B2_REQUIRE(aligned16(codes), "b2_u8_decode: codes must be 16-byte aligned");
+  B2_CUDA_TRY(ensure_ring_smem(reinterpret_cast<const void*>(decode_ring_kernel)));
+  decode_ring_kernel<<<sm_count(), kRingThreads, kRingSmem, static_cast<cudaStream_t>(stream)>>>(codes, hdr, n,
+                                                                                                  out);
   B2_CUDA_TRY(cudaGetLastError());
   return B2_OK;
 }
@@ -340,18 +322,9 @@ int b2_u8_compensate_encode(const float* x, float* delta, size_t n, uint8_t* cod
                             float* decoded, void* stream) {
   B2_REQUIRE(hdr, "b2_u8_compensate_encode: hdr is null");
   B2_REQUIRE(n == 0 || (x && delta && codes), "b2_u8_compensate_encode: null buffer");
-  B2_REQUIRE(n == 0 || (aligned16(x) && aligned16(delta) && (!decoded || aligned16(decoded))),
-             "b2_u8_compensate_encode: x, delta, decoded must be 16-byte aligned");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  init_keys_kernel<<<1, 1, 0, s>>>(hdr, n);
-  if (n) {
-    minmax_keys_kernel<true><<<grid_for((const void*)minmax_keys_kernel<true>), kThreads, 0, s>>>(
-        x, delta, n, reinterpret_cast<unsigned*>(hdr + 2));
-    quantize_kernel<true><<<grid_for((const void*)quantize_kernel<true>), kThreads, 0, s>>>(
-        x, delta, n, codes, hdr, decoded);
-  }
-  B2_CUDA_TRY(cudaGetLastError());
-  return B2_OK;
+  B2_REQUIRE(n == 0 || (aligned16(x) && aligned16(delta) && aligned16(codes) && (!decoded || aligned16(decoded))),
+             "b2_u8_compensate_encode: x, delta, codes, decoded must be 16-byte aligned");
+  return launch_encode(x, delta, n, codes, hdr, decoded, static_cast<cudaStream_t>(stream));
 }
 
 int b2_u8_pack_wire(const uint8_t* codes, const float* hdr, size_t n, uint8_t* wire, void* stream) {
