@@ -99,6 +99,31 @@ def build_host(force: bool = False) -> str | None:
     return HOSTLIB
 
 
+HOST_TEST_SRC = os.path.join(REPO, "tests", "cpp", "test_host_api.cpp")
+HOST_TEST_BIN = os.path.join(REPO, "tests", "cpp", "test_host_api")
+
+
+def build_host_test(force: bool = False) -> str | None:
+    """C++ test of the drop-in layer (links the oracle as its checker)."""
+    oracle_dir = os.path.join(REPO, "oracle")
+    liboracle = os.path.join(oracle_dir, "liboracle.so")
+    if not (os.path.exists(HOST_TEST_SRC) and os.path.exists(HOSTLIB) and os.path.exists(liboracle)):
+        return None
+    if not force and not _stale(HOST_TEST_BIN, [HOST_TEST_SRC, HOSTLIB, liboracle]):
+        return HOST_TEST_BIN
+    cmd = ["g++", "-std=c++20", "-O2", "-I", INCLUDE, "-I", "/usr/local/cuda/include", HOST_TEST_SRC,
+           "-o", HOST_TEST_BIN + ".tmp", "-L", PKG_DIR, "-lrcomm_b200", "-lb2comm", "-L", oracle_dir, "-loracle",
+           "-L/usr/local/cuda/lib64", "-lcudart", "-lpthread",
+           f"-Wl,-rpath,{PKG_DIR}:{oracle_dir}:/usr/local/cuda/lib64",
+           "-Wl,-rpath,$ORIGIN/../../paper_2107_01499_b200:$ORIGIN/../../oracle"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("g++ failed on the host-layer test")
+    os.replace(HOST_TEST_BIN + ".tmp", HOST_TEST_BIN)
+    return HOST_TEST_BIN
+
+
 def build(force: bool = False, verbose: bool = False) -> None:
     build_cuda(force=force, verbose=verbose)
     build_host(force=force)

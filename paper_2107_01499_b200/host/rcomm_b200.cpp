@@ -1,0 +1,466 @@
+// rcomm_b200.cpp -- C++ host layer over the C ABI (see include/rcomm_b200/rcomm_b200.hpp).
+//
+// Everything that computes goes through libb2comm's sm_100a kernels; this
+// file only validates arguments the way the reference does, stages host
+// spans through device memory, and turns status codes into exceptions.
+#include "rcomm_b200/rcomm_b200.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <unordered_set>
+
+namespace rcomm::b200 {
+
+void check(int status) {
+  if (status != B2_OK)
+    throw Error(status, std::string(b2_status_string(status)) + ": " + b2_last_error());
+}
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(B2_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    cudaGetDevice(&prev);
+    if (dev >= 0 && dev != prev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+struct DevBuf {  // owned device allocation
+  void* p = nullptr;
+  explicit DevBuf(std::size_t bytes) {
+    if (bytes) cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// A float span resolved to a 16-byte aligned device buffer; host spans (and
+// misaligned device spans) are staged and written back by finish().
+struct Staged {
+  std::span<float> user;
+  float* dev = nullptr;
+  std::unique_ptr<DevBuf> own;
+  bool host = false;
+  Staged(std::span<float> x, cudaStream_t s) : user(x) {
+    const bool on_dev = is_device_ptr(x.data());
+    host = !on_dev;
+    if (on_dev && (reinterpret_cast<std::uintptr_t>(x.data()) & 15) == 0) {
+      dev = x.data();
+      return;
+    }
+    own = std::make_unique<DevBuf>(std::max<std::size_t>(x.size(), 1) * sizeof(float));
+    dev = own->as<float>();
+    if (!x.empty())
+      cuda_check(cudaMemcpyAsync(dev, x.data(), x.size() * sizeof(float), cudaMemcpyDefault, s), "stage in");
+  }
+  void finish(cudaStream_t s) {
+    if (own && !user.empty())
+      cuda_check(cudaMemcpyAsync(user.data(), dev, user.size() * sizeof(float), cudaMemcpyDefault, s), "stage out");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  }
+};
+
+std::vector<float> to_host(std::span<const float> x) {
+  std::vector<float> h(x.size());
+  if (!x.empty()) cuda_check(cudaMemcpy(h.data(), x.data(), x.size() * 4, cudaMemcpyDefault), "copy to host");
+  return h;
+}
+
+void check_codec(const Codec& c, std::mt19937* rng) {
+  if (c.kind == CodecKind::onebit)
+    throw Error(B2_ERR_UNSUPPORTED, "onebit codec is not implemented on the B200 path");
+  if (c.kind == CodecKind::uniform8 && c.rounding == Rounding::stochastic) {
+    if (!rng) throw Error(B2_ERR_INVALID, "uniform8 stochastic rounding needs a generator");  // codec.cpp:70
+    throw Error(B2_ERR_UNSUPPORTED, "uniform8 stochastic rounding is not implemented on the B200 path");
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ codec
+Payload Codec::encode(std::span<const float> x, std::mt19937* rng) const {
+  check_codec(*this, rng);
+  const std::size_t n = x.size();
+  if (kind == CodecKind::identity) {  // codec.cpp:41,47-50
+    std::vector<float> h = to_host(x);
+    for (float v : h)
+      if (!std::isfinite(v)) throw Error(B2_ERR_NONFINITE, "encode: non-finite input value");
+    Payload p(4 * n);
+    if (n) std::memcpy(p.data(), h.data(), 4 * n);
+    return p;
+  }
+  DevBuf xs((n ? n : 1) * 4), codes(n + 64), hdr(B2_U8_HDR_BYTES), wire(8 + n);
+  if (n) cuda_check(cudaMemcpy(xs.p, x.data(), 4 * n, cudaMemcpyDefault), "stage in");
+  check(b2_u8_encode(xs.as<float>(), n, codes.as<std::uint8_t>(), hdr.as<float>(), nullptr));
+  check(b2_u8_pack_wire(codes.as<std::uint8_t>(), hdr.as<float>(), n, wire.as<std::uint8_t>(), nullptr));
+  Payload p(8 + n);
+  cuda_check(cudaMemcpy(p.data(), wire.p, 8 + n, cudaMemcpyDeviceToHost), "copy payload");
+  float lohi[2];
+  std::memcpy(lohi, p.data(), 8);
+  if (!std::isfinite(lohi[0]) || !std::isfinite(lohi[1]))
+    throw Error(B2_ERR_NONFINITE, "encode: non-finite input value");  // codec.cpp:24-27
+  return p;
+}
+
+void Codec::decode(std::span<const std::uint8_t> payload, std::span<float> out) const {
+  const std::size_t n = out.size();
+  if (kind == CodecKind::onebit) throw Error(B2_ERR_UNSUPPORTED, "onebit codec is not implemented on the B200 path");
+  if (payload.size() != payload_size(n)) throw Error(B2_ERR_INVALID, "decode: malformed payload (length mismatch)");
+  if (n == 0) return;
+  if (kind == CodecKind::identity) {
+    cuda_check(cudaMemcpy(out.data(), payload.data(), 4 * n, cudaMemcpyDefault), "decode copy");
+    return;
+  }
+  DevBuf wire(8 + n), codes(n + 64), hdr(B2_U8_HDR_BYTES), res(4 * n);
+  cuda_check(cudaMemcpy(wire.p, payload.data(), 8 + n, cudaMemcpyDefault), "stage payload");
+  check(b2_u8_unpack_wire(wire.as<std::uint8_t>(), n, codes.as<std::uint8_t>(), hdr.as<float>(), nullptr));
+  check(b2_u8_decode(codes.as<std::uint8_t>(), hdr.as<float>(), n, res.as<float>(), nullptr));
+  cuda_check(cudaMemcpy(out.data(), res.p, 4 * n, cudaMemcpyDefault), "copy out");
+}
+
+std::vector<float> Codec::decode(std::span<const std::uint8_t> payload, std::size_t n) const {
+  std::vector<float> out(n);
+  decode(payload, std::span<float>(out));
+  return out;
+}
+
+Payload compensate_encode(const Codec& codec, std::span<const float> x, std::span<float> delta, std::mt19937* rng,
+                          std::vector<float>* decoded) {
+  check_codec(codec, rng);
+  const std::size_t n = x.size();
+  if (delta.size() != n) throw Error(B2_ERR_INVALID, "compensate_encode: length mismatch");  // codec.cpp:129
+  if (codec.kind == CodecKind::identity) {
+    std::vector<float> h = to_host(x), d = to_host(delta);
+    for (std::size_t k = 0; k < n; ++k) h[k] -= d[k];
+    Payload p = codec.encode(h);
+    std::vector<float> zero(n);
+    for (std::size_t k = 0; k < n; ++k) zero[k] = h[k] - h[k];
+    if (n) cuda_check(cudaMemcpy(delta.data(), zero.data(), 4 * n, cudaMemcpyDefault), "delta out");
+    if (decoded) *decoded = h;
+    return p;
+  }
+  DevBuf xs((n ? n : 1) * 4), ds((n ? n : 1) * 4), codes(n + 64), hdr(B2_U8_HDR_BYTES), dec((n ? n : 1) * 4),
+      wire(8 + n);
+  if (n) {
+    cuda_check(cudaMemcpy(xs.p, x.data(), 4 * n, cudaMemcpyDefault), "stage x");
+    cuda_check(cudaMemcpy(ds.p, delta.data(), 4 * n, cudaMemcpyDefault), "stage delta");
+  }
+  check(b2_u8_compensate_encode(xs.as<float>(), ds.as<float>(), n, codes.as<std::uint8_t>(), hdr.as<float>(),
+                                dec.as<float>(), nullptr));
+  check(b2_u8_pack_wire(codes.as<std::uint8_t>(), hdr.as<float>(), n, wire.as<std::uint8_t>(), nullptr));
+  Payload p(8 + n);
+  cuda_check(cudaMemcpy(p.data(), wire.p, 8 + n, cudaMemcpyDeviceToHost), "copy payload");
+  float lohi[2];
+  std::memcpy(lohi, p.data(), 8);
+  if (!std::isfinite(lohi[0]) || !std::isfinite(lohi[1]))
+    throw Error(B2_ERR_NONFINITE, "encode: non-finite input value");
+  if (n) cuda_check(cudaMemcpy(delta.data(), ds.p, 4 * n, cudaMemcpyDefault), "delta out");
+  if (decoded) {
+    decoded->resize(n);
+    if (n) cuda_check(cudaMemcpy(decoded->data(), dec.p, 4 * n, cudaMemcpyDeviceToHost), "decoded out");
+  }
+  return p;
+}
+
+ErrorState::ErrorState(std::size_t bucket_len, std::size_t owned_len, int device) : dlen_(bucket_len), elen_(owned_len) {
+  DeviceScope ds(device);
+  cuda_check(cudaMalloc(&delta_, std::max<std::size_t>(dlen_, 4) * 4), "cudaMalloc delta");
+  cuda_check(cudaMalloc(&eps_, std::max<std::size_t>(elen_, 4) * 4), "cudaMalloc epsilon");
+  cuda_check(cudaMemset(delta_, 0, std::max<std::size_t>(dlen_, 4) * 4), "memset");
+  cuda_check(cudaMemset(eps_, 0, std::max<std::size_t>(elen_, 4) * 4), "memset");
+}
+ErrorState::~ErrorState() {
+  if (delta_) cudaFree(delta_);
+  if (eps_) cudaFree(eps_);
+}
+ErrorState::ErrorState(ErrorState&& o) noexcept { *this = std::move(o); }
+ErrorState& ErrorState::operator=(ErrorState&& o) noexcept {
+  std::swap(delta_, o.delta_);
+  std::swap(eps_, o.eps_);
+  std::swap(dlen_, o.dlen_);
+  std::swap(elen_, o.elen_);
+  return *this;
+}
+std::vector<float> ErrorState::delta_host() const { return to_host({delta_, dlen_}); }
+std::vector<float> ErrorState::epsilon_host() const { return to_host({eps_, elen_}); }
+
+// ------------------------------------------------------------- topology
+std::pair<std::size_t, std::size_t> partition_range(std::size_t len, int n, int k) {
+  std::size_t lo, sz;
+  b2_partition_range(len, n, k, &lo, &sz);
+  return {lo, sz};
+}
+std::size_t owned_partition_len(std::size_t len, int world, int idx) { return b2_owned_partition_len(len, world, idx); }
+
+std::vector<int> Topology::neighbors(int rank, std::uint64_t round) const {
+  std::vector<int> out(static_cast<std::size_t>(std::max(n, 3)));
+  const int m = b2_topology_neighbors(static_cast<int>(kind), n, seed, rank, round, out.data());
+  if (m < 0) throw Error(B2_ERR_INVALID, b2_last_error());
+  out.resize(static_cast<std::size_t>(m));
+  return out;
+}
+
+// ---------------------------------------------------------- thread group
+struct ThreadGroup::State {
+  int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::vector<std::vector<std::uint8_t>> slots;
+  int arrived = 0, departed = 0;
+  std::uint64_t gen = 0;
+};
+
+ThreadGroup::ThreadGroup(int world) : s_(std::make_shared<State>()) {
+  s_->world = world;
+  s_->slots.resize(static_cast<std::size_t>(world));
+}
+ThreadGroup::~ThreadGroup() = default;
+int ThreadGroup::world() const { return s_->world; }
+
+AllGather ThreadGroup::allgather(int rank) {
+  auto s = s_;
+  return [s, rank](const void* send, std::size_t bytes, void* recv) {
+    std::unique_lock<std::mutex> lk(s->mu);
+    const std::uint64_t my_gen = s->gen;
+    s->slots[static_cast<std::size_t>(rank)].assign(static_cast<const std::uint8_t*>(send),
+                                                    static_cast<const std::uint8_t*>(send) + bytes);
+    if (++s->arrived == s->world) {
+      s->arrived = 0;
+      ++s->gen;
+      s->cv.notify_all();
+    } else {
+      s->cv.wait(lk, [&] { return s->gen != my_gen; });
+    }
+    for (int r = 0; r < s->world; ++r)
+      std::memcpy(static_cast<std::uint8_t*>(recv) + static_cast<std::size_t>(r) * bytes,
+                  s->slots[static_cast<std::size_t>(r)].data(), bytes);
+    // second rendezvous: nobody overwrites a slot before everyone copied it
+    const std::uint64_t g2 = s->gen;
+    if (++s->departed == s->world) {
+      s->departed = 0;
+      ++s->gen;
+      s->cv.notify_all();
+    } else {
+      s->cv.wait(lk, [&] { return s->gen != g2; });
+    }
+  };
+}
+
+// ---------------------------------------------------------------- endpoint
+int B200Endpoint::gather_trampoline(void* user, const void* send, std::size_t bytes, void* recv) {
+  try {
+    static_cast<B200Endpoint*>(user)->allgather_(send, bytes, recv);
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
+
+B200Endpoint::B200Endpoint(int rank, int world, int device, AllGather allgather)
+    : rank_(rank), world_(world), device_(device), allgather_(std::move(allgather)) {
+  DeviceScope ds(device_);
+  cudaStream_t s;
+  cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+  stream_ = s;
+  check(b2_comm_create(world_, rank_, device_, allgather_ ? &B200Endpoint::gather_trampoline : nullptr, this, &comm_));
+}
+
+B200Endpoint::~B200Endpoint() {
+  if (comm_) b2_comm_destroy(comm_);
+  if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
+}
+
+int B200Endpoint::node_of(int r) const {
+  if (r < 0 || r >= world_) throw Error(B2_ERR_INVALID, "unknown rank " + std::to_string(r));
+  return 0;
+}
+
+void B200Endpoint::sync() { check(b2_comm_sync(comm_, stream_)); }
+
+// --------------------------------------------------------------- primitives
+double c_fp_s(B200Endpoint& ep, double now, std::span<float> x, std::uint32_t bucket) {
+  DeviceScope ds(ep.device());
+  auto s = static_cast<cudaStream_t>(ep.stream());
+  Staged b(x, s);
+  check(b2_c_fp_s(ep.handle(), b.dev, x.size(), bucket, s));
+  b.finish(s);
+  ep.sync();
+  const int g = ep.world_size(), me = ep.rank();
+  if (g > 1) {
+    const std::size_t own = owned_partition_len(x.size(), g, me);
+    ep.account(4 * (x.size() - own) + 4 * own * (g - 1), 2 * (g - 1));  // 2(n-1) messages, test_collectives.cpp:95
+  }
+  return now;
+}
+
+double c_lp_s(B200Endpoint& ep, double now, std::span<float> x, const Codec& codec, ErrorState* es,
+              std::mt19937* rng, std::uint32_t bucket) {
+  check_codec(codec, rng);
+  DeviceScope ds(ep.device());
+  auto s = static_cast<cudaStream_t>(ep.stream());
+  Staged b(x, s);
+  check(b2_c_lp_s(ep.handle(), b.dev, x.size(), static_cast<int>(codec.kind), es ? es->delta() : nullptr,
+                  es ? es->delta_len() : 0, es ? es->epsilon() : nullptr, es ? es->epsilon_len() : 0, bucket, s));
+  b.finish(s);
+  ep.sync();
+  const int g = ep.world_size(), me = ep.rank();
+  if (g > 1) {
+    std::uint64_t sent = 0;
+    for (int k = 0; k < g; ++k)
+      if (k != me) sent += codec.payload_size(partition_range(x.size(), g, k).second);
+    sent += (g - 1) * codec.payload_size(owned_partition_len(x.size(), g, me));
+    ep.account(sent, 2 * (g - 1));
+  }
+  return now;
+}
+
+namespace {
+std::vector<int> nbrs_of(B200Endpoint& ep, const Topology& topo, std::uint64_t round) {
+  if (topo.n != ep.world_size()) throw Error(B2_ERR_INVALID, "topology size mismatch");  // collectives.cpp:232
+  return topo.neighbors(ep.rank(), round);
+}
+}  // namespace
+
+double d_fp_s(B200Endpoint& ep, double now, std::span<float> x, const Topology& topo, std::uint64_t round,
+              ReduceMode mode, std::uint32_t bucket) {
+  const auto nb = nbrs_of(ep, topo, round);
+  DeviceScope ds(ep.device());
+  auto s = static_cast<cudaStream_t>(ep.stream());
+  Staged b(x, s);
+  check(b2_d_fp_s(ep.handle(), b.dev, x.size(), nb.data(), static_cast<int>(nb.size()), static_cast<int>(mode),
+                  bucket, s));
+  b.finish(s);
+  ep.sync();
+  ep.account((nb.size() - 1) * 4 * x.size(), nb.size() - 1);
+  return now;
+}
+
+double d_lp_s(B200Endpoint& ep, double now, std::span<float> x, const Topology& topo, std::uint64_t round,
+              const Codec& codec, ReduceMode mode, std::mt19937* rng, std::uint32_t bucket) {
+  check_codec(codec, rng);
+  const auto nb = nbrs_of(ep, topo, round);
+  DeviceScope ds(ep.device());
+  auto s = static_cast<cudaStream_t>(ep.stream());
+  Staged b(x, s);
+  check(b2_d_lp_s(ep.handle(), b.dev, x.size(), nb.data(), static_cast<int>(nb.size()), static_cast<int>(codec.kind),
+                  static_cast<int>(mode), bucket, s));
+  b.finish(s);
+  ep.sync();
+  ep.account((nb.size() - 1) * codec.payload_size(x.size()), nb.size() - 1);
+  return now;
+}
+
+// ------------------------------------------------------------------ tensors
+namespace {
+std::size_t shape_product(const std::vector<std::size_t>& shape) {  // tensor.cpp:9-17
+  std::size_t p = 1;
+  for (std::size_t d : shape) {
+    if (d == 0) throw Error(B2_ERR_INVALID, "tensor shape has a zero dimension");
+    p *= d;
+  }
+  return shape.empty() ? 0 : p;
+}
+std::shared_ptr<float> device_alloc(std::size_t n, int device) {
+  DeviceScope ds(device);
+  float* p = nullptr;
+  cuda_check(cudaMalloc(&p, std::max<std::size_t>(n, 4) * sizeof(float)), "cudaMalloc tensor");
+  return std::shared_ptr<float>(p, [](float* q) { cudaFree(q); });
+}
+}  // namespace
+
+FlatTensor::FlatTensor(std::string name, std::vector<std::size_t> shape)
+    : name_(std::move(name)), shape_(std::move(shape)) {
+  if (name_.empty()) throw Error(B2_ERR_INVALID, "tensor name must be non-empty");
+  len_ = capacity_ = shape_product(shape_);
+  storage_ = device_alloc(len_, -1);
+  cuda_check(cudaMemset(storage_.get(), 0, std::max<std::size_t>(len_, 4) * 4), "memset");
+}
+
+FlatTensor::FlatTensor(std::string name, std::vector<std::size_t> shape, const std::vector<float>& values,
+                       int device)
+    : name_(std::move(name)), shape_(std::move(shape)) {
+  if (name_.empty()) throw Error(B2_ERR_INVALID, "tensor name must be non-empty");
+  len_ = capacity_ = shape_product(shape_);
+  if (values.size() != len_) throw Error(B2_ERR_INVALID, "tensor '" + name_ + "': shape/data length mismatch");
+  storage_ = device_alloc(len_, device);
+  if (len_) cuda_check(cudaMemcpy(storage_.get(), values.data(), 4 * len_, cudaMemcpyHostToDevice), "upload");
+}
+
+std::vector<float> FlatTensor::to_host() const { return b200::to_host({data(), len_}); }
+
+FlatTensor BucketArena::as_flat(const std::string& name) const {
+  FlatTensor t;
+  t.name_ = name;
+  t.shape_ = {len_};
+  t.storage_ = storage_;
+  t.offset_ = 0;
+  t.len_ = t.capacity_ = len_;
+  return t;
+}
+
+BucketArena BucketArena::flatten(std::span<FlatTensor*> tensors) {  // tensor.cpp:46-68
+  if (tensors.empty()) throw Error(B2_ERR_INVALID, "flatten: empty tensor list");
+  std::unordered_set<std::string> seen;
+  std::size_t total = 0;
+  for (FlatTensor* t : tensors) {
+    if (t->size() == 0) throw Error(B2_ERR_INVALID, "flatten: zero-length tensor '" + t->name() + "'");
+    if (!seen.insert(t->name()).second) throw Error(B2_ERR_INVALID, "flatten: duplicate tensor name '" + t->name() + "'");
+    total += t->size();
+  }
+  int device = 0;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, tensors[0]->data()) == cudaSuccess) device = a.device;
+  BucketArena arena;
+  arena.storage_ = device_alloc(total, device);
+  arena.len_ = total;
+  std::vector<const float*> srcs;
+  std::vector<std::size_t> lens;
+  for (FlatTensor* t : tensors) {
+    srcs.push_back(t->data());
+    lens.push_back(t->size());
+  }
+  DeviceScope ds(device);
+  check(b2_bucket_flatten(srcs.data(), lens.data(), static_cast<int>(srcs.size()), arena.storage_.get(), nullptr));
+  cuda_check(cudaDeviceSynchronize(), "flatten sync");
+  std::size_t off = 0;
+  for (FlatTensor* t : tensors) {
+    arena.members_.push_back({t->name(), off, t->size()});
+    t->storage_ = arena.storage_;  // repoint: writes alias both ways (tensor.cpp:63-64)
+    t->offset_ = off;
+    t->capacity_ = total;
+    off += t->size();
+  }
+  return arena;
+}
+
+}  // namespace rcomm::b200
