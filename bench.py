@@ -80,6 +80,15 @@ def algorithmic_bytes(prim: str, n: int, g: int):
     return 10 * n, 0  # codec: read x, write codes, read codes, write x
 
 
+def ncu_traffic(prim: str, g: int):
+    """DRAM bytes per launch measured by ncu (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(prim, {}).get(str(g))
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -280,7 +289,7 @@ def run_b200(args, rank: int, world: int):
         roof = {"bound": "hbm", "achieved": round(hbm_b / t_s / 1e9, 2), "peak": hbm_peak, "unit": "GB/s",
                 "peak_kind": f"{peak_kind} HBM copy (MEASURED_PEAKS.json)"}
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
-    roof["traffic"] = args.traffic
+    roof["traffic"] = args.traffic if args.traffic is not None else ncu_traffic(prim, g)
     roof["algorithmic_bytes"] = {"hbm": hbm_b, "nvlink_ingress": nvl_b}
     roof["t_roof_us"] = round(max(t_roof_hbm, t_roof_nvl) * 1e6, 1)
     roof["kernel"] = {"c_lp_s": "central_kernel<uint8> (one fused launch per step)",
