@@ -173,8 +173,8 @@ class B200Endpoint:
 
     # -- phase tracing (ncu cannot replay kernels that rendezvous across GPUs)
     TRACE_POINTS = ("start", "p1_first_minmax", "p1_first_push", "p1_done", "p2_ready", "p2_minmax",
-                    "p2_done", "p3_first", "end", "p2_pass", "p1_step0", "p1_step1", "p1_step2", "p1_step3", "p1_step4",
-                    "p1_step5")
+                    "p2_done", "p3_first", "end", "p2_pass") + tuple(f"p1_step{i}" for i in range(8)) + tuple(
+                    f"p1_fenced{i}" for i in range(8))
 
     def enable_trace(self, on: bool = True) -> None:
         check(lib.b2_comm_enable_trace(self._h, int(on)))
@@ -186,7 +186,7 @@ class B200Endpoint:
         import numpy as _np
         torch.cuda.synchronize(self.device)
         grid = torch.cuda.get_device_properties(self.device).multi_processor_count
-        buf = (C.c_uint64 * (grid * 16))()
+        buf = (C.c_uint64 * (grid * 32))()
         n = C.c_int()
         check(lib.b2_comm_read_trace(self._h, buf, grid, C.byref(n)))
         t = _np.ctypeslib.as_array(buf).reshape(grid, n.value).astype(_np.float64)

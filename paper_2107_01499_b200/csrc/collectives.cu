@@ -123,6 +123,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   __shared__ float2 red[32];
   __shared__ float s_lo[kMaxRanks], s_step[kMaxRanks];
   __shared__ SrcDec s_dec[kMaxRanks];
+  __shared__ SrcDec s_dec3[kMaxRanks];  // phase-3 owner headers (written by the producer)
+  __shared__ int s_fast3[kMaxRanks];
   __shared__ int s_fast;
   __shared__ int s_flag;
   __shared__ volatile int s_gate;
@@ -407,9 +409,10 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       });
     }
     if (i == 0) B2_TRACE(kTrP1FirstB);
-    if (i < 6) B2_TRACE(kTrP1Step + i);
+    B2_TRACE(kTrP1Step + i);
     if (cons && consumer_arrive<true>(a.cta_done + k, &s_flag) && ct == 0)
       red_release_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);
+    B2_TRACE(kTrP1Fenced + i);
   }
   B2_TRACE(kTrP1Done);
 
@@ -578,46 +581,56 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
       pp[i].wait_flag = &hdr_of(a.win[k])->ready2;
       pp[i].wait_target = a.epoch;
     }
-    if (cons) {
-      if (ct < g) {  // one consumer thread per owner: wait, then its header
-        const int k = powner[ct];
-        WinHdr* hk = hdr_of(a.win[k]);
-        wait_geq(&hk->ready2, a.epoch, a.timeout_ns, a.status);
-        if (CODEC == kU8) {
-          const float2 h = k == me ? mine->hdr2 : ld_peer_f2(&hk->hdr2);
-          const U8Params q = u8_params(h.x, h.y);
-          s_dec[ct] = SrcDec{q.lo, q.step, q.c23};
-          s_lo[ct] = q.fastdec ? 1.0f : 0.0f;  // per-owner fast-decode flag
-        }
+    // header of owner i: read by the producer after owner i's flag (ready
+    // callback) or, for the edge elements, by consumer warp 0 of the last CTA
+    auto load_hdr = [&](int i) {
+      const int k = powner[i];
+      WinHdr* hk = hdr_of(a.win[k]);
+      if (CODEC == kU8) {
+        const float2 h = k == me ? mine->hdr2 : ld_peer_f2(&hk->hdr2);
+        const U8Params q = u8_params(h.x, h.y);
+        s_dec3[i] = SrcDec{q.lo, q.step, q.c23};
+        s_fast3[i] = q.fastdec;
       }
-      consumer_sync();
-      B2_TRACE(kTrP3First);
-    }
+    };
+    if (cons) B2_TRACE(kTrP3First);
     if (CODEC == kU8) {
-      r.run_multi(pp, g, [&](int i, const uint8_t* st, size_t e0, size_t units, int) {
-        const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
-        const SrcDec kd = s_dec[i];
-        if (s_lo[i] != 0.0f) {
-          for (int gi = ct; gi < int(units * 4); gi += kConsumers)
-            __stcs(x4 + ((e0 >> 2) + gi), dequant4_fast(cs[gi], kd.lo, kd.step, kd.c23));
-        } else {
-          for (int gi = ct; gi < int(units * 4); gi += kConsumers)
-            __stcs(x4 + ((e0 >> 2) + gi), dequant4(cs[gi], kd.lo, kd.step));
-        }
-      });
-      for (int i = 0; i < g; ++i) {
-        const uint8_t* src = a.win[powner[i]] + a.off_out2;
-        const SrcDec kd = s_dec[i];
-        r.edges(pp[i], [&](size_t e) { a.x[e] = dequant1(__ldcg(src + (e - pbase[i])), kd.lo, kd.step); });
-      }
+      r.run_multi(
+          pp, g,
+          [&](int i, const uint8_t* st, size_t e0, size_t units, int) {
+            const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
+            const SrcDec kd = s_dec3[i];
+            if (s_fast3[i]) {
+              for (int gi = ct; gi < int(units * 4); gi += kConsumers)
+                __stcs(x4 + ((e0 >> 2) + gi), dequant4_fast(cs[gi], kd.lo, kd.step, kd.c23));
+            } else {
+              for (int gi = ct; gi < int(units * 4); gi += kConsumers)
+                __stcs(x4 + ((e0 >> 2) + gi), dequant4(cs[gi], kd.lo, kd.step));
+            }
+          },
+          load_hdr);
     } else {
       r.run_multi(pp, g, [&](int, const uint8_t* st, size_t e0, size_t units, int) {
         const float4* fs = reinterpret_cast<const float4*>(st);
         for (int gi = ct; gi < int(units * 4); gi += kConsumers) __stcs(x4 + ((e0 >> 2) + gi), fs[gi]);
       });
+    }
+    // unaligned heads/tails (last CTA, consumer warp 0): wait + header per owner
+    if (cons && blockIdx.x == gridDim.x - 1 && ct < 32) {
       for (int i = 0; i < g; ++i) {
-        const float* src = reinterpret_cast<const float*>(a.win[powner[i]] + a.off_out2);
-        r.edges(pp[i], [&](size_t e) { a.x[e] = __ldcg(src + (e - pbase[i])); });
+        if (pp[i].body_begin() == pp[i].s && pp[i].body_end() == pp[i].s + pp[i].n) continue;
+        if (ct == 0) {
+          wait_geq(&hdr_of(a.win[powner[i]])->ready2, a.epoch, a.timeout_ns, a.status);
+          load_hdr(i);
+        }
+        __syncwarp();
+        const uint8_t* src = a.win[powner[i]] + a.off_out2;
+        const SrcDec kd = s_dec3[i];
+        r.edges(pp[i], [&](size_t e) {
+          a.x[e] = CODEC == kU8 ? dequant1(__ldcg(src + (e - pbase[i])), kd.lo, kd.step)
+                               : __ldcg(reinterpret_cast<const float*>(src) + (e - pbase[i]));
+        });
+        __syncwarp();
       }
     }
     (void)plo;

@@ -28,7 +28,7 @@ enum Codec : int { kIdentity = 0, kU8 = 1 };
 // Per-CTA phase timestamps (%globaltimer, ns) written by consumer thread 0
 // when tracing is enabled -- the multi-GPU replacement for ncu, which cannot
 // replay kernels that rendezvous with other GPUs.
-constexpr int kTraceSlots = 16;
+constexpr int kTraceSlots = 32;
 enum TracePoint : int {
   kTrStart = 0,
   kTrP1FirstA = 1,   // phase 1: first chunk's (min,max) final
@@ -40,7 +40,8 @@ enum TracePoint : int {
   kTrP3First = 7,    // phase 3: first owner's payload ready
   kTrEnd = 8,
   kTrP2Pass = 9,     // phase 2: second pass done, before the publication fence
-  kTrP1Step = 10,    // 10..15: phase-1 step i (chunk me+1+i) pushed, before its fence
+  kTrP1Step = 10,    // 10..17: phase-1 step i (chunk me+1+i) pushed, before its fence
+  kTrP1Fenced = 18,  // 18..25: phase-1 step i fenced and signalled
 };
 
 // Centralized ScatterReduce (C_FP_S, C_LP_S).

@@ -152,6 +152,14 @@ struct Ring {
   // at once, which keeps NVLink fan-in balanced whatever the rank skew.
   template <class F>
   __device__ void run_multi(const PassDesc* ps, int np, F&& consume) {
+    run_multi(ps, np, consume, [](int) {});
+  }
+  // ready(i) runs on the producer lane right after pass i's wait flag is
+  // satisfied and before its first tile is handed over, so anything it writes
+  // to shared memory (e.g. the pass's codec header) is visible to the
+  // consumers of every tile of pass i (mbarrier release/acquire).
+  template <class F, class R>
+  __device__ void run_multi(const PassDesc* ps, int np, F&& consume, R&& ready) {
     size_t mm[kMaxRanks];
     bool w[kMaxRanks];
     size_t m = 0;
@@ -160,13 +168,22 @@ struct Ring {
       const size_t nt = (ps[i].nunits() + T - 1) / T;
       mm[i] = nt > blockIdx.x ? (nt - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
       m = mm[i] > m ? mm[i] : m;
-      w[i] = ps[i].wait_flag == nullptr;
+      w[i] = false;
     }
     for (size_t t = 0; t < m; ++t)
       for (int i = 0; i < np; ++i)
-        if (t < mm[i])
+        if (t < mm[i]) {
+          if (producer && (threadIdx.x & 31) == 0 && !w[i]) {
+            if (ps[i].wait_flag) {
+              wait_geq(ps[i].wait_flag, ps[i].wait_target, timeout_ns, status);
+              fence_proxy_async();
+            }
+            ready(i);
+          }
+          w[i] = true;
           tile(ps[i], tile_index(ps[i], t, mm[i]),
                [&](const uint8_t* st, size_t e0, size_t units, int T) { consume(i, st, e0, units, T); }, w[i]);
+        }
   }
 
   // One tile of a pass (producer lane 0 issues, consumers consume).  The

@@ -19,6 +19,7 @@ for it in range(3):
     b2.c_lp_s(ep, 0.0, x, U8, None)
     t = ep.read_trace(raw=True)
     names = ep.TRACE_POINTS
+    raw0 = None
     out = {}
     for i, nm in enumerate(names):
         col = t[:, i]
