@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) encode_ring_kernel(const floa
     lo = fmin_nan(lo, v);
     hi = fmax_nan(hi, v);
   });
-  if (!r.producer) {
+  if (r.ct >= 0) {
     const float2 m = consumer_minmax(lo, hi, red);
     if (ct == 0) {
       if (m.x != m.x || m.y != m.y) {

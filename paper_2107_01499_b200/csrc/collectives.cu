@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   if (threadIdx.x == 0) s_gate = 0;
   __syncthreads();
   const int G = gridDim.x, g = a.g, me = a.me, ct = r.ct;
-  const bool cons = !r.producer;
+  const bool cons = r.ct >= 0;
   float4* x4 = reinterpret_cast<float4*>(a.x);
   float4* dl4 = reinterpret_cast<float4*>(a.delta);
   int bad = 0;
@@ -329,7 +329,34 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     mlo_ = kInf;
     mhi_ = -kInf;
   };
-  if (CODEC == kU8) {
+  if (CODEC == kU8 && r.storer) {
+    // ---- storer warp: push every staged tile of every chunk (same tile order
+    // as the consumers), then wait for the writes and signal the owner.
+    if ((threadIdx.x & 31) == 0) {
+      for (int i = 0; i < g; ++i) {
+        const int k = (me + 1 + i) % g;
+        size_t lo, sz;
+        part_range(a.n, g, k, lo, sz);
+        PassDesc px = xpass(lo, sz);
+        px.reverse = true;
+        uint8_t* dst = a.win[k] + a.off_recv1 + size_t(me) * a.slot_stride;
+        const size_t ebase = lo & ~size_t(15);
+        const int T = px.tile_units();
+        const size_t nun = px.nunits(), nt = (nun + T - 1) / T;
+        const size_t m = nt > blockIdx.x ? (nt - blockIdx.x + G - 1) / G : 0;
+        for (size_t j = 0; j < m; ++j) {
+          const size_t t = r.tile_index(px, j, m);
+          const size_t units = (nun - t * T) < size_t(T) ? (nun - t * T) : size_t(T);
+          const size_t e0 = 16 * (px.u0() + t * T);
+          r.slot_push(dst + (e0 - ebase), unsigned(units * 16));
+        }
+        bulk_wait_all();  // this CTA's pushes of chunk k are performed
+        fence_proxy_async();
+        __threadfence_system();
+        red_release_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);  // arrival: this CTA's codes
+      }
+    }
+  } else if (CODEC == kU8) {
     size_t lo0, sz0;
     part_range(a.n, g, (me + 1) % g, lo0, sz0);
     const PassDesc p0 = xpass(lo0, sz0);
@@ -337,7 +364,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     mm_edges(p0);
     mm_publish((me + 1) % g);
   }
-  for (int i = 0; i < g; ++i) {
+  for (int i = 0; i < g && !(CODEC == kU8 && r.storer); ++i) {
     const int k = (me + 1 + i) % g;
     size_t lo, sz;
     part_range(a.n, g, k, lo, sz);
@@ -354,19 +381,24 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
         if (blockIdx.x == 0 && ct == 0) {
           hdr_of(a.win[k])->hdr1[me] = mm;  // remote 8-byte store into owner k's header
           if (sz && !(finite_f(mm.x) && finite_f(mm.y))) latch(a.status, kStatusNonFinite);
+          __threadfence_system();
+          red_release_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);  // arrival: header
         }
       }
+      // codes go to a staging slot; the storer warp pushes it with a TMA bulk
+      // store and signals the owner, so consumers never wait on NVLink drain
       auto push = [&](const uint8_t* st, size_t e0, size_t units, int T) {
         const float4* xs = reinterpret_cast<const float4*>(st);
         const float4* ds = reinterpret_cast<const float4*>(st + size_t(T) * 64);
+        uint32_t* sl = reinterpret_cast<uint32_t*>(r.slot_acquire());
         for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
           float4 y = xs[gi];
           if (EC) y = sub4(y, ds[gi]);
           const uint32_t q = quantize4(y, p.lo, p.inv);
-          const size_t e = e0 + 4 * size_t(gi);
-          *reinterpret_cast<uint32_t*>(dst + (e - ebase)) = q;
-          if (EC) dl4[e >> 2] = sub4(y, dequant4(q, p));
+          sl[gi] = q;
+          if (EC) dl4[(e0 >> 2) + gi] = sub4(y, dequant4(q, p));
         }
+        r.slot_commit();
       };
       if (i + 1 < g) {  // B(k) interleaved with A(next chunk)
         const int kn = (me + 2 + i) % g;
@@ -386,6 +418,13 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
         dst[e - ebase] = q;
         if (EC) a.delta[e] = __fsub_rn(y, dequant1(q, p.lo, p.step));
       });
+      if (cons && blockIdx.x == G - 1 && ct < 32) {  // arrival: unaligned head/tail codes
+        __threadfence_system();
+        __syncwarp();
+        if (ct == 0) red_release_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);
+      }
+      B2_TRACE(kTrP1Step + i);
+      continue;
     } else {  // identity: y travels as fp32
       float* dstf = reinterpret_cast<float*>(dst);
       r.run(px, [&](const uint8_t* st, size_t e0, size_t units, int T) {
@@ -429,7 +468,9 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   for (int j = 0; j < g; ++j)
     pf.base[j] = a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride - size_t(pf.eb) * mbase;
   pf.wait_flag = &mine->arrive1;
-  pf.wait_target = (unsigned long long)g * a.epoch;
+  // arrivals per contributing rank: uint8 = every CTA's storer + header + edges;
+  // identity = the last CTA
+  pf.wait_target = (unsigned long long)g * (CODEC == kU8 ? unsigned(G) + 2u : 1u) * a.epoch;
   if (cons) {
     if (ct == 0) wait_geq(&mine->arrive1, pf.wait_target, a.timeout_ns, a.status);
     B2_TRACE(kTrP2Ready);
@@ -649,7 +690,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
   Ring r;
   r.init(smem, a.status, a.timeout_ns);
   const int G = gridDim.x, me = a.me, p = a.parity, ct = r.ct;
-  const bool cons = !r.producer;
+  const bool cons = r.ct >= 0;
   WinHdr* mine = hdr_of(a.win[me]);
   uint8_t* mybuf = a.win[me] + a.off_dbuf;
   float4* x4 = reinterpret_cast<float4*>(a.x);

@@ -52,6 +52,7 @@ struct Window {
 struct Blob {  // what each rank publishes about one window
   int pid;
   int device;
+  int grid;  // persistent grid size: per-CTA arrival counts must agree across ranks
   unsigned long long ptr;
   unsigned long long bytes;
   cudaIpcMemHandle_t handle;
@@ -149,6 +150,7 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
     Blob mine{};
     mine.pid = static_cast<int>(getpid());
     mine.device = c->device;
+    mine.grid = sm_count();
     mine.ptr = reinterpret_cast<unsigned long long>(w->local);
     mine.bytes = w->bytes;
     if (cudaIpcGetMemHandle(&mine.handle, w->local) != cudaSuccess) {
@@ -164,6 +166,11 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
       if (all[j].bytes != w->bytes) {
         set_error("rank %d window size %llu != %zu: mismatched collective arguments", j,
                   all[j].bytes, w->bytes);
+        return fail(B2_ERR_INVALID);
+      }
+      if (all[j].grid != mine.grid) {
+        set_error("rank %d runs %d CTAs per launch, rank %d runs %d: all GPUs must have the same SM count", j,
+                  all[j].grid, c->rank, mine.grid);
         return fail(B2_ERR_INVALID);
       }
       if (j == c->rank) continue;

@@ -19,12 +19,18 @@
 
 namespace b2 {
 
-constexpr int kConsumerWarps = 19;  // 20 warps = 5 per SM sub-partition at 96 regs
-constexpr int kConsumers = 32 * kConsumerWarps;          // 608 consumer threads
-constexpr int kRingThreads = kConsumers + 32;             // + 1 producer warp
-constexpr int kStages = 6;
+// Warp roles: warp 0 = producer (TMA loads), warp 1 = storer (TMA bulk
+// stores of staged payloads to peers + their completion/signalling), warps
+// 2.. = consumers.  20 warps = 5 per SM sub-partition at 96 registers.
+constexpr int kConsumerWarps = 18;
+constexpr int kConsumers = 32 * kConsumerWarps;          // 576 consumer threads
+constexpr int kFirstConsumer = 64;                        // threadIdx of consumer 0
+constexpr int kRingThreads = kConsumers + kFirstConsumer; // 640
+constexpr int kStages = 5;
 constexpr int kStageBytes = 32768;
-constexpr int kRingSmem = 256 + kStages * kStageBytes;    // barriers + ring
+constexpr int kSlots = 5;                                 // staging ring for pushed payloads
+constexpr int kSlotBytes = 8192;                          // codes of one 32 KB fp32 tile
+constexpr int kRingSmem = 256 + kStages * kStageBytes + kSlots * kSlotBytes;  // 200 KB + barriers
 constexpr int kConsumerBar = 1;                           // named barrier id
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -62,6 +68,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
+// shared -> global (local HBM or a peer's window) bulk store, tracked by the
+// issuing thread's bulk async-group
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// the smem source of every committed bulk store has been read
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// every committed bulk store has completed (its writes are performed)
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync %0, %1;" ::"n"(kConsumerBar), "n"(kConsumers) : "memory");
 }
@@ -85,20 +108,30 @@ struct PassDesc {
 struct Ring {
   uint64_t* full;
   uint64_t* empty;
+  uint64_t* staged;  // consumers -> storer: slot filled
+  uint64_t* sfree;   // storer -> consumers: slot read by the bulk store
   uint8_t* buf;
+  uint8_t* slots;
   int stage = 0;
   unsigned phase = 0;
+  int slot = 0;       // staging cursor (consumers and storer walk it in lock step)
+  unsigned sphase = 0;
   bool producer;
-  int ct;  // consumer thread index 0..kConsumers-1 (producer: -1)
+  bool storer;
+  int ct;  // consumer thread index 0..kConsumers-1 (producer / storer: -1)
   int* status;
   unsigned long long timeout_ns;
 
   __device__ void init(uint8_t* smem, int* st, unsigned long long to) {
     full = reinterpret_cast<uint64_t*>(smem);
     empty = full + kStages;
+    staged = empty + kStages;
+    sfree = staged + kSlots;
     buf = smem + 256;
+    slots = buf + size_t(kStages) * kStageBytes;
     producer = threadIdx.x < 32;
-    ct = producer ? -1 : int(threadIdx.x) - 32;
+    storer = threadIdx.x >= 32 && threadIdx.x < kFirstConsumer;
+    ct = threadIdx.x >= kFirstConsumer ? int(threadIdx.x) - kFirstConsumer : -1;
     status = st;
     timeout_ns = to;
     if (threadIdx.x == 0) {
@@ -106,9 +139,39 @@ struct Ring {
         mbar_init(full + i, 1);
         mbar_init(empty + i, kConsumerWarps);
       }
+      for (int i = 0; i < kSlots; ++i) {
+        mbar_init(staged + i, kConsumerWarps);
+        mbar_init(sfree + i, 1);
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+  }
+  __device__ __forceinline__ void advance_slot() {
+    if (++slot == kSlots) {
+      slot = 0;
+      sphase ^= 1u;
+    }
+  }
+  // consumers: wait until the current staging slot may be overwritten
+  __device__ __forceinline__ uint8_t* slot_acquire() {
+    mbar_wait(sfree + slot, sphase ^ 1u);
+    return slots + size_t(slot) * kSlotBytes;
+  }
+  // consumers: the slot is filled (every consumer thread calls this)
+  __device__ __forceinline__ void slot_commit() {
+    fence_proxy_async_smem();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(staged + slot);
+    advance_slot();
+  }
+  // storer lane 0: push the next filled slot to dst (bytes), release the slot
+  __device__ __forceinline__ void slot_push(void* dst, unsigned bytes) {
+    mbar_wait(staged + slot, sphase);
+    bulk_s2g(dst, slots + size_t(slot) * kSlotBytes, bytes);
+    bulk_wait_read_all();
+    mbar_arrive(sfree + slot);
+    advance_slot();
   }
   __device__ __forceinline__ void advance() {
     if (++stage == kStages) {
@@ -173,7 +236,7 @@ struct Ring {
     for (size_t t = 0; t < m; ++t)
       for (int i = 0; i < np; ++i)
         if (t < mm[i]) {
-          if (producer && (threadIdx.x & 31) == 0 && !w[i]) {
+          if (producer && threadIdx.x == 0 && !w[i]) {
             if (ps[i].wait_flag) {
               wait_geq(ps[i].wait_flag, ps[i].wait_target, timeout_ns, status);
               fence_proxy_async();
@@ -193,6 +256,7 @@ struct Ring {
     const size_t u0 = p.u0(), nun = p.nunits();
     const int T = p.tile_units();
     const size_t units = (nun - t * T) < size_t(T) ? (nun - t * T) : size_t(T);
+    if (storer) return;
     if (producer) {
       if ((threadIdx.x & 31) != 0) return;
       if (!waited) {
@@ -220,7 +284,7 @@ struct Ring {
   // Unaligned head/tail elements of a pass (consumer warp 0 of the last CTA).
   template <class F>
   __device__ void edges(const PassDesc& p, F&& fn) const {
-    if (producer || blockIdx.x != gridDim.x - 1 || ct >= 32) return;
+    if (ct < 0 || blockIdx.x != gridDim.x - 1 || ct >= 32) return;
     const size_t b0 = p.body_begin(), b1 = p.body_end(), e1 = p.s + p.n;
     for (size_t e = p.s + ct; e < b0; e += 32) fn(e);
     for (size_t e = b1 + ct; e < e1; e += 32) fn(e);
@@ -231,7 +295,7 @@ struct Ring {
 __device__ __forceinline__ float2 consumer_minmax(float lo, float hi, float2* smem /*[32]*/) {
   lo = warp_min_nan(lo);
   hi = warp_max_nan(hi);
-  const int w = (threadIdx.x >> 5) - 1, l = threadIdx.x & 31;
+  const int w = (threadIdx.x >> 5) - kFirstConsumer / 32, l = threadIdx.x & 31;
   consumer_sync();
   if (l == 0) smem[w] = make_float2(lo, hi);
   consumer_sync();
@@ -246,7 +310,7 @@ __device__ __forceinline__ float2 consumer_minmax(float lo, float hi, float2* sm
 __device__ __forceinline__ void consumer_grid_sync(unsigned* ws) {
   __threadfence();
   consumer_sync();
-  if (threadIdx.x == 32) {
+  if (threadIdx.x == kFirstConsumer) {
     volatile unsigned* gen = ws + 1;
     const unsigned g0 = *gen;
     if (atomicAdd(ws, 1u) == gridDim.x - 1) {
@@ -272,8 +336,8 @@ template <bool SYS>
 __device__ __forceinline__ bool consumer_arrive(unsigned* ctr, int* flag_smem,
                                                 unsigned long long* tr = nullptr) {
   fence_proxy_async();  // every writer: generic -> async-proxy (TMA readers)
-  consumer_sync();      // all consumer writes happen-before thread 32's fence
-  if (threadIdx.x == 32) {
+  consumer_sync();      // all consumer writes happen-before consumer 0's fence
+  if (threadIdx.x == kFirstConsumer) {
     if (tr) tr[0] = globaltimer();
     // one cumulative fence per CTA (the cooperative-groups grid-sync pattern)
     if (SYS)
