@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
           const size_t e0 = 16 * (px.u0() + t * T);
           r.slot_push(dst + (e0 - ebase), unsigned(units * 16));
         }
-        bulk_wait_all();  // this CTA's pushes of chunk k are performed
+        r.push_drain();  // this CTA's pushes of chunk k are performed
         fence_proxy_async();
         __threadfence_system();
         red_release_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);  // arrival: this CTA's codes

@@ -76,9 +76,10 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned by
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
-// the smem source of every committed bulk store has been read
-__device__ __forceinline__ void bulk_wait_read_all() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+// the smem source of every committed bulk store but the N most recent has been read
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 // every committed bulk store has completed (its writes are performed)
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -165,18 +166,30 @@ struct Ring {
     if ((threadIdx.x & 31) == 0) mbar_arrive(staged + slot);
     advance_slot();
   }
-  // storer lane 0: push the next filled slot to dst (bytes), release the slot
+  // storer lane 0: push the next filled slot to dst.  Up to kPushInFlight
+  // bulk stores stay in flight; a slot is released to the consumers once its
+  // store has finished reading shared memory (FIFO order).
+  static constexpr int kPushInFlight = kSlots - 1;
+  int pending = 0;    // storer: slots pushed but not yet released
+  int rel = 0;        // storer: oldest unreleased slot
   __device__ __forceinline__ void slot_push(void* dst, unsigned bytes) {
     mbar_wait(staged + slot, sphase);
     bulk_s2g(dst, slots + size_t(slot) * kSlotBytes, bytes);
-    bulk_wait_read_all();
-    mbar_arrive(sfree + slot);
     advance_slot();
+    if (++pending > kPushInFlight) {
+      bulk_wait_read<kPushInFlight>();
+      mbar_arrive(sfree + rel);
+      rel = rel + 1 == kSlots ? 0 : rel + 1;
+      --pending;
+    }
   }
-  __device__ __forceinline__ void advance() {
-    if (++stage == kStages) {
-      stage = 0;
-      phase ^= 1u;
+  // storer lane 0: every push performed (writes visible); release all slots
+  __device__ __forceinline__ void push_drain() {
+    bulk_wait_all();
+    while (pending > 0) {
+      mbar_arrive(sfree + rel);
+      rel = rel + 1 == kSlots ? 0 : rel + 1;
+      --pending;
     }
   }
 
