@@ -183,6 +183,12 @@ struct Ring {
       --pending;
     }
   }
+  __device__ __forceinline__ void advance() {
+    if (++stage == kStages) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
   // storer lane 0: every push performed (writes visible); release all slots
   __device__ __forceinline__ void push_drain() {
     bulk_wait_all();
