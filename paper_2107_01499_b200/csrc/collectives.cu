@@ -118,8 +118,7 @@ __device__ __forceinline__ void set_eps4(float* eps, size_t e, size_t lo, float4
 
 // ---------------------------------------------------------------- C_* kernel
 template <int CODEC, bool EC>
-__global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
+__device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
   __shared__ float2 red[32];
   __shared__ float s_lo[kMaxRanks], s_step[kMaxRanks];
   __shared__ SrcDec s_dec[kMaxRanks];
@@ -128,8 +127,6 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   __shared__ int s_fast;
   __shared__ int s_flag;
   __shared__ volatile int s_gate;
-  Ring r;
-  r.init(smem, a.status, a.timeout_ns);
   if (threadIdx.x == 0) s_gate = 0;
   __syncthreads();
   const int G = gridDim.x, g = a.g, me = a.me, ct = r.ct;
@@ -330,25 +327,13 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
     mhi_ = -kInf;
   };
   if (CODEC == kU8 && r.storer) {
-    // ---- storer warp: push every staged tile of every chunk (same tile order
-    // as the consumers), then wait for the writes and signal the owner.
+    // ---- storer warp: push every staged tile of every chunk (destination and
+    // size travel with the slot; a marker slot ends chunk k), then wait for
+    // the writes and signal the owner.
     if ((threadIdx.x & 31) == 0) {
       for (int i = 0; i < g; ++i) {
         const int k = (me + 1 + i) % g;
-        size_t lo, sz;
-        part_range(a.n, g, k, lo, sz);
-        PassDesc px = xpass(lo, sz);
-        px.reverse = true;
-        uint8_t* dst = a.win[k] + a.off_recv1 + size_t(me) * a.slot_stride;
-        const size_t ebase = lo & ~size_t(15);
-        const int T = px.tile_units();
-        const size_t nun = px.nunits(), nt = (nun + T - 1) / T;
-        const size_t m = nt > blockIdx.x ? (nt - blockIdx.x + G - 1) / G : 0;
-        for (size_t j = 0; j < m; ++j) {
-          const size_t t = r.tile_index(px, j, m);
-          const size_t units = (nun - t * T) < size_t(T) ? (nun - t * T) : size_t(T);
-          const size_t e0 = 16 * (px.u0() + t * T);
-          r.slot_push(dst + (e0 - ebase), unsigned(units * 16));
+        while (r.slot_push()) {
         }
         r.push_drain();  // this CTA's pushes of chunk k are performed
         fence_proxy_async();
@@ -398,7 +383,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
           sl[gi] = q;
           if (EC) dl4[(e0 >> 2) + gi] = sub4(y, dequant4(q, p));
         }
-        r.slot_commit();
+        r.slot_commit(dst + (e0 - ebase), unsigned(units * 16));
       };
       if (i + 1 < g) {  // B(k) interleaved with A(next chunk)
         const int kn = (me + 2 + i) % g;
@@ -410,6 +395,10 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
         mm_publish(kn);
       } else {
         r.run(px, push);
+      }
+      if (cons) {  // end of chunk k for the storer
+        r.slot_acquire();
+        r.slot_commit(nullptr, 0u);
       }
       r.edges(px, [&](size_t e) {
         float y = a.x[e];
@@ -679,16 +668,24 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   B2_TRACE(kTrEnd);
 }
 
+// The kernels: ring setup, the body, then the dynamic tile counters are reset
+// for the next launch on this window.
+template <int CODEC, bool EC>
+__global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  Ring r;
+  r.init(smem, a.status, a.timeout_ns, a.sched);
+  central_body<CODEC, EC>(a, r);
+  r.finish(a.sched_end);
+}
+
 // ---------------------------------------------------------------- D_* kernel
 template <int CODEC>
-__global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
+__device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
   __shared__ float2 red[32];
   __shared__ SrcDec s_dec[kMaxRanks];
   __shared__ int s_fast;
   __shared__ int s_flag;
-  Ring r;
-  r.init(smem, a.status, a.timeout_ns);
   const int G = gridDim.x, me = a.me, p = a.parity, ct = r.ct;
   const bool cons = r.ct >= 0;
   WinHdr* mine = hdr_of(a.win[me]);
@@ -862,6 +859,15 @@ __global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
     for (int i = 0; i < a.nnb; ++i)
       if (a.nbrs[i] != me) red_release_sys_add(&hdr_of(a.win[a.nbrs[i]])->dreads[p], 1ull);
   B2_TRACE(kTrEnd);
+}
+
+template <int CODEC>
+__global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  Ring r;
+  r.init(smem, a.status, a.timeout_ns, a.sched);
+  decent_body<CODEC>(a, r);
+  r.finish(a.sched_end);
 }
 
 template <typename K, typename A>

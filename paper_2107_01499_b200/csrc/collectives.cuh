@@ -58,10 +58,16 @@ struct CentralArgs {
   float2* partials;             // local workspace [(kMaxRanks + 1) * grid]
   unsigned* cta_done;           // local workspace [kMaxRanks + 2]
   unsigned* gridbar;            // local workspace [2]: consumer grid barrier
+  unsigned long long* sched;    // local workspace [kSchedPasses]: dynamic tile counters, or null
+  unsigned* sched_end;          // local workspace: CTAs finished (counter reset)
   int* status;                  // mapped host status word
   unsigned long long timeout_ns;
   unsigned long long* trace;    // [grid * kTraceSlots] globaltimer stamps, or null
 };
+
+// Dynamic tile counters per window: one per pass of a launch (C_*: at most
+// 3g+2 passes, D_*: 3), reset by the last CTA of every launch.
+constexpr int kSchedPasses = 64;
 
 // Decentralized neighbourhood reduce (D_FP_S, D_LP_S).
 struct DecentArgs {
@@ -79,6 +85,8 @@ struct DecentArgs {
   float2* partials;
   unsigned* cta_done;
   unsigned* gridbar;
+  unsigned long long* sched;
+  unsigned* sched_end;
   int* status;
   unsigned long long timeout_ns;
   unsigned long long* trace;

@@ -47,6 +47,7 @@ struct Window {
   unsigned long long exp_reads[2] = {0, 0};
   float2* partials = nullptr;
   unsigned* cta_done = nullptr;
+  unsigned long long* sched = nullptr;  // [kSchedPasses] tile counters + end counter
 };
 
 struct Blob {  // what each rank publishes about one window
@@ -97,6 +98,7 @@ void free_window(b2_comm* c, Window* w) {
   if (w->local) cudaFree(w->local);
   if (w->partials) cudaFree(w->partials);
   if (w->cta_done) cudaFree(w->cta_done);
+  if (w->sched) cudaFree(w->sched);
   delete w;
   (void)c;
 }
@@ -136,7 +138,9 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
       cudaMalloc(&w->partials, sizeof(float2) * (kMaxRanks + 1) * max_persistent_grid()) !=
           cudaSuccess ||
       cudaMalloc(&w->cta_done, sizeof(unsigned) * (kMaxRanks + 4)) != cudaSuccess ||
-      cudaMemset(w->cta_done, 0, sizeof(unsigned) * (kMaxRanks + 4)) != cudaSuccess) {
+      cudaMemset(w->cta_done, 0, sizeof(unsigned) * (kMaxRanks + 4)) != cudaSuccess ||
+      cudaMalloc(&w->sched, sizeof(unsigned long long) * (kSchedPasses + 1)) != cudaSuccess ||
+      cudaMemset(w->sched, 0, sizeof(unsigned long long) * (kSchedPasses + 1)) != cudaSuccess) {
     set_error("window allocation of %zu bytes failed: %s", w->bytes,
               cudaGetErrorString(cudaGetLastError()));
     return fail(B2_ERR_CUDA);
@@ -380,6 +384,15 @@ int b2_comm_sync(b2_comm_t c, void* stream) {
   return b2_comm_poll(c);
 }
 
+// B2_STATIC_SCHED=1: static round-robin tile assignment (A/B measurements)
+static bool static_sched() {
+  static const bool v = [] {
+    const char* e = getenv("B2_STATIC_SCHED");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite, float* delta,
                    size_t delta_len, float* eps, size_t eps_len, uint32_t bucket, void* stream) {
   int rc = check_comm(c, x, n);
@@ -412,6 +425,8 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   a.partials = w->partials;
   a.cta_done = w->cta_done;
   a.gridbar = w->cta_done + kMaxRanks + 2;
+  a.sched = static_sched() ? nullptr : w->sched;
+  a.sched_end = reinterpret_cast<unsigned*>(w->sched + kSchedPasses);
   a.status = c->status_d;
   a.timeout_ns = c->timeout_ns;
   a.trace = c->trace;
@@ -472,6 +487,8 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
   a.partials = w->partials;
   a.cta_done = w->cta_done;
   a.gridbar = w->cta_done + kMaxRanks + 2;
+  a.sched = static_sched() ? nullptr : w->sched;
+  a.sched_end = reinterpret_cast<unsigned*>(w->sched + kSchedPasses);
   a.status = c->status_d;
   a.timeout_ns = c->timeout_ns;
   a.trace = c->trace;

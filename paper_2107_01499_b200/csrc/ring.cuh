@@ -30,7 +30,7 @@ constexpr int kStages = 5;
 constexpr int kStageBytes = 32768;
 constexpr int kSlots = 5;                                 // staging ring for pushed payloads
 constexpr int kSlotBytes = 8192;                          // codes of one 32 KB fp32 tile
-constexpr int kRingSmem = 256 + kStages * kStageBytes + kSlots * kSlotBytes;  // 200 KB + barriers
+constexpr int kRingSmem = 512 + kStages * kStageBytes + kSlots * kSlotBytes;  // 200 KB + control
 constexpr int kConsumerBar = 1;                           // named barrier id
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -113,6 +113,8 @@ struct Ring {
   uint64_t* sfree;   // storer -> consumers: slot read by the bulk store
   uint8_t* buf;
   uint8_t* slots;
+  void** slot_dst;     // smem [kSlots]: push destination of a staged slot
+  unsigned* slot_len;  // smem [kSlots]: its byte count (0 = end-of-chunk marker)
   int stage = 0;
   unsigned phase = 0;
   int slot = 0;       // staging cursor (consumers and storer walk it in lock step)
@@ -120,15 +122,22 @@ struct Ring {
   bool producer;
   bool storer;
   int ct;  // consumer thread index 0..kConsumers-1 (producer / storer: -1)
+  unsigned long long* info;            // smem [kStages]: (pass << 40 | tile) of a stage, ~0 = END
+  unsigned long long* sched = nullptr;  // global per-pass tile counters (dynamic mode) or null
+  int npass = 0;                        // passes streamed so far (identical in every role)
   int* status;
   unsigned long long timeout_ns;
 
-  __device__ void init(uint8_t* smem, int* st, unsigned long long to) {
+  __device__ void init(uint8_t* smem, int* st, unsigned long long to, unsigned long long* sched_ctrs = nullptr) {
+    sched = sched_ctrs;
     full = reinterpret_cast<uint64_t*>(smem);
     empty = full + kStages;
     staged = empty + kStages;
     sfree = staged + kSlots;
-    buf = smem + 256;
+    info = reinterpret_cast<unsigned long long*>(sfree + kSlots);
+    slot_dst = reinterpret_cast<void**>(info + kStages);
+    slot_len = reinterpret_cast<unsigned*>(slot_dst + kSlots);
+    buf = smem + 512;
     slots = buf + size_t(kStages) * kStageBytes;
     producer = threadIdx.x < 32;
     storer = threadIdx.x >= 32 && threadIdx.x < kFirstConsumer;
@@ -159,22 +168,34 @@ struct Ring {
     mbar_wait(sfree + slot, sphase ^ 1u);
     return slots + size_t(slot) * kSlotBytes;
   }
-  // consumers: the slot is filled (every consumer thread calls this)
-  __device__ __forceinline__ void slot_commit() {
+  // consumers: the slot is filled (every consumer thread calls this).
+  // Consumer 0 records where the storer must push it (bytes == 0: a marker).
+  __device__ __forceinline__ void slot_commit(void* dst, unsigned bytes) {
+    if (ct == 0) {
+      slot_dst[slot] = dst;
+      slot_len[slot] = bytes;
+    }
     fence_proxy_async_smem();
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(staged + slot);
     advance_slot();
   }
-  // storer lane 0: push the next filled slot to dst.  Up to kPushInFlight
-  // bulk stores stay in flight; a slot is released to the consumers once its
-  // store has finished reading shared memory (FIFO order).
+  // storer lane 0: push the next filled slot.  Up to kPushInFlight bulk
+  // stores stay in flight; a slot is released to the consumers once its store
+  // has finished reading shared memory (FIFO order).  Returns false (and
+  // consumes the slot) on a marker.
   static constexpr int kPushInFlight = kSlots - 1;
   int pending = 0;    // storer: slots pushed but not yet released
   int rel = 0;        // storer: oldest unreleased slot
-  __device__ __forceinline__ void slot_push(void* dst, unsigned bytes) {
+  __device__ __forceinline__ bool slot_push() {
     mbar_wait(staged + slot, sphase);
-    bulk_s2g(dst, slots + size_t(slot) * kSlotBytes, bytes);
+    const unsigned bytes = slot_len[slot];
+    if (bytes == 0) {  // marker: release it in FIFO order too
+      advance_slot();
+      ++pending;
+      return false;
+    }
+    bulk_s2g(slot_dst[slot], slots + size_t(slot) * kSlotBytes, bytes);
     advance_slot();
     if (++pending > kPushInFlight) {
       bulk_wait_read<kPushInFlight>();
@@ -182,6 +203,7 @@ struct Ring {
       rel = rel + 1 == kSlots ? 0 : rel + 1;
       --pending;
     }
+    return true;
   }
   __device__ __forceinline__ void advance() {
     if (++stage == kStages) {
@@ -199,105 +221,165 @@ struct Ring {
     }
   }
 
+  // ---------------------------------------------------------------- passes
   // Stream one pass.  consume(stage_ptr, first_element, units, tile_units)
-  // runs on every consumer thread for every tile this CTA owns.
+  // runs on every consumer thread for every tile handed to this CTA.
   template <class F>
   __device__ void run(const PassDesc& p, F&& consume) {
-    const int T = p.tile_units();
-    const size_t ntiles = (p.nunits() + T - 1) / T;
-    const size_t m = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    bool waited = p.wait_flag == nullptr;
-    for (size_t i = 0; i < m; ++i) tile(p, tile_index(p, i, m), consume, waited);
-  }
-  __device__ __forceinline__ size_t tile_index(const PassDesc& p, size_t i, size_t m) const {
-    return blockIdx.x + (p.reverse ? m - 1 - i : i) * gridDim.x;
+    stream(&p, 1, [&](int, const uint8_t* st, size_t e0, size_t units, int T) { consume(st, e0, units, T); },
+           [](int) {});
   }
 
-  // Stream two passes with their tiles interleaved (a0 b0 a1 b1 ...), so e.g.
-  // an NVLink-bound push pass overlaps an HBM-bound min/max pass.
+  // Two passes with their tiles interleaved (a b a b ...), so e.g. an
+  // NVLink-bound push pass overlaps an HBM-bound min/max pass.
   template <class FA, class FB>
   __device__ void run2(const PassDesc& pa, FA&& fa, const PassDesc& pb, FB&& fb) {
-    const int Ta = pa.tile_units(), Tb = pb.tile_units();
-    const size_t na = (pa.nunits() + Ta - 1) / Ta, nb = (pb.nunits() + Tb - 1) / Tb;
-    const size_t ma = na > blockIdx.x ? (na - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const size_t mb = nb > blockIdx.x ? (nb - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const size_t m = ma > mb ? ma : mb;
-    bool wa = pa.wait_flag == nullptr, wb = pb.wait_flag == nullptr;
-    for (size_t i = 0; i < m; ++i) {
-      if (i < ma) tile(pa, tile_index(pa, i, ma), fa, wa);
-      if (i < mb) tile(pb, tile_index(pb, i, mb), fb, wb);
-    }
+    const PassDesc ps[2] = {pa, pb};
+    stream(ps, 2,
+           [&](int i, const uint8_t* st, size_t e0, size_t units, int T) {
+             if (i == 0)
+               fa(st, e0, units, T);
+             else
+               fb(st, e0, units, T);
+           },
+           [](int) {});
   }
 
-  // Stream np passes with their tiles interleaved round-robin (pass 0 tile 0,
-  // pass 1 tile 0, ..., pass 0 tile 1, ...): e.g. pull every owner's payload
-  // at once, which keeps NVLink fan-in balanced whatever the rank skew.
+  // np passes interleaved round-robin: e.g. pull every owner's payload at
+  // once (balanced NVLink fan-in whatever the rank skew).  ready(i) runs on
+  // the producer lane after pass i's wait flag is satisfied and before its
+  // first tile is handed over, so what it writes to shared memory (e.g. the
+  // pass's codec header) is visible to the consumers of all of pass i's tiles.
   template <class F>
   __device__ void run_multi(const PassDesc* ps, int np, F&& consume) {
-    run_multi(ps, np, consume, [](int) {});
+    stream(ps, np, consume, [](int) {});
   }
-  // ready(i) runs on the producer lane right after pass i's wait flag is
-  // satisfied and before its first tile is handed over, so anything it writes
-  // to shared memory (e.g. the pass's codec header) is visible to the
-  // consumers of every tile of pass i (mbarrier release/acquire).
   template <class F, class R>
   __device__ void run_multi(const PassDesc* ps, int np, F&& consume, R&& ready) {
-    size_t mm[kMaxRanks];
-    bool w[kMaxRanks];
-    size_t m = 0;
-    for (int i = 0; i < np; ++i) {
-      const int T = ps[i].tile_units();
-      const size_t nt = (ps[i].nunits() + T - 1) / T;
-      mm[i] = nt > blockIdx.x ? (nt - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-      m = mm[i] > m ? mm[i] : m;
-      w[i] = false;
-    }
-    for (size_t t = 0; t < m; ++t)
-      for (int i = 0; i < np; ++i)
-        if (t < mm[i]) {
-          if (producer && threadIdx.x == 0 && !w[i]) {
-            if (ps[i].wait_flag) {
-              wait_geq(ps[i].wait_flag, ps[i].wait_target, timeout_ns, status);
-              fence_proxy_async();
-            }
-            ready(i);
-          }
-          w[i] = true;
-          tile(ps[i], tile_index(ps[i], t, mm[i]),
-               [&](const uint8_t* st, size_t e0, size_t units, int T) { consume(i, st, e0, units, T); }, w[i]);
-        }
+    stream(ps, np, consume, ready);
   }
 
-  // One tile of a pass (producer lane 0 issues, consumers consume).  The
-  // producer honours the pass's wait flag before its first tile (`waited`).
-  template <class F>
-  __device__ __forceinline__ void tile(const PassDesc& p, size_t t, F&& consume, bool& waited) {
-    const size_t u0 = p.u0(), nun = p.nunits();
-    const int T = p.tile_units();
-    const size_t units = (nun - t * T) < size_t(T) ? (nun - t * T) : size_t(T);
+  // The scheduler.  Static mode (sched == nullptr): CTA b takes tiles b, b+G,
+  // ... of every pass.  Dynamic mode: the producer lane grabs tiles from one
+  // global counter per pass (atomicAdd), so fast SMs take more tiles and every
+  // CTA finishes a pass at about the same time -- static assignment left a
+  // 10-20 us spread per pass, and every grid barrier waits for the slowest
+  // CTA.  Reverse passes hand tiles out from the END (the producer maps the
+  // counter c to ntiles-1-c), which is what makes a reverse re-read hit L2.
+  // The stage's tile (or the END marker) travels to the consumers in shared
+  // memory (info[]), published by the mbarrier arrive.
+  template <class F, class R>
+  __device__ void stream(const PassDesc* ps, int np, F&& consume, R&& ready) {
+    const int pid0 = npass;
+    npass += np;
     if (storer) return;
     if (producer) {
       if ((threadIdx.x & 31) != 0) return;
-      if (!waited) {
-        wait_geq(p.wait_flag, p.wait_target, timeout_ns, status);
-        fence_proxy_async();
-        waited = true;
+      bool live[kMaxRanks], got[kMaxRanks];
+      size_t nt[kMaxRanks], k[kMaxRanks];
+      int nlive = 0;
+      for (int i = 0; i < np; ++i) {
+        const int T = ps[i].tile_units();
+        nt[i] = (ps[i].nunits() + T - 1) / T;
+        k[i] = 0;
+        got[i] = false;
+        live[i] = nt[i] > (sched ? 0 : blockIdx.x);
+        nlive += live[i];
       }
-      mbar_wait(empty + stage, phase ^ 1u);
-      const unsigned bytes = unsigned(units * 16 * p.eb);
-      mbar_expect_tx(full + stage, bytes * p.nsrc);
-      uint8_t* dst = buf + size_t(stage) * kStageBytes;
-      const size_t off = size_t(p.eb) * 16 * (u0 + t * T);
-      for (int i = 0; i < p.nsrc; ++i)
-        bulk_g2s(dst + size_t(i) * T * 16 * p.eb, p.base[i] + off, bytes, full + stage);
+      int nready = 0;
+      while (nlive) {
+        for (int i = 0; i < np; ++i) {
+          if (!live[i]) continue;
+          if (!got[i]) {
+            // A pass whose data is not published yet is skipped while another
+            // pass has tiles to hand out; with nothing else to do, block.
+            if (ps[i].wait_flag && ld_acquire_sys(ps[i].wait_flag) < ps[i].wait_target) {
+              if (nready > 0) continue;
+              wait_geq(ps[i].wait_flag, ps[i].wait_target, timeout_ns, status);
+            }
+            if (ps[i].wait_flag) fence_proxy_async();
+            ready(i);
+            got[i] = true;
+            ++nready;
+          }
+          size_t t;
+          if (sched) {
+            const unsigned long long c = atomicAdd(sched + pid0 + i, 1ull);
+            if (c >= nt[i]) {
+              live[i] = false;
+              --nlive;
+              --nready;
+              continue;
+            }
+            t = ps[i].reverse ? nt[i] - 1 - c : c;
+          } else {
+            const size_t m = (nt[i] - blockIdx.x + gridDim.x - 1) / gridDim.x;
+            const size_t j = k[i]++;
+            t = blockIdx.x + (ps[i].reverse ? m - 1 - j : j) * gridDim.x;
+            if (k[i] == m) {
+              live[i] = false;
+              --nlive;
+              --nready;
+            }
+          }
+          issue(ps[i], i, t);
+        }
+      }
+      mbar_wait(empty + stage, phase ^ 1u);  // END marker
+      info[stage] = ~0ull;
+      mbar_arrive(full + stage);
       advance();
       return;
     }
-    mbar_wait(full + stage, phase);
-    consume(buf + size_t(stage) * kStageBytes, 16 * (u0 + t * T), units, T);
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(empty + stage);
+    while (true) {
+      mbar_wait(full + stage, phase);
+      const unsigned long long inf = info[stage];
+      if (inf == ~0ull) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(empty + stage);
+        advance();
+        break;
+      }
+      const int i = int(inf >> 40);
+      const size_t t = size_t(inf & ((1ull << 40) - 1));
+      const PassDesc& p = ps[i];
+      const int T = p.tile_units();
+      const size_t nun = p.nunits();
+      const size_t units = (nun - t * T) < size_t(T) ? (nun - t * T) : size_t(T);
+      consume(i, buf + size_t(stage) * kStageBytes, 16 * (p.u0() + t * T), units, T);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(empty + stage);
+      advance();
+    }
+  }
+
+  // producer lane: load tile t of pass p (index i) into the next stage
+  __device__ __forceinline__ void issue(const PassDesc& p, int i, size_t t) {
+    const size_t nun = p.nunits();
+    const int T = p.tile_units();
+    const size_t units = (nun - t * T) < size_t(T) ? (nun - t * T) : size_t(T);
+    mbar_wait(empty + stage, phase ^ 1u);
+    info[stage] = (static_cast<unsigned long long>(i) << 40) | t;
+    const unsigned bytes = unsigned(units * 16 * p.eb);
+    mbar_expect_tx(full + stage, bytes * p.nsrc);
+    uint8_t* dst = buf + size_t(stage) * kStageBytes;
+    const size_t off = size_t(p.eb) * 16 * (p.u0() + t * T);
+    for (int s = 0; s < p.nsrc; ++s) bulk_g2s(dst + size_t(s) * T * 16 * p.eb, p.base[s] + off, bytes, full + stage);
     advance();
+  }
+
+  // Kernel epilogue (all threads): the last CTA resets the dynamic tile
+  // counters for the next launch on this workspace.
+  __device__ void finish(unsigned* end_ctr) {
+    __syncthreads();
+    if (sched && threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(end_ctr, 1u) == gridDim.x - 1) {
+        for (int i = 0; i < npass; ++i) sched[i] = 0ull;
+        *end_ctr = 0u;
+        __threadfence();
+      }
+    }
   }
 
   // Unaligned head/tail elements of a pass (consumer warp 0 of the last CTA).
