@@ -175,6 +175,10 @@ class B200Endpoint:
     TRACE_POINTS = ("start", "p1_first_minmax", "p1_first_push", "p1_done", "p2_ready", "p2_minmax",
                     "p2_done", "p3_first", "end", "p2_pass") + tuple(f"p1_step{i}" for i in range(8)) + tuple(
                     f"p1_fenced{i}" for i in range(8))
+    # accumulated waits (ns -> us, not timestamps) of the traced stream:
+    # consumers on a free staging slot, producer on arrival gates, producer on
+    # a free stage, storer retiring pushes, consumers on a full stage
+    WAIT_POINTS = ("w_slot", "w_gate", "w_empty", "w_retire", "w_full", "w_other")
 
     def enable_trace(self, on: bool = True) -> None:
         check(lib.b2_comm_enable_trace(self._h, int(on)))
@@ -194,6 +198,11 @@ class B200Endpoint:
         if raw:
             return _np.where(t > 0, (t - t0) / 1e3, _np.nan)
         out = {}
+        for i, name in enumerate(self.WAIT_POINTS):
+            col = t[:, 26 + i]
+            col = col[col > 0]
+            if col.size:
+                out[name] = (round(float(_np.median(col)) / 1e3, 2), round(float(col.max()) / 1e3, 2))
         for i, name in enumerate(self.TRACE_POINTS):
             col = t[:, i]
             col = col[col > 0]

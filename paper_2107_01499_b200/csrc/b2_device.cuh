@@ -14,6 +14,8 @@ namespace b2 {
 
 constexpr int kThreads = 512;     // threads per CTA for every persistent kernel
 constexpr int kMaxRanks = 8;
+// 16-byte units per arrival region of a gated pass (ring.cuh PassDesc::gate)
+constexpr int kGateUnits = 2048;
 
 // ------------------------------------------------------------ float helpers
 
@@ -173,6 +175,10 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
 __device__ __forceinline__ void red_release_sys_add(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void red_relaxed_sys_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) encode_ring_kernel(const floa
     keys[1] = 0u;
   }
   grid.sync();
-  PassDesc p;
+  PassDesc p = PassDesc::make();
   p.s = 0;
   p.n = n;
   p.eb = 4;
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) decode_ring_kernel(const uint
   Ring r;
   r.init(smem, nullptr, 0);
   const U8Params q = u8_params(hdr[0], hdr[1]);
-  PassDesc p;
+  PassDesc p = PassDesc::make();
   p.s = 0;
   p.n = n;
   p.eb = 1;

@@ -123,21 +123,32 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
   __shared__ float s_lo[kMaxRanks], s_step[kMaxRanks];
   __shared__ SrcDec s_dec[kMaxRanks];
   __shared__ SrcDec s_dec3[kMaxRanks];  // phase-3 owner headers (written by the producer)
+  __shared__ U8Params s_p1[kMaxRanks];   // phase-1 params of chunk pass i
+  __shared__ float2 s_mm1[kMaxRanks];
   __shared__ int s_fast3[kMaxRanks];
   __shared__ int s_fast;
   __shared__ int s_flag;
   __shared__ volatile int s_gate;
-  if (threadIdx.x == 0) s_gate = 0;
-  __syncthreads();
+  // Pass tables live in shared memory, written once by thread 0: a
+  // PassDesc is 128 bytes and per-thread copies would cost local-memory
+  // traffic for all 640 threads of every CTA.
+  __shared__ PassDesc s_pc[kMaxRanks];      // chunk (me+1+i)%g, forward (phase 1A / identity push)
+  __shared__ PassDesc s_pq[kMaxRanks + 1];  // uint8 phase 1B: the chunks reversed; [g]: my fold
+  __shared__ PassDesc s_pp[kMaxRanks];      // phase 3: owner (me+1+i)%g's payload
+  __shared__ PassDesc s_m[3];               // g=1: all of x, reversed, codes; g>1: [1] = y2 cache
   const int G = gridDim.x, g = a.g, me = a.me, ct = r.ct;
   const bool cons = r.ct >= 0;
   float4* x4 = reinterpret_cast<float4*>(a.x);
   float4* dl4 = reinterpret_cast<float4*>(a.delta);
   int bad = 0;
-  B2_TRACE(kTrStart);
+  size_t mlo, msz;
+  part_range(a.n, g, me, mlo, msz);
+  WinHdr* mine = hdr_of(a.win[me]);
+  const size_t mbase = mlo & ~size_t(15);
+  const unsigned long long gmul = (unsigned long long)g * a.epoch;
 
   auto xpass = [&](size_t lo, size_t sz) {
-    PassDesc p;
+    PassDesc p = PassDesc::make();
     p.s = lo;
     p.n = sz;
     p.eb = 4;
@@ -146,6 +157,51 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     if (EC) p.base[1] = reinterpret_cast<const uint8_t*>(a.delta);
     return p;
   };
+  if (threadIdx.x == 0) {
+    s_gate = 0;
+    s_m[0] = xpass(0, a.n);
+    s_m[1] = g == 1 ? s_m[0] : xpass(mlo, msz);
+    s_m[1].reverse = true;
+    if (g > 1) s_m[1].nsrc = 1;
+    s_m[2] = s_m[0];
+    s_m[2].eb = 1;
+    s_m[2].nsrc = 1;
+    s_m[2].base[0] = a.win[0] + a.off_recv1;  // g=1 EC: element e -> codes[e]
+    for (int i = 0; i < g; ++i) {
+      const int k = (me + 1 + i) % g;  // i == g-1: my own chunk
+      size_t lo, sz;
+      part_range(a.n, g, k, lo, sz);
+      s_pc[i] = xpass(lo, sz);
+      s_pq[i] = s_pc[i];
+      s_pq[i].reverse = CODEC == kU8;  // re-read backwards: the tails are in L2
+      PassDesc& pp = s_pp[i];
+      pp = PassDesc::make();
+      pp.s = lo;
+      pp.n = sz;
+      pp.eb = CODEC == kU8 ? 1 : 4;
+      pp.nsrc = 1;
+      pp.base[0] = a.win[k] + a.off_out2 - size_t(pp.eb) * (lo & ~size_t(15));
+      pp.wait_flag = &hdr_of(a.win[k])->ready2;
+      pp.wait_target = a.epoch;
+    }
+    PassDesc& pf = s_pq[g];  // my fold: the g contributions to my chunk
+    pf = PassDesc::make();
+    pf.s = mlo;
+    pf.n = msz;
+    pf.eb = CODEC == kU8 ? 1 : 4;
+    pf.nsrc = g;
+    for (int j = 0; j < g; ++j)
+      pf.base[j] = a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride - size_t(pf.eb) * mbase;
+    pf.wait_flag = &mine->arrive1;  // uint8: every rank's header; identity: every rank's data
+    pf.wait_target = gmul;
+    if (CODEC == kU8) {  // uint8: each tile waits for its region's g contributions
+      pf.gate = reinterpret_cast<const unsigned long long*>(a.win[me] + a.off_gate);
+      pf.gate_mult = gmul;
+      pf.reverse = true;
+    }
+  }
+  __syncthreads();
+  B2_TRACE(kTrStart);
   // minmax pass over y = x (- delta) of [lo, lo+sz) -> partial slot
   auto minmax_pass = [&](const PassDesc& p, int slot) {
     float lo = kInf, hi = -kInf;
@@ -179,7 +235,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     // (0 at the minimum element, 255 at the maximum; all 0 when degenerate),
     // so the second header is (D1(0), D1(qmax)) without a pass and the output
     // D2(Q2(D1(q1))) is a function of q1 alone: two passes, 12 N bytes.
-    const PassDesc px = xpass(0, a.n);
+    const PassDesc& px = s_m[0];
     minmax_pass(px, 0);
     U8Params p1{}, p2{};
     if (cons) {
@@ -196,8 +252,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
           latch(a.status, kStatusNonFinite);
       }
     }
-    PassDesc pb = px;
-    pb.reverse = true;  // the tail of x that pass A just read is still in L2
+    const PassDesc& pb = s_m[1];  // reversed: the tail of x that pass A just read is still in L2
     r.run(pb, [&](const uint8_t* st, size_t e0, size_t units, int) {
       const float4* xs = reinterpret_cast<const float4*>(st);
       for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
@@ -214,7 +269,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
   }
   if (CODEC == kU8 && g == 1) {
     // ------------------------------------------------ single rank, error feedback
-    const PassDesc px = xpass(0, a.n);
+    const PassDesc& px = s_m[0];
     minmax_pass(px, 0);
     float2 mm1 = make_float2(0.f, 0.f);
     U8Params p1{};
@@ -268,12 +323,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
       }
       if (ct == 0) s_gate = 1;  // codes of every CTA are written: release the producer
     }
-    PassDesc pc;
-    pc.s = 0;
-    pc.n = a.n;
-    pc.eb = 1;
-    pc.nsrc = 1;
-    pc.base[0] = codes;
+    const PassDesc& pc = s_m[2];  // the codes
     if (r.producer && (threadIdx.x & 31) == 0) gate_wait(&s_gate, 1);
     r.run(pc, [&](const uint8_t* st, size_t e0, size_t units, int) {
       const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
@@ -297,186 +347,10 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     return;
   }
 
-  // ------------------------------------------------------ phase 1: encode + push
-  // uint8: A(k0) | B(k0)+A(k1) | B(k1)+A(k2) | ... | B(k_last), one consumer
-  // grid barrier after each segment to finalise the next chunk's (min, max).
-  // Step i pushes to owner me+1+i: a permutation of destinations across ranks.
-  float mlo_ = kInf, mhi_ = -kInf;  // running (min, max) of the chunk in pass A
-  auto mm_consume = [&](const uint8_t* st, size_t, size_t units, int T) {
-    const float4* xs = reinterpret_cast<const float4*>(st);
-    const float4* ds = reinterpret_cast<const float4*>(st + size_t(T) * 64);
-    for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
-      float4 v = xs[gi];
-      if (EC) v = sub4(v, ds[gi]);
-      mm_acc(mlo_, mhi_, v);
-    }
-  };
-  auto mm_edges = [&](const PassDesc& p) {
-    r.edges(p, [&](size_t e) {
-      float v = a.x[e];
-      if (EC) v = __fsub_rn(v, a.delta[e]);
-      mm_acc1(mlo_, mhi_, v);
-    });
-  };
-  auto mm_publish = [&](int slot) {  // per-CTA partial of the finished pass A
-    if (cons) {
-      const float2 mm = consumer_minmax(mlo_, mhi_, red);
-      if (ct == 0) a.partials[size_t(slot) * G + blockIdx.x] = mm;
-    }
-    mlo_ = kInf;
-    mhi_ = -kInf;
-  };
-  if (CODEC == kU8 && r.storer) {
-    // ---- storer warp: push every staged tile of every chunk (destination and
-    // size travel with the slot; a marker slot ends chunk k), then wait for
-    // the writes and signal the owner.
-    if ((threadIdx.x & 31) == 0) {
-      for (int i = 0; i < g; ++i) {
-        const int k = (me + 1 + i) % g;
-        while (r.slot_push()) {
-        }
-        r.push_drain();  // this CTA's pushes of chunk k are performed
-        fence_proxy_async();
-        __threadfence_system();
-        red_release_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);  // arrival: this CTA's codes
-      }
-    }
-  } else if (CODEC == kU8) {
-    size_t lo0, sz0;
-    part_range(a.n, g, (me + 1) % g, lo0, sz0);
-    const PassDesc p0 = xpass(lo0, sz0);
-    r.run(p0, mm_consume);
-    mm_edges(p0);
-    mm_publish((me + 1) % g);
-  }
-  for (int i = 0; i < g && !(CODEC == kU8 && r.storer); ++i) {
-    const int k = (me + 1 + i) % g;
-    size_t lo, sz;
-    part_range(a.n, g, k, lo, sz);
-    PassDesc px = xpass(lo, sz);
-    px.reverse = CODEC == kU8;  // re-read chunk k backwards: its tail is L2-resident
-    uint8_t* dst = a.win[k] + a.off_recv1 + size_t(me) * a.slot_stride;
-    const size_t ebase = lo & ~size_t(15);  // slot element index = e - ebase
-    if (CODEC == kU8) {
-      U8Params p{};
-      if (cons) {
-        const float2 mm = finish_minmax(k);
-        if (i == 0) B2_TRACE(kTrP1FirstA);
-        p = u8_params(mm.x, mm.y);
-        if (blockIdx.x == 0 && ct == 0) {
-          hdr_of(a.win[k])->hdr1[me] = mm;  // remote 8-byte store into owner k's header
-          if (sz && !(finite_f(mm.x) && finite_f(mm.y))) latch(a.status, kStatusNonFinite);
-          __threadfence_system();
-          red_release_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);  // arrival: header
-        }
-      }
-      // codes go to a staging slot; the storer warp pushes it with a TMA bulk
-      // store and signals the owner, so consumers never wait on NVLink drain
-      auto push = [&](const uint8_t* st, size_t e0, size_t units, int T) {
-        const float4* xs = reinterpret_cast<const float4*>(st);
-        const float4* ds = reinterpret_cast<const float4*>(st + size_t(T) * 64);
-        uint32_t* sl = reinterpret_cast<uint32_t*>(r.slot_acquire());
-        for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
-          float4 y = xs[gi];
-          if (EC) y = sub4(y, ds[gi]);
-          const uint32_t q = quantize4(y, p.lo, p.inv);
-          sl[gi] = q;
-          if (EC) dl4[(e0 >> 2) + gi] = sub4(y, dequant4(q, p));
-        }
-        r.slot_commit(dst + (e0 - ebase), unsigned(units * 16));
-      };
-      if (i + 1 < g) {  // B(k) interleaved with A(next chunk)
-        const int kn = (me + 2 + i) % g;
-        size_t lon, szn;
-        part_range(a.n, g, kn, lon, szn);
-        const PassDesc pn = xpass(lon, szn);
-        r.run2(px, push, pn, mm_consume);
-        mm_edges(pn);
-        mm_publish(kn);
-      } else {
-        r.run(px, push);
-      }
-      if (cons) {  // end of chunk k for the storer
-        r.slot_acquire();
-        r.slot_commit(nullptr, 0u);
-      }
-      r.edges(px, [&](size_t e) {
-        float y = a.x[e];
-        if (EC) y = __fsub_rn(y, a.delta[e]);
-        const uint8_t q = quantize1(y, p.lo, p.inv);
-        dst[e - ebase] = q;
-        if (EC) a.delta[e] = __fsub_rn(y, dequant1(q, p.lo, p.step));
-      });
-      if (cons && blockIdx.x == G - 1 && ct < 32) {  // arrival: unaligned head/tail codes
-        __threadfence_system();
-        __syncwarp();
-        if (ct == 0) red_release_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);
-      }
-      B2_TRACE(kTrP1Step + i);
-      continue;
-    } else {  // identity: y travels as fp32
-      float* dstf = reinterpret_cast<float*>(dst);
-      r.run(px, [&](const uint8_t* st, size_t e0, size_t units, int T) {
-        const float4* xs = reinterpret_cast<const float4*>(st);
-        const float4* ds = reinterpret_cast<const float4*>(st + size_t(T) * 64);
-        for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
-          float4 y = xs[gi];
-          if (EC) y = sub4(y, ds[gi]);
-          const size_t e = e0 + 4 * size_t(gi);
-          *reinterpret_cast<float4*>(dstf + (e - ebase)) = y;
-          if (a.check_finite) bad |= !finite4(y);
-          if (EC) dl4[e >> 2] = sub4(y, y);
-        }
-      });
-      r.edges(px, [&](size_t e) {
-        float y = a.x[e];
-        if (EC) y = __fsub_rn(y, a.delta[e]);
-        dstf[e - ebase] = y;
-        if (a.check_finite) bad |= !finite_f(y);
-        if (EC) a.delta[e] = __fsub_rn(y, y);
-      });
-    }
-    if (i == 0) B2_TRACE(kTrP1FirstB);
-    B2_TRACE(kTrP1Step + i);
-    if (cons && consumer_arrive<true>(a.cta_done + k, &s_flag) && ct == 0)
-      red_release_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);
-    B2_TRACE(kTrP1Fenced + i);
-  }
-  B2_TRACE(kTrP1Done);
-
-  // ------------------------------------------------------ phase 2: owner reduce
-  size_t mlo, msz;
-  part_range(a.n, g, me, mlo, msz);
-  WinHdr* mine = hdr_of(a.win[me]);
-  const size_t mbase = mlo & ~size_t(15);
-  PassDesc pf;
-  pf.s = mlo;
-  pf.n = msz;
-  pf.eb = CODEC == kU8 ? 1 : 4;
-  pf.nsrc = g;
-  for (int j = 0; j < g; ++j)
-    pf.base[j] = a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride - size_t(pf.eb) * mbase;
-  pf.wait_flag = &mine->arrive1;
-  // arrivals per contributing rank: uint8 = every CTA's storer + header + edges;
-  // identity = the last CTA
-  pf.wait_target = (unsigned long long)g * (CODEC == kU8 ? unsigned(G) + 2u : 1u) * a.epoch;
-  if (cons) {
-    if (ct == 0) wait_geq(&mine->arrive1, pf.wait_target, a.timeout_ns, a.status);
-    B2_TRACE(kTrP2Ready);
-    consumer_sync();
-    if (ct == 0) s_fast = 1;
-    consumer_sync();
-    if (CODEC == kU8 && ct < g) {
-      const float2 h = __ldcg(&mine->hdr1[ct]);
-      const U8Params q = u8_params(h.x, h.y);
-      s_dec[ct] = SrcDec{q.lo, q.step, q.c23};
-      if (!(q.fastdec && fold_fast_ok(q.lo, q.step))) s_fast = 0;
-    }
-    consumer_sync();
-  }
-  const bool fast = s_fast != 0;
+  // ------------------------------------------------------ phase 1 / 2 common
+  const PassDesc& pf = s_pq[g];  // my fold
   // pairs of aligned groups through the fold (8 fp64 chains per thread)
-  auto fold_pairs = [&](const uint8_t* st, size_t units, int T, auto&& body) {
+  auto fold_pairs = [&](const uint8_t* st, size_t units, int T, bool fast, auto&& body) {
     const int ng = int(units * 4);
     for (int gi = ct; gi < ng; gi += 2 * kConsumers) {
       const int g1 = gi + kConsumers;
@@ -498,28 +372,180 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     return __double2float_rn(acc);
   };
   uint8_t* out2 = a.win[me] + a.off_out2;
-  // g >= 2: one fold pass, y2 cached in x's own chunk (the fold is issue-bound,
-  // re-reading 4N/g bytes is cheaper than re-folding N contributions)
-  const bool cache = g >= 2;
+  // chunk k = (me+1+i) % g for pass i; i == g-1 is my own chunk
+  const PassDesc* pc = s_pc;
+  auto ck = [&](int i) { return i + me + 1 < g ? i + me + 1 : i + me + 1 - g; };
+
   if (CODEC == kU8) {
-    float lo = kInf, hi = -kInf;
-    r.run(pf, [&](const uint8_t* st, size_t e0, size_t units, int T) {
-      fold_pairs(st, units, T, [&](int gi, float4 y) {
-        const size_t e = e0 + 4 * size_t(gi);
-        if (EC) y = sub4(y, eps4(a.eps, e, mlo));
-        if (cache) x4[e >> 2] = y;  // x's own chunk is dead after phase 1: cache y2 there
-        mm_acc(lo, hi, y);
+    // ---------------------------------------- phase 1A: (min, max) of every chunk
+    // One pass over x with the chunks' tiles interleaved; per-chunk partials,
+    // one grid barrier, then CTA 0 sends each owner its header.
+    float cl[kMaxRanks], ch[kMaxRanks];
+#pragma unroll
+    for (int j = 0; j < kMaxRanks; ++j) {
+      cl[j] = kInf;
+      ch[j] = -kInf;
+    }
+    r.run_multi(pc, g, [&](int i, const uint8_t* st, size_t, size_t units, int T) {
+      const float4* xs = reinterpret_cast<const float4*>(st);
+      const float4* ds = reinterpret_cast<const float4*>(st + size_t(T) * 64);
+      float lo = kInf, hi = -kInf;
+      for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
+        float4 v = xs[gi];
+        if (EC) v = sub4(v, ds[gi]);
+        mm_acc(lo, hi, v);
+      }
+#pragma unroll
+      for (int j = 0; j < kMaxRanks; ++j)
+        if (j == i) {
+          cl[j] = fmin_nan(cl[j], lo);
+          ch[j] = fmax_nan(ch[j], hi);
+        }
+    });
+#pragma unroll
+    for (int j = 0; j < kMaxRanks; ++j)
+      if (j < g)
+        r.edges(pc[j], [&](size_t e) {
+          float v = a.x[e];
+          if (EC) v = __fsub_rn(v, a.delta[e]);
+          mm_acc1(cl[j], ch[j], v);
+        });
+    if (cons) {
+#pragma unroll
+      for (int j = 0; j < kMaxRanks; ++j)
+        if (j < g) {
+          const float2 mm = consumer_minmax(cl[j], ch[j], red);
+          if (ct == 0) a.partials[size_t(j) * G + blockIdx.x] = mm;
+        }
+      consumer_grid_sync(a.gridbar);
+      for (int j = 0; j < g; ++j) {
+        const float2 mm = reduce_partials(a.partials + size_t(j) * G, G, red, ct);
+        if (ct == 0) {
+          s_mm1[j] = mm;
+          s_p1[j] = u8_params(mm.x, mm.y);
+        }
+      }
+      B2_TRACE(kTrP1FirstA);
+      if (blockIdx.x == 0 && ct == 0) {
+        for (int j = 0; j < g; ++j) {
+          hdr_of(a.win[ck(j)])->hdr1[me] = s_mm1[j];  // remote 8-byte store into owner's header
+          if (pc[j].n && !(finite_f(s_mm1[j].x) && finite_f(s_mm1[j].y))) latch(a.status, kStatusNonFinite);
+        }
+        __threadfence_system();
+        for (int j = 0; j < g; ++j) red_release_sys_add(&hdr_of(a.win[ck(j)])->arrive1, 1ull);
+      }
+      consumer_sync();
+    }
+
+    // ------------------------- phase 1B + 2A: push every chunk, fold as it lands
+    // Pass i < g quantizes chunk ck(i) straight into owner ck(i)'s window;
+    // the signaller warp confirms the stores (one system fence per batch of
+    // tiles) and adds each tile's units to the owner's region counter.  Pass g is my fold: each
+    // tile waits for its region to hold all g contributions, so the fold runs
+    // under the all-to-all instead of after it.  Chunks are walked backwards
+    // (their tails are still in L2 from phase 1A).
+    auto load_dec = [&]() {  // contribution headers -> smem (one thread)
+      int fast = 1;
+      for (int j = 0; j < g; ++j) {
+        const float2 h = __ldcg(&mine->hdr1[j]);
+        const U8Params q = u8_params(h.x, h.y);
+        s_dec[j] = SrcDec{q.lo, q.step, q.c23};
+        if (!(q.fastdec && fold_fast_ok(q.lo, q.step))) fast = 0;
+      }
+      s_fast = fast;
+    };
+    r.timed = a.trace != nullptr;
+    if (r.storer && (threadIdx.x & 31) == 0) {
+      r.signal_loop();
+      if (a.trace) {
+        a.trace[size_t(blockIdx.x) * kTraceSlots + kTrP1Step + 1] = globaltimer();  // pushes landed
+        a.trace[size_t(blockIdx.x) * kTraceSlots + kTrWait + 3] = r.wt[1];           // storer: retiring
+      }
+    }
+    float lo2 = kInf, hi2 = -kInf;
+    r.run_multi(
+        s_pq, g + 1,
+        [&](int i, const uint8_t* st, size_t e0, size_t units, int T) {
+          if (i < g) {
+            const int k = ck(i);
+            const U8Params p = s_p1[i];
+            const float4* xs = reinterpret_cast<const float4*>(st);
+            const float4* ds = reinterpret_cast<const float4*>(st + size_t(T) * 64);
+            uint32_t* dst = reinterpret_cast<uint32_t*>(a.win[k] + a.off_recv1 + size_t(me) * a.slot_stride +
+                                                        (e0 - (pc[i].s & ~size_t(15))));
+            r.slot_acquire();
+            for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
+              float4 y = xs[gi];
+              if (EC) y = sub4(y, ds[gi]);
+              const uint32_t q = quantize4(y, p.lo, p.inv);
+              dst[gi] = q;  // straight into owner k's window (NVLink for k != me)
+              if (EC) dl4[(e0 >> 2) + gi] = sub4(y, dequant4(q, p));
+            }
+            unsigned long long* sig = reinterpret_cast<unsigned long long*>(a.win[k] + a.off_gate) +
+                                      ((e0 >> 4) - pc[i].u0()) / kGateUnits;
+            r.slot_commit(sig, unsigned(units));
+          } else {
+            fold_pairs(st, units, T, s_fast != 0, [&](int gi, float4 y) {
+              const size_t e = e0 + 4 * size_t(gi);
+              if (EC) y = sub4(y, eps4(a.eps, e, mlo));
+              x4[e >> 2] = y;  // x's own chunk was consumed by its push: cache y2 there
+              mm_acc(lo2, hi2, y);
+            });
+          }
+        },
+        [&](int i) {
+          if (i == g) load_dec();
+        });
+    if (cons) {  // marker: the signaller confirms everything and stops
+      r.slot_acquire();
+      r.slot_commit(nullptr, 0u, true);
+    }
+    if (a.trace && (ct == 0 || (r.producer && threadIdx.x == 0))) {
+      unsigned long long* tw = a.trace + size_t(blockIdx.x) * kTraceSlots + kTrWait;
+      if (ct == 0) {
+        tw[0] = r.wt[0];  // consumers: free staging slot
+        tw[4] = r.wt[2];  // consumers: full stage
+      } else {
+        tw[1] = r.wt[0];  // producer: arrival gates
+        tw[2] = r.wt[1];  // producer: free stage
+      }
+    }
+    r.timed = false;
+    B2_TRACE(kTrP1Done);
+    // unaligned heads/tails (warp 0 of the last CTA): pushed with plain stores,
+    // announced on arrive_e; then the fold of my chunk's own heads/tails
+    if (cons && blockIdx.x == G - 1 && ct < 32) {
+      for (int i = 0; i < g; ++i) {
+        const U8Params p = s_p1[i];
+        uint8_t* dst = a.win[ck(i)] + a.off_recv1 + size_t(me) * a.slot_stride;
+        const size_t ebase = pc[i].s & ~size_t(15);
+        r.edges(pc[i], [&](size_t e) {
+          float y = a.x[e];
+          if (EC) y = __fsub_rn(y, a.delta[e]);
+          const uint8_t q = quantize1(y, p.lo, p.inv);
+          dst[e - ebase] = q;
+          if (EC) a.delta[e] = __fsub_rn(y, dequant1(q, p.lo, p.step));
+        });
+      }
+      __threadfence_system();
+      __syncwarp();
+      if (ct == 0) {
+        for (int i = 0; i < g; ++i) red_release_sys_add(&hdr_of(a.win[ck(i)])->arrive_e, 1ull);
+        wait_geq(&mine->arrive_e, gmul, a.timeout_ns, a.status);
+        wait_geq(&mine->arrive1, gmul, a.timeout_ns, a.status);
+        load_dec();
+      }
+      __syncwarp();
+      r.edges(pf, [&](size_t e) {
+        float y = fold1(e);
+        if (EC) y = __fsub_rn(y, a.eps[e - mlo]);
+        a.x[e] = y;
+        mm_acc1(lo2, hi2, y);
       });
-    });
-    r.edges(pf, [&](size_t e) {
-      float y = fold1(e);
-      if (EC) y = __fsub_rn(y, a.eps[e - mlo]);
-      if (cache) a.x[e] = y;
-      mm_acc1(lo, hi, y);
-    });
+    }
     U8Params p{};
     if (cons) {
-      const float2 mm0 = consumer_minmax(lo, hi, red);
+      const float2 mm0 = consumer_minmax(lo2, hi2, red);
       if (ct == 0) a.partials[size_t(kMaxRanks) * G + blockIdx.x] = mm0;
       fence_proxy_async();
       const float2 mm = finish_minmax(kMaxRanks);
@@ -544,9 +570,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
       out2[e - mbase] = q;
       if (EC) a.eps[e - mlo] = __fsub_rn(y, dequant1(q, p.lo, p.step));
     };
-    PassDesc ps = xpass(mlo, msz);  // the y2 cached in x's own chunk
-    ps.nsrc = 1;
-    ps.reverse = true;
+    const PassDesc& ps = s_m[1];  // the y2 cached in x's own chunk (reversed)
     if (r.producer && (threadIdx.x & 31) == 0) gate_wait(&s_gate, 1);
     r.run(ps, [&](const uint8_t* st, size_t e0, size_t units, int) {
       const float4* ys = reinterpret_cast<const float4*>(st);
@@ -554,9 +578,47 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     });
     r.edges(ps, [&](size_t e) { emit1(e, a.x[e]); });
   } else {
+    // ---------------------------------------------- identity: phase 1 push
+    // Step i stores chunk me+1+i into its owner's window (a permutation of
+    // destinations across ranks); the last CTA to finish a step signals.
+    for (int i = 0; i < g; ++i) {
+      const int k = ck(i);
+      const PassDesc& px = pc[i];
+      float* dstf = reinterpret_cast<float*>(a.win[k] + a.off_recv1 + size_t(me) * a.slot_stride);
+      const size_t ebase = px.s & ~size_t(15);  // slot element index = e - ebase
+      r.run(px, [&](const uint8_t* st, size_t e0, size_t units, int T) {
+        const float4* xs = reinterpret_cast<const float4*>(st);
+        const float4* ds = reinterpret_cast<const float4*>(st + size_t(T) * 64);
+        for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
+          float4 y = xs[gi];
+          if (EC) y = sub4(y, ds[gi]);
+          const size_t e = e0 + 4 * size_t(gi);
+          *reinterpret_cast<float4*>(dstf + (e - ebase)) = y;
+          if (a.check_finite) bad |= !finite4(y);
+          if (EC) dl4[e >> 2] = sub4(y, y);
+        }
+      });
+      r.edges(px, [&](size_t e) {
+        float y = a.x[e];
+        if (EC) y = __fsub_rn(y, a.delta[e]);
+        dstf[e - ebase] = y;
+        if (a.check_finite) bad |= !finite_f(y);
+        if (EC) a.delta[e] = __fsub_rn(y, y);
+      });
+      if (i == 0) B2_TRACE(kTrP1FirstB);
+      B2_TRACE(kTrP1Step + i);
+      if (cons && consumer_arrive<true>(a.cta_done + k, &s_flag) && ct == 0)
+        red_release_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);
+      B2_TRACE(kTrP1Fenced + i);
+    }
+    B2_TRACE(kTrP1Done);
+
+    // ------------------------------------------ identity: phase 2 owner reduce
+    if (cons && ct == 0) wait_geq(&mine->arrive1, pf.wait_target, a.timeout_ns, a.status);
+    B2_TRACE(kTrP2Ready);
     float* outf = reinterpret_cast<float*>(out2);
     r.run(pf, [&](const uint8_t* st, size_t e0, size_t units, int T) {
-      fold_pairs(st, units, T, [&](int gi, float4 y) {
+      fold_pairs(st, units, T, true, [&](int gi, float4 y) {
         const size_t e = e0 + 4 * size_t(gi);
         if (EC) y = sub4(y, eps4(a.eps, e, mlo));
         if (a.check_finite) bad |= !finite4(y);
@@ -593,28 +655,12 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
   // once with tiles interleaved round-robin (balanced fan-in whatever the rank
   // skew), plus the owner's own payload decoded into its own chunk.
   {
-    PassDesc pp[kMaxRanks];
-    size_t plo[kMaxRanks], pbase[kMaxRanks];
-    int powner[kMaxRanks];
-    for (int i = 0; i < g; ++i) {
-      const int k = (me + 1 + i) % g;  // i == g-1: self (local)
-      size_t lo, sz;
-      part_range(a.n, g, k, lo, sz);
-      powner[i] = k;
-      plo[i] = lo;
-      pbase[i] = lo & ~size_t(15);
-      pp[i].s = lo;
-      pp[i].n = sz;
-      pp[i].eb = CODEC == kU8 ? 1 : 4;
-      pp[i].nsrc = 1;
-      pp[i].base[0] = a.win[k] + a.off_out2 - size_t(pp[i].eb) * pbase[i];
-      pp[i].wait_flag = &hdr_of(a.win[k])->ready2;
-      pp[i].wait_target = a.epoch;
-    }
+    const PassDesc* pp = s_pp;
+    auto powner = [&](int i) { return i + me + 1 < g ? i + me + 1 : i + me + 1 - g; };  // g-1: self
     // header of owner i: read by the producer after owner i's flag (ready
     // callback) or, for the edge elements, by consumer warp 0 of the last CTA
     auto load_hdr = [&](int i) {
-      const int k = powner[i];
+      const int k = powner(i);
       WinHdr* hk = hdr_of(a.win[k]);
       if (CODEC == kU8) {
         const float2 h = k == me ? mine->hdr2 : ld_peer_f2(&hk->hdr2);
@@ -650,20 +696,19 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
       for (int i = 0; i < g; ++i) {
         if (pp[i].body_begin() == pp[i].s && pp[i].body_end() == pp[i].s + pp[i].n) continue;
         if (ct == 0) {
-          wait_geq(&hdr_of(a.win[powner[i]])->ready2, a.epoch, a.timeout_ns, a.status);
+          wait_geq(&hdr_of(a.win[powner(i)])->ready2, a.epoch, a.timeout_ns, a.status);
           load_hdr(i);
         }
         __syncwarp();
-        const uint8_t* src = a.win[powner[i]] + a.off_out2;
+        const uint8_t* src = a.win[powner(i)] + a.off_out2;
         const SrcDec kd = s_dec3[i];
         r.edges(pp[i], [&](size_t e) {
-          a.x[e] = CODEC == kU8 ? dequant1(__ldcg(src + (e - pbase[i])), kd.lo, kd.step)
-                               : __ldcg(reinterpret_cast<const float*>(src) + (e - pbase[i]));
+          a.x[e] = CODEC == kU8 ? dequant1(__ldcg(src + (e - (pp[i].s & ~size_t(15)))), kd.lo, kd.step)
+                               : __ldcg(reinterpret_cast<const float*>(src) + (e - (pp[i].s & ~size_t(15))));
         });
         __syncwarp();
       }
     }
-    (void)plo;
   }
   B2_TRACE(kTrEnd);
 }
@@ -694,12 +739,23 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
   int bad = 0;
   B2_TRACE(kTrStart);
 
-  PassDesc px;
-  px.s = 0;
-  px.n = a.n;
-  px.eb = 4;
-  px.nsrc = 1;
-  px.base[0] = reinterpret_cast<const uint8_t*>(a.x);
+  __shared__ PassDesc s_d[3];  // all of x, all of x reversed, the gather (shared: see central_body)
+  if (threadIdx.x == 0) {
+    PassDesc& px = s_d[0];
+    px = PassDesc::make();
+    px.n = a.n;
+    px.base[0] = reinterpret_cast<const uint8_t*>(a.x);
+    s_d[1] = px;
+    s_d[1].reverse = true;
+    PassDesc& pg = s_d[2];  // every neighbour's buffer (self included), ascending order
+    pg = PassDesc::make();
+    pg.n = a.n;
+    pg.eb = CODEC == kU8 ? 1 : 4;
+    pg.nsrc = a.nnb;
+    for (int i = 0; i < a.nnb; ++i) pg.base[i] = a.win[a.nbrs[i]] + a.off_dbuf;
+  }
+  __syncthreads();
+  const PassDesc& px = s_d[0];
 
   if (a.nnb == 1) {
     // ----- the neighbourhood is {self}: nothing is published or read;
@@ -722,8 +778,7 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
         if (blockIdx.x == 0 && ct == 0 && a.n && !(finite_f(mm.x) && finite_f(mm.y)))
           latch(a.status, kStatusNonFinite);
       }
-      PassDesc pb = px;
-      pb.reverse = true;
+      const PassDesc& pb = s_d[1];
       r.run(pb, [&](const uint8_t* st, size_t e0, size_t units, int) {
         const float4* xs = reinterpret_cast<const float4*>(st);
         for (int gi = ct; gi < int(units * 4); gi += kConsumers)
@@ -804,12 +859,7 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
   B2_TRACE(kTrP1Done);
 
   // ----- gather: every neighbour's buffer (self included), ascending order
-  PassDesc pg;
-  pg.s = 0;
-  pg.n = a.n;
-  pg.eb = CODEC == kU8 ? 1 : 4;
-  pg.nsrc = a.nnb;
-  for (int i = 0; i < a.nnb; ++i) pg.base[i] = a.win[a.nbrs[i]] + a.off_dbuf;
+  const PassDesc& pg = s_d[2];
   // producer: wait for every neighbour's publication before streaming
   if (r.producer && (threadIdx.x & 31) == 0) {
     for (int i = 0; i < a.nnb; ++i) wait_geq(&hdr_of(a.win[a.nbrs[i]])->dready[p], a.epoch, a.timeout_ns, a.status);

@@ -16,7 +16,8 @@ struct WinHdr {
   unsigned long long ready2;    // central: epoch of my published phase-2 output
   unsigned long long dready[2]; // decentral: epoch of my published buffer, per parity
   unsigned long long dreads[2]; // decentral: #neighbour reads of my buffer completed (cumulative)
-  unsigned long long pad0[2];
+  unsigned long long arrive_e;  // central uint8: #ranks whose unaligned head/tail codes for me landed
+  unsigned long long pad0;
   float2 hdr1[kMaxRanks];       // central uint8: (min,max) of my chunk as encoded by rank j
   float2 hdr2;                  // central uint8: (min,max) of my phase-2 payload
   float2 dhdr[2];               // decentral uint8: (min,max) of my bucket, per parity
@@ -42,6 +43,7 @@ enum TracePoint : int {
   kTrP2Pass = 9,     // phase 2: second pass done, before the publication fence
   kTrP1Step = 10,    // 10..17: phase-1 step i (chunk me+1+i) pushed, before its fence
   kTrP1Fenced = 18,  // 18..25: phase-1 step i fenced and signalled
+  kTrWait = 26,      // 26..31: accumulated ns (not stamps) -- Ring::wt[] of the traced stream
 };
 
 // Centralized ScatterReduce (C_FP_S, C_LP_S).
@@ -54,7 +56,7 @@ struct CentralArgs {
   float* delta;                 // ErrorState::delta (n) or null
   float* eps;                   // ErrorState::epsilon (owned len) or null
   uint8_t* win[kMaxRanks];      // every rank's window base (peer-mapped; win[me] local)
-  size_t off_recv1, slot_stride, off_out2;
+  size_t off_gate, off_recv1, slot_stride, off_out2;
   float2* partials;             // local workspace [(kMaxRanks + 1) * grid]
   unsigned* cta_done;           // local workspace [kMaxRanks + 2]
   unsigned* gridbar;            // local workspace [2]: consumer grid barrier

@@ -42,7 +42,7 @@ struct Window {
   uint8_t* local = nullptr;
   uint8_t* peer[kMaxRanks] = {};
   bool ipc_opened[kMaxRanks] = {};
-  size_t off_recv1 = 0, slot_stride = 0, off_out2 = 0, off_dbuf[2] = {0, 0};
+  size_t off_gate = 0, off_recv1 = 0, slot_stride = 0, off_out2 = 0, off_dbuf[2] = {0, 0};
   unsigned long long epoch = 0;
   unsigned long long exp_reads[2] = {0, 0};
   float2* partials = nullptr;
@@ -116,6 +116,9 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
   size_t off = 256;  // WinHdr
   if (family == kCentral) {
     const size_t maxchunk = (n + g - 1) / g;
+    // uint8 phase-1 region counters of my chunk (PassDesc::gate)
+    w->off_gate = off;
+    off += round_up(sizeof(unsigned long long) * (maxchunk / (16 * kGateUnits) + 2), 256);
     w->slot_stride = round_up(size_t(elem) * (maxchunk + 8), 256);
     w->off_recv1 = off;
     off += size_t(g) * w->slot_stride;
@@ -134,7 +137,7 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
     return rc;
   };
   if (cudaMalloc(&w->local, w->bytes) != cudaSuccess ||
-      cudaMemset(w->local, 0, 256) != cudaSuccess ||
+      cudaMemset(w->local, 0, family == kCentral ? w->off_recv1 : 256) != cudaSuccess ||
       cudaMalloc(&w->partials, sizeof(float2) * (kMaxRanks + 1) * max_persistent_grid()) !=
           cudaSuccess ||
       cudaMalloc(&w->cta_done, sizeof(unsigned) * (kMaxRanks + 4)) != cudaSuccess ||
@@ -419,6 +422,7 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   a.delta = delta;
   a.eps = eps;
   for (int j = 0; j < c->world; ++j) a.win[j] = w->peer[j];
+  a.off_gate = w->off_gate;
   a.off_recv1 = w->off_recv1;
   a.slot_stride = w->slot_stride;
   a.off_out2 = w->off_out2;

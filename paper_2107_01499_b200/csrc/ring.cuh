@@ -19,18 +19,24 @@
 
 namespace b2 {
 
-// Warp roles: warp 0 = producer (TMA loads), warp 1 = storer (TMA bulk
-// stores of staged payloads to peers + their completion/signalling), warps
-// 2.. = consumers.  20 warps = 5 per SM sub-partition at 96 registers.
+// Warp roles: warp 0 = producer (TMA loads), warp 1 = signaller ("storer":
+// confirms the consumers' pushes to peers and signals their readers, see
+// slot_commit), warps 2.. = consumers.  20 warps = 5 per SM sub-partition at 96 registers.
 constexpr int kConsumerWarps = 18;
 constexpr int kConsumers = 32 * kConsumerWarps;          // 576 consumer threads
 constexpr int kFirstConsumer = 64;                        // threadIdx of consumer 0
 constexpr int kRingThreads = kConsumers + kFirstConsumer; // 640
-constexpr int kStages = 5;
-constexpr int kStageBytes = 32768;
-constexpr int kSlots = 5;                                 // staging ring for pushed payloads
-constexpr int kSlotBytes = 8192;                          // codes of one 32 KB fp32 tile
-constexpr int kRingSmem = 512 + kStages * kStageBytes + kSlots * kSlotBytes;  // 200 KB + control
+#ifndef B2_RING_STAGES  // overridable for the ring microbenchmark (tests/cpp/ring_bench.cu)
+#define B2_RING_STAGES 5
+#endif
+#ifndef B2_RING_STAGE_BYTES
+#define B2_RING_STAGE_BYTES 32768
+#endif
+constexpr int kStages = B2_RING_STAGES;
+constexpr int kStageBytes = B2_RING_STAGE_BYTES;
+constexpr int kSlots = 16;                      // push credits: consumers -> signaller
+constexpr int kCtrlBytes = 2048;                // mbarriers + stage/slot metadata + producer state
+constexpr int kRingSmem = kCtrlBytes + kStages * kStageBytes;  // 162 KB by default
 constexpr int kConsumerBar = 1;                           // named barrier id
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -47,6 +53,16 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+#ifdef B2_MBAR_POLL
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+  return;
+#endif
   asm volatile(
       "{\n .reg .pred p;\n"
       "WAIT_%=:\n"
@@ -54,6 +70,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
       " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 // global (local HBM or peer-mapped NVLink address) -> shared, completes tx on bar
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
@@ -81,8 +108,12 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
-// every committed bulk store has completed (its writes are performed)
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// every committed bulk store but the N most recent has completed (writes performed)
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { bulk_wait<0>(); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -90,31 +121,80 @@ __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync %0, %1;" ::"n"(kConsumerBar), "n"(kConsumers) : "memory");
 }
 
-struct PassDesc {
-  size_t s = 0, n = 0;                  // element range
-  int nsrc = 1, eb = 4;                 // sources, bytes per element
-  const uint8_t* base[kMaxRanks] = {};  // address of element e of source i = base[i] + eb * e
-  const unsigned long long* wait_flag = nullptr;  // producer: wait *flag >= target before loading
-  unsigned long long wait_target = 0;
-  bool reverse = false;  // walk this CTA's tiles backwards: re-reads the tail of a
-                         // range that was streamed forwards just before from L2
-  __host__ __device__ int tile_units() const { return kStageBytes / (nsrc * 16 * eb); }
+// Tile gating: a pass may be gated per region of kGateUnits (b2_device.cuh) 16-byte units
+// (from the pass start): tile t may only be loaded once gate[region] >=
+// gate_mult * (units of that region).  Writers add the units they delivered,
+// so the count does not depend on anybody's tile size.
+
+struct PassDesc {  // trivially constructible (lives in shared memory); build with make()
+  size_t s, n;                     // element range
+  int nsrc, eb;                    // sources, bytes per element
+  const uint8_t* base[kMaxRanks];  // address of element e of source i = base[i] + eb * e (i < nsrc)
+  const unsigned long long* wait_flag;  // producer: wait *flag >= target before loading
+  unsigned long long wait_target;
+  const unsigned long long* gate;  // per-region arrival counters, or null
+  unsigned long long gate_mult;
+  bool reverse;  // walk the tiles backwards: re-reads the tail of a range
+                 // that was streamed forwards just before from L2
+  static __host__ __device__ PassDesc make() {
+    PassDesc p{};
+    p.nsrc = 1;
+    p.eb = 4;
+    return p;
+  }
+  // a power of two (so tiles of every pass over one range nest in gate regions)
+  __host__ __device__ int tile_units() const {
+    const int m = kStageBytes / (nsrc * 16 * eb);
+    int t = 1;
+    while (2 * t <= m) t *= 2;
+    return t;
+  }
   __host__ __device__ size_t u0() const { return (s + 15) >> 4; }
   __host__ __device__ size_t u1() const { return (s + n) >> 4; }
   __host__ __device__ size_t nunits() const { return u1() > u0() ? u1() - u0() : 0; }
   __host__ __device__ size_t body_begin() const { return nunits() ? 16 * u0() : s + n; }
   __host__ __device__ size_t body_end() const { return nunits() ? 16 * u1() : s + n; }
+  __host__ __device__ size_t region_of(size_t t) const { return t * size_t(tile_units()) / kGateUnits; }
+  __host__ __device__ unsigned long long gate_target(size_t r) const {
+    const size_t left = nunits() - r * kGateUnits;
+    return gate_mult * (left < size_t(kGateUnits) ? left : size_t(kGateUnits));
+  }
 };
+
+// What the producer tells the consumers about a stage (pass == kEndPass: END).
+struct TileInfo {
+  unsigned long long e0;  // first element of the tile
+  unsigned units;         // 16-byte units in the tile
+  unsigned short pass;    // index of the pass in the stream() call
+  unsigned short T;       // tile_units() of the pass (source stride in the stage)
+};
+constexpr unsigned short kEndPass = 0xFFFF;
+
+// Producer-lane bookkeeping of one pass of a stream() call, in shared memory
+// (per-tile work of the single producer lane is the ring's critical path:
+// everything that does not change per tile is computed once per pass).
+struct ProdPass {
+  unsigned long long nt;    // tiles
+  unsigned long long k;     // statically assigned tiles taken so far
+  unsigned long long ms;    // statically assigned tiles of this CTA
+  unsigned long long dyn0;  // first dynamically scheduled logical tile
+  unsigned long long nun;   // 16-byte units
+  unsigned long long u0;    // first unit
+  unsigned long long rdy;   // gated passes: 1 + a region known to have landed (0: none)
+  unsigned T;               // tile units
+  unsigned tbytes;          // bytes of one source of a full tile (T * 16 * eb)
+};
+constexpr int kMaxPasses = kMaxRanks + 1;
 
 struct Ring {
   uint64_t* full;
   uint64_t* empty;
-  uint64_t* staged;  // consumers -> storer: slot filled
-  uint64_t* sfree;   // storer -> consumers: slot read by the bulk store
+  uint64_t* staged;  // consumers -> signaller: the pushes of a credit are issued
+  uint64_t* sfree;   // signaller -> consumers: the credit is free again
   uint8_t* buf;
-  uint8_t* slots;
-  void** slot_dst;     // smem [kSlots]: push destination of a staged slot
-  unsigned* slot_len;  // smem [kSlots]: its byte count (0 = end-of-chunk marker)
+  unsigned* slot_len;  // smem [kSlots]: 0 = end marker
+  unsigned long long** slot_sig;  // smem [kSlots]: counter to bump once the pushes have landed, or null
+  unsigned* slot_sigv;            // smem [kSlots]: by how much
   int stage = 0;
   unsigned phase = 0;
   int slot = 0;       // staging cursor (consumers and storer walk it in lock step)
@@ -122,9 +202,12 @@ struct Ring {
   bool producer;
   bool storer;
   int ct;  // consumer thread index 0..kConsumers-1 (producer / storer: -1)
-  unsigned long long* info;            // smem [kStages]: (pass << 40 | tile) of a stage, ~0 = END
+  TileInfo* info;                       // smem [kStages]: the tile a stage holds
+  ProdPass* pst;                        // smem [kMaxPasses]: producer state of the current stream
   unsigned long long* sched = nullptr;  // global per-pass tile counters (dynamic mode) or null
   int npass = 0;                        // passes streamed so far (identical in every role)
+  unsigned long long wt[4] = {0, 0, 0, 0};  // traced waits (ns): slot/gate, empty/retire, full
+  bool timed = false;                   // accumulate wt[] (tracing only)
   int* status;
   unsigned long long timeout_ns;
 
@@ -134,11 +217,12 @@ struct Ring {
     empty = full + kStages;
     staged = empty + kStages;
     sfree = staged + kSlots;
-    info = reinterpret_cast<unsigned long long*>(sfree + kSlots);
-    slot_dst = reinterpret_cast<void**>(info + kStages);
-    slot_len = reinterpret_cast<unsigned*>(slot_dst + kSlots);
-    buf = smem + 512;
-    slots = buf + size_t(kStages) * kStageBytes;
+    info = reinterpret_cast<TileInfo*>(sfree + kSlots);
+    pst = reinterpret_cast<ProdPass*>(smem + 1024);
+    slot_sig = reinterpret_cast<unsigned long long**>(info + kStages);
+    slot_len = reinterpret_cast<unsigned*>(slot_sig + kSlots);
+    slot_sigv = slot_len + kSlots;
+    buf = smem + kCtrlBytes;
     producer = threadIdx.x < 32;
     storer = threadIdx.x >= 32 && threadIdx.x < kFirstConsumer;
     ct = threadIdx.x >= kFirstConsumer ? int(threadIdx.x) - kFirstConsumer : -1;
@@ -157,53 +241,69 @@ struct Ring {
     }
     __syncthreads();
   }
+  __device__ __forceinline__ unsigned long long tnow() const { return timed ? globaltimer() : 0ull; }
   __device__ __forceinline__ void advance_slot() {
     if (++slot == kSlots) {
       slot = 0;
       sphase ^= 1u;
     }
   }
-  // consumers: wait until the current staging slot may be overwritten
-  __device__ __forceinline__ uint8_t* slot_acquire() {
+  // ------------------------------------------------ push credits
+  // Consumers store pushed payloads straight to the destination (STG over
+  // NVLink: measured faster than TMA bulk stores to peers) and hand the
+  // signaller warp (the "storer" role) one credit per tile: the counter to
+  // bump once those stores are visible at system scope.  The signaller takes
+  // every credit staged so far, issues ONE fence.acq_rel.sys for the batch
+  // (cumulative over the consumers' stores, ordered before it by the
+  // mbarrier release/acquire) and bumps the counters with relaxed reds -- so
+  // the consumers never block on NVLink completion, and a reader learns about
+  // each tile a fence latency after its last store.
+  __device__ __forceinline__ void slot_acquire() {  // every consumer thread
+    const unsigned long long t0 = tnow();
     mbar_wait(sfree + slot, sphase ^ 1u);
-    return slots + size_t(slot) * kSlotBytes;
+    if (timed) wt[0] += globaltimer() - t0;
   }
-  // consumers: the slot is filled (every consumer thread calls this).
-  // Consumer 0 records where the storer must push it (bytes == 0: a marker).
-  __device__ __forceinline__ void slot_commit(void* dst, unsigned bytes) {
+  // every consumer thread, after its stores of the tile (sig == nullptr and
+  // !marker: nothing to signal; marker: the signaller stops after this credit)
+  __device__ __forceinline__ void slot_commit(unsigned long long* sig, unsigned sigv, bool marker = false) {
     if (ct == 0) {
-      slot_dst[slot] = dst;
-      slot_len[slot] = bytes;
+      slot_sig[slot] = sig;
+      slot_sigv[slot] = sigv;
+      slot_len[slot] = marker ? 0u : 1u;
     }
-    fence_proxy_async_smem();
+    fence_proxy_async();  // the stores will be read by TMA (async proxy)
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(staged + slot);
     advance_slot();
   }
-  // storer lane 0: push the next filled slot.  Up to kPushInFlight bulk
-  // stores stay in flight; a slot is released to the consumers once its store
-  // has finished reading shared memory (FIFO order).  Returns false (and
-  // consumes the slot) on a marker.
-  static constexpr int kPushInFlight = kSlots - 1;
-  int pending = 0;    // storer: slots pushed but not yet released
-  int rel = 0;        // storer: oldest unreleased slot
-  __device__ __forceinline__ bool slot_push() {
-    mbar_wait(staged + slot, sphase);
-    const unsigned bytes = slot_len[slot];
-    if (bytes == 0) {  // marker: release it in FIFO order too
-      advance_slot();
-      ++pending;
-      return false;
+  // signaller lane 0: serve credits until the marker; returns after it
+  __device__ __forceinline__ void signal_loop() {
+    bool done = false;
+    while (!done) {
+      mbar_wait(staged + slot, sphase);
+      int n = 1;  // every credit staged by now joins the batch (a marker ends it)
+      {
+        int sl = slot;
+        unsigned ph = sphase;
+        while (n < kSlots && slot_len[sl] != 0) {
+          const int nx = sl + 1 == kSlots ? 0 : sl + 1;
+          const unsigned nph = sl + 1 == kSlots ? ph ^ 1u : ph;
+          if (!mbar_test(staged + nx, nph)) break;
+          sl = nx;
+          ph = nph;
+          ++n;
+        }
+      }
+      const unsigned long long t0 = tnow();
+      fence_acq_rel_sys();
+      if (timed) wt[1] += globaltimer() - t0;
+      for (int j = 0; j < n; ++j) {
+        if (slot_len[slot] == 0) done = true;
+        if (slot_sig[slot]) red_relaxed_sys_add(slot_sig[slot], slot_sigv[slot]);
+        mbar_arrive(sfree + slot);
+        advance_slot();
+      }
     }
-    bulk_s2g(slot_dst[slot], slots + size_t(slot) * kSlotBytes, bytes);
-    advance_slot();
-    if (++pending > kPushInFlight) {
-      bulk_wait_read<kPushInFlight>();
-      mbar_arrive(sfree + rel);
-      rel = rel + 1 == kSlots ? 0 : rel + 1;
-      --pending;
-    }
-    return true;
   }
   __device__ __forceinline__ void advance() {
     if (++stage == kStages) {
@@ -211,16 +311,6 @@ struct Ring {
       phase ^= 1u;
     }
   }
-  // storer lane 0: every push performed (writes visible); release all slots
-  __device__ __forceinline__ void push_drain() {
-    bulk_wait_all();
-    while (pending > 0) {
-      mbar_arrive(sfree + rel);
-      rel = rel + 1 == kSlots ? 0 : rel + 1;
-      --pending;
-    }
-  }
-
   // ---------------------------------------------------------------- passes
   // Stream one pass.  consume(stage_ptr, first_element, units, tile_units)
   // runs on every consumer thread for every tile handed to this CTA.
@@ -259,15 +349,19 @@ struct Ring {
     stream(ps, np, consume, ready);
   }
 
-  // The scheduler.  Static mode (sched == nullptr): CTA b takes tiles b, b+G,
-  // ... of every pass.  Dynamic mode: the producer lane grabs tiles from one
-  // global counter per pass (atomicAdd), so fast SMs take more tiles and every
-  // CTA finishes a pass at about the same time -- static assignment left a
-  // 10-20 us spread per pass, and every grid barrier waits for the slowest
-  // CTA.  Reverse passes hand tiles out from the END (the producer maps the
-  // counter c to ntiles-1-c), which is what makes a reverse re-read hit L2.
+  // The scheduler.  Tile c of a pass (logical order) is physical tile
+  // t = reverse ? ntiles-1-c : c; reverse passes therefore start at the END,
+  // which is what makes a reverse re-read of a just-streamed range hit L2.
+  // Static mode (sched == nullptr): CTA b takes logical tiles b, b+G, ...
+  // Guided mode: the first kStaticEighths/8 of every pass is assigned
+  // statically the same way, the rest is handed out by one global atomic
+  // counter per pass, so fast SMs take more of the tail and every CTA
+  // finishes a pass at about the same time (static assignment left a 10-20 us
+  // spread per pass at 4 GPUs, and every grid barrier waits for the slowest
+  // CTA) while the atomic's latency is paid on a quarter of the tiles only.
   // The stage's tile (or the END marker) travels to the consumers in shared
   // memory (info[]), published by the mbarrier arrive.
+  static constexpr int kStaticEighths = 6;
   template <class F, class R>
   __device__ void stream(const PassDesc* ps, int np, F&& consume, R&& ready) {
     const int pid0 = npass;
@@ -275,78 +369,116 @@ struct Ring {
     if (storer) return;
     if (producer) {
       if ((threadIdx.x & 31) != 0) return;
-      bool live[kMaxRanks], got[kMaxRanks];
-      size_t nt[kMaxRanks], k[kMaxRanks];
-      int nlive = 0;
+      const unsigned long long G = gridDim.x, b = blockIdx.x;
+      unsigned live = 0, got = 0, rev = 0, gated = 0;  // bit i: pass i
       for (int i = 0; i < np; ++i) {
-        const int T = ps[i].tile_units();
-        nt[i] = (ps[i].nunits() + T - 1) / T;
-        k[i] = 0;
-        got[i] = false;
-        live[i] = nt[i] > (sched ? 0 : blockIdx.x);
-        nlive += live[i];
+        const PassDesc& p = ps[i];
+        ProdPass& q = pst[i];
+        const int T = p.tile_units();
+        q.T = unsigned(T);
+        q.tbytes = unsigned(T * 16 * p.eb);
+        q.u0 = p.u0();
+        q.nun = p.nunits();
+        q.nt = (q.nun + T - 1) / T;
+        const unsigned long long mall = q.nt > b ? (q.nt - b + G - 1) / G : 0;
+        const unsigned long long S = sched ? q.nt * kStaticEighths / 8 / G : mall;
+        q.ms = S < mall ? S : mall;
+        q.dyn0 = S * G;
+        q.k = 0;
+        q.rdy = 0;
+        if (q.ms > 0 || (sched && q.dyn0 < q.nt)) live |= 1u << i;
+        if (p.reverse) rev |= 1u << i;
+        if (p.gate) gated |= 1u << i;
       }
-      int nready = 0;
-      while (nlive) {
+      // logical index of pass i's next tile for this CTA (take: claim it);
+      // ~0 = the pass has nothing left for this CTA
+      auto next = [&](int i, bool take) -> unsigned long long {
+        ProdPass& q = pst[i];
+        const unsigned long long k = q.k;
+        if (k < q.ms) {
+          if (take) q.k = k + 1;
+          return b + k * G;
+        }
+        if (!sched) return ~0ull;
+        const unsigned long long c =
+            q.dyn0 + (take ? atomicAdd(sched + pid0 + i, 1ull)
+                           : *reinterpret_cast<volatile unsigned long long*>(sched + pid0 + i));
+        return c < q.nt ? c : ~0ull;
+      };
+      bool force = false;  // a whole round skipped everything: block on the next gate
+      while (live) {
+        bool issued = false;
         for (int i = 0; i < np; ++i) {
-          if (!live[i]) continue;
-          if (!got[i]) {
+          const unsigned bit = 1u << i;
+          if (!(live & bit)) continue;
+          if (!(got & bit)) {
             // A pass whose data is not published yet is skipped while another
             // pass has tiles to hand out; with nothing else to do, block.
-            if (ps[i].wait_flag && ld_acquire_sys(ps[i].wait_flag) < ps[i].wait_target) {
-              if (nready > 0) continue;
-              wait_geq(ps[i].wait_flag, ps[i].wait_target, timeout_ns, status);
+            const PassDesc& p = ps[i];
+            if (p.wait_flag && ld_acquire_sys(p.wait_flag) < p.wait_target) {
+              if ((live & got) && !force) continue;
+              wait_geq(p.wait_flag, p.wait_target, timeout_ns, status);
             }
-            if (ps[i].wait_flag) fence_proxy_async();
+            if (p.wait_flag) fence_proxy_async();
             ready(i);
-            got[i] = true;
-            ++nready;
+            got |= bit;
           }
-          size_t t;
-          if (sched) {
-            const unsigned long long c = atomicAdd(sched + pid0 + i, 1ull);
-            if (c >= nt[i]) {
-              live[i] = false;
-              --nlive;
-              --nready;
-              continue;
-            }
-            t = ps[i].reverse ? nt[i] - 1 - c : c;
-          } else {
-            const size_t m = (nt[i] - blockIdx.x + gridDim.x - 1) / gridDim.x;
-            const size_t j = k[i]++;
-            t = blockIdx.x + (ps[i].reverse ? m - 1 - j : j) * gridDim.x;
-            if (k[i] == m) {
-              live[i] = false;
-              --nlive;
-              --nready;
+          if ((gated & bit) && (live & got & ~bit) && !force) {
+            // peek at the next tile: if its region has not landed yet and
+            // another pass has work, serve that one first (relaxed load; the
+            // acquire happens once per region below)
+            const unsigned long long c = next(i, false);
+            if (c != ~0ull) {
+              const PassDesc& p = ps[i];
+              const size_t rg = p.region_of((rev & bit) ? pst[i].nt - 1 - c : c);
+              if (pst[i].rdy != rg + 1 &&
+                  *reinterpret_cast<const volatile unsigned long long*>(p.gate + rg) < p.gate_target(rg))
+                continue;
             }
           }
-          issue(ps[i], i, t);
+          const unsigned long long c = next(i, true);
+          if (c == ~0ull) {
+            live &= ~bit;
+            continue;
+          }
+          const unsigned long long t = (rev & bit) ? pst[i].nt - 1 - c : c;
+          if (gated & bit) {
+            const PassDesc& p = ps[i];
+            const size_t rg = p.region_of(t);
+            if (pst[i].rdy != rg + 1) {
+              const unsigned long long t0 = tnow();
+              wait_geq(p.gate + rg, p.gate_target(rg), timeout_ns, status);
+              if (timed) wt[0] += globaltimer() - t0;
+              fence_proxy_async();
+              pst[i].rdy = rg + 1;
+            }
+          }
+          issue(ps[i], pst[i], i, t);
+          issued = true;
+          force = false;
         }
+        if (!issued && live) force = true;
       }
       mbar_wait(empty + stage, phase ^ 1u);  // END marker
-      info[stage] = ~0ull;
+      info[stage].pass = kEndPass;
       mbar_arrive(full + stage);
       advance();
       return;
     }
+    // consumers: everything they need travels in info[]; the pass table is
+    // only read by the producer lane
     while (true) {
+      const unsigned long long t0 = tnow();
       mbar_wait(full + stage, phase);
-      const unsigned long long inf = info[stage];
-      if (inf == ~0ull) {
+      if (timed) wt[2] += globaltimer() - t0;
+      const TileInfo ti = info[stage];
+      if (ti.pass == kEndPass) {
         __syncwarp();
         if ((threadIdx.x & 31) == 0) mbar_arrive(empty + stage);
         advance();
         break;
       }
-      const int i = int(inf >> 40);
-      const size_t t = size_t(inf & ((1ull << 40) - 1));
-      const PassDesc& p = ps[i];
-      const int T = p.tile_units();
-      const size_t nun = p.nunits();
-      const size_t units = (nun - t * T) < size_t(T) ? (nun - t * T) : size_t(T);
-      consume(i, buf + size_t(stage) * kStageBytes, 16 * (p.u0() + t * T), units, T);
+      consume(int(ti.pass), buf + size_t(stage) * kStageBytes, size_t(ti.e0), size_t(ti.units), int(ti.T));
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(empty + stage);
       advance();
@@ -354,17 +486,20 @@ struct Ring {
   }
 
   // producer lane: load tile t of pass p (index i) into the next stage
-  __device__ __forceinline__ void issue(const PassDesc& p, int i, size_t t) {
-    const size_t nun = p.nunits();
-    const int T = p.tile_units();
-    const size_t units = (nun - t * T) < size_t(T) ? (nun - t * T) : size_t(T);
+  __device__ __forceinline__ void issue(const PassDesc& p, const ProdPass& q, int i, unsigned long long t) {
+    const unsigned long long left = q.nun - t * q.T;
+    const unsigned units = left < q.T ? unsigned(left) : q.T;
+    const unsigned long long u = q.u0 + t * q.T;
+    const int nsrc = p.nsrc, eb = p.eb;
+    const unsigned long long t0 = tnow();
     mbar_wait(empty + stage, phase ^ 1u);
-    info[stage] = (static_cast<unsigned long long>(i) << 40) | t;
-    const unsigned bytes = unsigned(units * 16 * p.eb);
-    mbar_expect_tx(full + stage, bytes * p.nsrc);
+    if (timed) wt[1] += globaltimer() - t0;
+    info[stage] = TileInfo{16ull * u, units, static_cast<unsigned short>(i), static_cast<unsigned short>(q.T)};
+    const unsigned bytes = units * 16u * unsigned(eb);
+    mbar_expect_tx(full + stage, bytes * unsigned(nsrc));
     uint8_t* dst = buf + size_t(stage) * kStageBytes;
-    const size_t off = size_t(p.eb) * 16 * (p.u0() + t * T);
-    for (int s = 0; s < p.nsrc; ++s) bulk_g2s(dst + size_t(s) * T * 16 * p.eb, p.base[s] + off, bytes, full + stage);
+    const unsigned long long off = 16ull * unsigned(eb) * u;
+    for (int s = 0; s < nsrc; ++s) bulk_g2s(dst + size_t(s) * q.tbytes, p.base[s] + off, bytes, full + stage);
     advance();
   }
 

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) fold_kernel(const uint8_t* co
   for (int i = threadIdx.x; i < g * 256; i += blockDim.x)
     s_tab[i] = double(dequant1(uint8_t(i & 255), s_lo[i >> 8], s_step[i >> 8]));
   __syncthreads();
-  PassDesc p;
+  PassDesc p = PassDesc::make();
   p.s = 0;
   p.n = n;
   p.eb = 1;

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) pull_kernel(const uint8_t* sr
   extern __shared__ __align__(128) uint8_t smem[];
   Ring r;
   r.init(smem, st, 1000000000ull);
-  PassDesc p;
+  PassDesc p = PassDesc::make();
   p.s = 0;
   p.n = bytes;
   p.eb = 1;

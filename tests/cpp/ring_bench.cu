@@ -23,24 +23,30 @@ using namespace b2;
   } while (0)
 
 // MODE 0: minmax only; 1: quantize -> codes (1 B/elem write); 2: two passes
-// (minmax then quantize) over the same range; 3: decode codes -> x write
+// (minmax then quantize, reversed) over the same range; 3: decode codes -> x
+// write.  sched != null: dynamic tile scheduling (the collectives' default).
 template <int MODE>
 __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(float* x, uint8_t* codes, size_t n, float2* out,
-                                                               int* status) {
+                                                               int* status, unsigned long long* sched) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float2 red[32];
+  __shared__ PassDesc s_p[2];
   Ring r;
-  r.init(smem, status, 1000000000ull);
-  PassDesc p;
-  p.s = 0;
-  p.n = n;
-  p.eb = MODE == 3 ? 1 : 4;
-  p.nsrc = 1;
-  p.base[0] = MODE == 3 ? codes : reinterpret_cast<const uint8_t*>(x);
+  r.init(smem, status, 1000000000ull, sched);
+  if (threadIdx.x == 0) {
+    PassDesc p = PassDesc::make();
+    p.n = n;
+    p.eb = MODE == 3 ? 1 : 4;
+    p.base[0] = MODE == 3 ? codes : reinterpret_cast<const uint8_t*>(x);
+    s_p[0] = p;
+    p.reverse = true;
+    s_p[1] = p;
+  }
+  __syncthreads();
   float lo = 1e30f, hi = -1e30f;
   const int ct = r.ct;
   if (MODE == 0 || MODE == 2) {
-    r.run(p, [&](const uint8_t* st, size_t, size_t units, int) {
+    r.run(s_p[0], [&](const uint8_t* st, size_t, size_t units, int) {
       const float4* xs = reinterpret_cast<const float4*>(st);
       for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
         const float4 v = xs[gi];
@@ -50,36 +56,61 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(float* x, uint8_t
     });
   }
   if (MODE == 1 || MODE == 2) {
-    r.run(p, [&](const uint8_t* st, size_t e0, size_t units, int) {
+    r.run(s_p[MODE == 2 ? 1 : 0], [&](const uint8_t* st, size_t e0, size_t units, int) {
       const float4* xs = reinterpret_cast<const float4*>(st);
       uint32_t* c32 = reinterpret_cast<uint32_t*>(codes + e0);
       for (int gi = ct; gi < int(units * 4); gi += kConsumers) c32[gi] = quantize4(xs[gi], -1.0f, 127.5f);
     });
   }
   if (MODE == 3) {
-    r.run(p, [&](const uint8_t* st, size_t e0, size_t units, int) {
+    r.run(s_p[0], [&](const uint8_t* st, size_t e0, size_t units, int) {
       const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
       float4* x4 = reinterpret_cast<float4*>(x + e0);
       for (int gi = ct; gi < int(units * 4); gi += kConsumers)
         __stcs(x4 + gi, dequant4_fast(cs[gi], -1.0f, 0.0078431f, -65793.0f));
     });
   }
-  if (!r.producer) {
+  if (ct >= 0) {
     const float2 m = consumer_minmax(lo, hi, red);
     if (ct == 0) out[blockIdx.x] = m;
   }
+  r.finish(reinterpret_cast<unsigned*>(sched + 64));
 }
 
-template <int MODE>
-float run(float* x, uint8_t* c, size_t n, float2* out, int* st, int nsm, int reps) {
-  CK(cudaFuncSetAttribute(ring_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingSmem));
-  ring_kernel<MODE><<<nsm, kRingThreads, kRingSmem>>>(x, c, n, out, st);
+// plain LDG baseline: grid-stride float4 loads, 8 in flight per thread
+__global__ void __launch_bounds__(512) ldg_minmax(const float4* x, size_t n4, float2* out) {
+  float lo = 1e30f, hi = -1e30f;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + 7 * stride < n4; i += 8 * stride) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcs(x + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      lo = fmin_nan(lo, fmin_nan(fmin_nan(v[u].x, v[u].y), fmin_nan(v[u].z, v[u].w)));
+      hi = fmax_nan(hi, fmax_nan(fmax_nan(v[u].x, v[u].y), fmax_nan(v[u].z, v[u].w)));
+    }
+  }
+  for (; i < n4; i += stride) {
+    const float4 v = x[i];
+    lo = fmin_nan(lo, fmin_nan(fmin_nan(v.x, v.y), fmin_nan(v.z, v.w)));
+    hi = fmax_nan(hi, fmax_nan(fmax_nan(v.x, v.y), fmax_nan(v.z, v.w)));
+  }
+  lo = warp_min_nan(lo);
+  hi = warp_max_nan(hi);
+  if ((threadIdx.x & 31) == 0) out[blockIdx.x * 16 + threadIdx.x / 32] = make_float2(lo, hi);
+}
+
+float run_ldg(const float* x, size_t n, float2* out, int nsm, int per_sm, int reps) {
+  auto go = [&] { ldg_minmax<<<nsm * per_sm, 512>>>(reinterpret_cast<const float4*>(x), n / 4, out); };
+  go();
   CK(cudaDeviceSynchronize());
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
   CK(cudaEventRecord(a));
-  for (int i = 0; i < reps; ++i) ring_kernel<MODE><<<nsm, kRingThreads, kRingSmem>>>(x, c, n, out, st);
+  for (int i = 0; i < reps; ++i) go();
   CK(cudaEventRecord(b));
   CK(cudaEventSynchronize(b));
   float ms;
@@ -88,9 +119,10 @@ float run(float* x, uint8_t* c, size_t n, float2* out, int* st, int nsm, int rep
 }
 
 template <int MODE>
-float run_coop(float* x, uint8_t* c, size_t n, float2* out, int* st, int nsm, int reps) {
+float run(float* x, uint8_t* c, size_t n, float2* out, int* st, int nsm, int reps, unsigned long long* sched) {
   CK(cudaFuncSetAttribute(ring_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingSmem));
-  void* args[] = {&x, &c, &n, &out, &st};
+  unsigned long long* sc = sched;
+  void* args[] = {&x, &c, &n, &out, &st, &sc};
   auto go = [&] {
     CK(cudaLaunchCooperativeKernel((const void*)ring_kernel<MODE>, dim3(nsm), dim3(kRingThreads), args, kRingSmem, 0));
   };
@@ -118,22 +150,34 @@ int main() {
   int* st;
   CK(cudaMalloc(&x, nmax * 4));
   CK(cudaMalloc(&c, nmax));
-  CK(cudaMalloc(&out, 8 * 1024));
+  CK(cudaMalloc(&out, 8 * 1024 * 64));
   CK(cudaMalloc(&st, 4));
   CK(cudaMemset(x, 0, nmax * 4));
-  for (size_t n : {size_t(1000), size_t(100000000)}) {
-    printf("launch n=%zu: regular %.1f us, cooperative %.1f us\n", n, run<0>(x, c, n, out, st, nsm, 20) * 1e3,
-           run_coop<0>(x, c, n, out, st, nsm, 20) * 1e3);
+  printf("ring: %d stages x %d B\n", kStages, kStageBytes);
+  for (int per_sm : {2, 4}) {
+    const size_t n = 100000000;
+    const float t = run_ldg(x, n, out, nsm, per_sm, 10);
+    printf("LDG minmax n=%zu, %d CTAs/SM: %.1f us (%.0f GB/s)\n", n, per_sm, t * 1e3, n * 4.0 / 1e6 / t);
   }
-  for (size_t n : {size_t(12500000), size_t(25000000), size_t(50000000), size_t(100000000)}) {
-    const double mb = n * 4.0 / 1e6;
-    float t0 = run<0>(x, c, n, out, st, nsm, 10);
-    float t1 = run<1>(x, c, n, out, st, nsm, 10);
-    float t2 = run<2>(x, c, n, out, st, nsm, 10);
-    float t3 = run<3>(x, c, n, out, st, nsm, 10);
-    printf("n=%zu (%.0f MB x): minmax %.1f us (%.0f GB/s) | quantize %.1f us (%.0f GB/s) | minmax+quantize %.1f us | "
-           "decode %.1f us (%.0f GB/s)\n",
-           n, mb, t0 * 1e3, mb / t0, t1 * 1e3, (n * 5.0 / 1e6) / t1, t2 * 1e3, t3 * 1e3, (n * 5.0 / 1e6) / t3);
+  unsigned long long* sched;
+  CK(cudaMalloc(&sched, 65 * 8));
+  CK(cudaMemset(sched, 0, 65 * 8));
+  unsigned long long* endc = sched;  // static runs still need a valid end counter
+  for (int dyn = 0; dyn < 2; ++dyn) {
+    unsigned long long* sc = dyn ? sched : nullptr;
+    (void)endc;
+    printf("launch n=1000 (%s): %.1f us\n", dyn ? "dynamic" : "static", run<0>(x, c, 1000, out, st, nsm, 20, sc) * 1e3);
+    for (size_t n : {size_t(25000000), size_t(100000000)}) {
+      const double mb = n * 4.0 / 1e6;
+      float t0 = run<0>(x, c, n, out, st, nsm, 10, sc);
+      float t1 = run<1>(x, c, n, out, st, nsm, 10, sc);
+      float t2 = run<2>(x, c, n, out, st, nsm, 10, sc);
+      float t3 = run<3>(x, c, n, out, st, nsm, 10, sc);
+      printf("%s n=%zu (%.0f MB x): minmax %.1f us (%.0f GB/s) | quantize %.1f us (%.0f GB/s) | minmax+quantize(rev) "
+             "%.1f us | decode %.1f us (%.0f GB/s)\n",
+             dyn ? "dynamic" : "static ", n, mb, t0 * 1e3, mb / t0, t1 * 1e3, (n * 5.0 / 1e6) / t1, t2 * 1e3,
+             t3 * 1e3, (n * 5.0 / 1e6) / t3);
+    }
   }
   return 0;
 }
