@@ -176,9 +176,10 @@ class B200Endpoint:
                     "p2_done", "p3_first", "end", "p2_pass") + tuple(f"p1_step{i}" for i in range(8)) + tuple(
                     f"p1_fenced{i}" for i in range(8))
     # accumulated waits (ns -> us, not timestamps) of the traced stream:
-    # consumers on a free staging slot, producer on arrival gates, producer on
-    # a free stage, storer retiring pushes, consumers on a full stage
-    WAIT_POINTS = ("w_slot", "w_gate", "w_empty", "w_retire", "w_full", "w_other")
+    # (C_LP_S phase 1B) encode consumers on a free credit, fold producer on
+    # arrival gates, encode producer on a free stage, signaller in fences,
+    # encode / fold consumers on a full stage
+    WAIT_POINTS = ("w_slot", "w_gate", "w_empty", "w_retire", "w_full", "w_fullB")
 
     def enable_trace(self, on: bool = True) -> None:
         check(lib.b2_comm_enable_trace(self._h, int(on)))
@@ -197,7 +198,7 @@ class B200Endpoint:
         t0 = t[:, 0].min()
         if raw:
             return _np.where(t > 0, (t - t0) / 1e3, _np.nan)
-        out = {}
+        out = {"t0_ns": int(t0)}  # absolute %globaltimer of this rank's first CTA start
         for i, name in enumerate(self.WAIT_POINTS):
             col = t[:, 26 + i]
             col = col[col > 0]

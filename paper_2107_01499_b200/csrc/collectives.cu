@@ -157,6 +157,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     if (EC) p.base[1] = reinterpret_cast<const uint8_t*>(a.delta);
     return p;
   };
+  B2_TRACE(kTrP1Fenced + 7);  // kernel entry (before the pass tables are built)
   if (threadIdx.x == 0) {
     s_gate = 0;
     s_m[0] = xpass(0, a.n);
@@ -167,10 +168,11 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     s_m[2].eb = 1;
     s_m[2].nsrc = 1;
     s_m[2].base[0] = a.win[0] + a.off_recv1;  // g=1 EC: element e -> codes[e]
+    const size_t cbase = a.n / size_t(g), cextra = a.n - cbase * size_t(g);
     for (int i = 0; i < g; ++i) {
       const int k = (me + 1 + i) % g;  // i == g-1: my own chunk
-      size_t lo, sz;
-      part_range(a.n, g, k, lo, sz);
+      const size_t lo = size_t(k) * cbase + (size_t(k) < cextra ? size_t(k) : cextra);
+      const size_t sz = cbase + (size_t(k) < cextra ? 1 : 0);
       s_pc[i] = xpass(lo, sz);
       s_pq[i] = s_pc[i];
       s_pq[i].reverse = CODEC == kU8;  // re-read backwards: the tails are in L2
@@ -191,7 +193,9 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     pf.eb = CODEC == kU8 ? 1 : 4;
     pf.nsrc = g;
     for (int j = 0; j < g; ++j)
-      pf.base[j] = a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride - size_t(pf.eb) * mbase;
+      pf.base[j] = (CODEC == kU8 ? a.win[j] + a.off_recv1 + size_t(me) * a.slot_stride  // pulled from rank j
+                                 : a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride)  // pushed by rank j
+                   - size_t(pf.eb) * mbase;
     pf.wait_flag = &mine->arrive1;  // uint8: every rank's header; identity: every rank's data
     pf.wait_target = gmul;
     if (CODEC == kU8) {  // uint8: each tile waits for its region's g contributions
@@ -350,10 +354,10 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
   // ------------------------------------------------------ phase 1 / 2 common
   const PassDesc& pf = s_pq[g];  // my fold
   // pairs of aligned groups through the fold (8 fp64 chains per thread)
-  auto fold_pairs = [&](const uint8_t* st, size_t units, int T, bool fast, auto&& body) {
+  auto fold_pairs = [&](const uint8_t* st, size_t units, int T, bool fast, int gct, int gn, auto&& body) {
     const int ng = int(units * 4);
-    for (int gi = ct; gi < ng; gi += 2 * kConsumers) {
-      const int g1 = gi + kConsumers;
+    for (int gi = gct; gi < ng; gi += 2 * gn) {
+      const int g1 = gi + gn;
       const bool has1 = g1 < ng;
       float4 y0, y1;
       fold2<CODEC>(g, fast, st, gi, has1 ? g1 : gi, T, s_dec, 1.0, y0, y1);
@@ -364,7 +368,8 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
   auto fold1 = [&](size_t e) -> float {
     double acc = 0.0;
     for (int j = 0; j < g; ++j) {
-      const uint8_t* slot = a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride;
+      const uint8_t* slot = CODEC == kU8 ? a.win[j] + a.off_recv1 + size_t(me) * a.slot_stride
+                                         : a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride;
       const float d = CODEC == kU8 ? dequant1(__ldcg(slot + (e - mbase)), s_dec[j].lo, s_dec[j].step)
                                    : __ldcg(reinterpret_cast<const float*>(slot) + (e - mbase));
       acc = __dadd_rn(acc, double(d));
@@ -410,6 +415,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
           if (EC) v = __fsub_rn(v, a.delta[e]);
           mm_acc1(cl[j], ch[j], v);
         });
+    B2_TRACE(kTrP1Step + 2);  // this CTA's share of the min/max pass streamed
     if (cons) {
 #pragma unroll
       for (int j = 0; j < kMaxRanks; ++j)
@@ -418,6 +424,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
           if (ct == 0) a.partials[size_t(j) * G + blockIdx.x] = mm;
         }
       consumer_grid_sync(a.gridbar);
+      B2_TRACE(kTrP1Step + 3);
       for (int j = 0; j < g; ++j) {
         const float2 mm = reduce_partials(a.partials + size_t(j) * G, G, red, ct);
         if (ct == 0) {
@@ -431,19 +438,27 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
           hdr_of(a.win[ck(j)])->hdr1[me] = s_mm1[j];  // remote 8-byte store into owner's header
           if (pc[j].n && !(finite_f(s_mm1[j].x) && finite_f(s_mm1[j].y))) latch(a.status, kStatusNonFinite);
         }
+        B2_TRACE(kTrP1Fenced + 4);  // headers stored
         __threadfence_system();
-        for (int j = 0; j < g; ++j) red_release_sys_add(&hdr_of(a.win[ck(j)])->arrive1, 1ull);
+        B2_TRACE(kTrP1Fenced + 5);  // headers fenced
+        // one fence above orders the headers before every signal (relaxed reds:
+        // a .release per red would repeat the fence g times)
+        for (int j = 0; j < g; ++j) red_relaxed_sys_add(&hdr_of(a.win[ck(j)])->arrive1, 1ull);
+        B2_TRACE(kTrP1Fenced + 6);  // headers signalled
       }
       consumer_sync();
     }
 
-    // ------------------------- phase 1B + 2A: push every chunk, fold as it lands
-    // Pass i < g quantizes chunk ck(i) straight into owner ck(i)'s window;
-    // the signaller warp confirms the stores (one system fence per batch of
-    // tiles) and adds each tile's units to the owner's region counter.  Pass g is my fold: each
-    // tile waits for its region to hold all g contributions, so the fold runs
-    // under the all-to-all instead of after it.  Chunks are walked backwards
-    // (their tails are still in L2 from phase 1A).
+    // ------------------------- phase 1B + 2A: encode every chunk, fold as it lands
+    // Pass i < g quantizes chunk ck(i) into MY window (slot ck(i)); the
+    // signaller warp confirms the stores (one system fence per batch of
+    // tiles) and adds each tile's units to owner ck(i)'s region counter.  Pass
+    // g is my fold: its tiles PULL the g encodings of a region of my chunk
+    // straight from the g windows with TMA once the region's counter says all
+    // g have landed -- so the NVLink transfer is asynchronous TMA reads (warps
+    // never stall on remote stores, which measured 168 us for this pass mix)
+    // and the fold runs under the encode instead of after it.  Chunks are
+    // walked backwards (their tails are still in L2 from phase 1A).
     auto load_dec = [&]() {  // contribution headers -> smem (one thread)
       int fast = 1;
       for (int j = 0; j < g; ++j) {
@@ -463,51 +478,66 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
       }
     }
     float lo2 = kInf, hi2 = -kInf;
-    r.run_multi(
-        s_pq, g + 1,
+    // split mode: pipe A (3 stages, 10 consumer warps) encodes from local x,
+    // pipe B (2 stages, 8 warps) folds from the TMA pulls
+    r.split_begin();
+    const int gct = r.gct, gn = r.gn;
+    r.stream_split(
+        s_pq, g,
         [&](int i, const uint8_t* st, size_t e0, size_t units, int T) {
-          if (i < g) {
-            const int k = ck(i);
-            const U8Params p = s_p1[i];
-            const float4* xs = reinterpret_cast<const float4*>(st);
-            const float4* ds = reinterpret_cast<const float4*>(st + size_t(T) * 64);
-            uint32_t* dst = reinterpret_cast<uint32_t*>(a.win[k] + a.off_recv1 + size_t(me) * a.slot_stride +
-                                                        (e0 - (pc[i].s & ~size_t(15))));
-            r.slot_acquire();
-            for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
-              float4 y = xs[gi];
-              if (EC) y = sub4(y, ds[gi]);
-              const uint32_t q = quantize4(y, p.lo, p.inv);
-              dst[gi] = q;  // straight into owner k's window (NVLink for k != me)
-              if (EC) dl4[(e0 >> 2) + gi] = sub4(y, dequant4(q, p));
-            }
-            unsigned long long* sig = reinterpret_cast<unsigned long long*>(a.win[k] + a.off_gate) +
-                                      ((e0 >> 4) - pc[i].u0()) / kGateUnits;
-            r.slot_commit(sig, unsigned(units));
-          } else {
-            fold_pairs(st, units, T, s_fast != 0, [&](int gi, float4 y) {
-              const size_t e = e0 + 4 * size_t(gi);
-              if (EC) y = sub4(y, eps4(a.eps, e, mlo));
-              x4[e >> 2] = y;  // x's own chunk was consumed by its push: cache y2 there
-              mm_acc(lo2, hi2, y);
-            });
+          const int k = ck(i);
+          const U8Params p = s_p1[i];
+          const float4* xs = reinterpret_cast<const float4*>(st);
+          const float4* ds = reinterpret_cast<const float4*>(st + size_t(T) * 64);
+          uint32_t* dst = reinterpret_cast<uint32_t*>(a.win[me] + a.off_recv1 + size_t(k) * a.slot_stride +
+                                                      (e0 - (pc[i].s & ~size_t(15))));
+          r.slot_acquire();
+          for (int gi = gct; gi < int(units * 4); gi += gn) {
+            float4 y = xs[gi];
+            if (EC) y = sub4(y, ds[gi]);
+            const uint32_t q = quantize4(y, p.lo, p.inv);
+            dst[gi] = q;  // my codes of chunk k, in my window: owner k pulls them
+            if (EC) dl4[(e0 >> 2) + gi] = sub4(y, dequant4(q, p));
           }
+          unsigned long long* sig = reinterpret_cast<unsigned long long*>(a.win[k] + a.off_gate) +
+                                    ((e0 >> 4) - pc[i].u0()) / kGateUnits;
+          r.slot_commit(sig, unsigned(units));
         },
-        [&](int i) {
-          if (i == g) load_dec();
+        [](int) {}, s_pq + g, 1,
+        [&](int, const uint8_t* st, size_t e0, size_t units, int T) {
+          fold_pairs(st, units, T, s_fast != 0, gct, gn, [&](int gi, float4 y) {
+            const size_t e = e0 + 4 * size_t(gi);
+            if (EC) y = sub4(y, eps4(a.eps, e, mlo));
+            x4[e >> 2] = y;  // x's own chunk was consumed by its encode: cache y2 there
+            mm_acc(lo2, hi2, y);
+          });
+        },
+        [&](int) {
+          load_dec();
+          if (a.trace) a.trace[size_t(blockIdx.x) * kTraceSlots + kTrP1Step + 7] = globaltimer();  // headers in
         });
-    if (cons) {  // marker: the signaller confirms everything and stops
+    if (r.group_a()) {  // marker: the signaller confirms everything and stops
       r.slot_acquire();
       r.slot_commit(nullptr, 0u, true);
     }
-    if (a.trace && (ct == 0 || (r.producer && threadIdx.x == 0))) {
+    r.split_end();
+    if (a.trace) {
       unsigned long long* tw = a.trace + size_t(blockIdx.x) * kTraceSlots + kTrWait;
+      unsigned long long* ts = a.trace + size_t(blockIdx.x) * kTraceSlots + kTrP1Step;
       if (ct == 0) {
-        tw[0] = r.wt[0];  // consumers: free staging slot
-        tw[4] = r.wt[2];  // consumers: full stage
-      } else {
-        tw[1] = r.wt[0];  // producer: arrival gates
-        tw[2] = r.wt[1];  // producer: free stage
+        tw[0] = r.wt[0];  // encode consumers: free credit
+        tw[4] = r.wt[2];  // encode consumers: full stage
+      } else if (ct == 32 * kSplitWarpsA) {
+        tw[5] = r.wt[2];  // fold consumers: full stage
+      } else if (r.producer && threadIdx.x == 0) {
+        tw[2] = r.wt[1];  // encode producer: free stage
+        unsigned long long enc = 0;
+        for (int i = 0; i < g; ++i) enc = r.pst[i].last > enc ? r.pst[i].last : enc;
+        ts[4] = enc;  // p1_step4: last encode tile issued
+      } else if (r.producer2 && threadIdx.x == kProducer2) {
+        tw[1] = r.wt[0];        // fold producer: arrival gates
+        ts[5] = r.pst2[0].first;  // p1_step5: first fold tile issued
+        ts[6] = r.pst2[0].last;   // p1_step6: last fold tile issued
       }
     }
     r.timed = false;
@@ -517,7 +547,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     if (cons && blockIdx.x == G - 1 && ct < 32) {
       for (int i = 0; i < g; ++i) {
         const U8Params p = s_p1[i];
-        uint8_t* dst = a.win[ck(i)] + a.off_recv1 + size_t(me) * a.slot_stride;
+        uint8_t* dst = a.win[me] + a.off_recv1 + size_t(ck(i)) * a.slot_stride;
         const size_t ebase = pc[i].s & ~size_t(15);
         r.edges(pc[i], [&](size_t e) {
           float y = a.x[e];
@@ -530,7 +560,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
       __threadfence_system();
       __syncwarp();
       if (ct == 0) {
-        for (int i = 0; i < g; ++i) red_release_sys_add(&hdr_of(a.win[ck(i)])->arrive_e, 1ull);
+        for (int i = 0; i < g; ++i) red_relaxed_sys_add(&hdr_of(a.win[ck(i)])->arrive_e, 1ull);
         wait_geq(&mine->arrive_e, gmul, a.timeout_ns, a.status);
         wait_geq(&mine->arrive1, gmul, a.timeout_ns, a.status);
         load_dec();
@@ -608,7 +638,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
       if (i == 0) B2_TRACE(kTrP1FirstB);
       B2_TRACE(kTrP1Step + i);
       if (cons && consumer_arrive<true>(a.cta_done + k, &s_flag) && ct == 0)
-        red_release_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);
+        red_relaxed_sys_add(&hdr_of(a.win[k])->arrive1, 1ull);  // consumer_arrive fenced (sys)
       B2_TRACE(kTrP1Fenced + i);
     }
     B2_TRACE(kTrP1Done);
@@ -618,7 +648,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     B2_TRACE(kTrP2Ready);
     float* outf = reinterpret_cast<float*>(out2);
     r.run(pf, [&](const uint8_t* st, size_t e0, size_t units, int T) {
-      fold_pairs(st, units, T, true, [&](int gi, float4 y) {
+      fold_pairs(st, units, T, true, ct, kConsumers, [&](int gi, float4 y) {
         const size_t e = e0 + 4 * size_t(gi);
         if (EC) y = sub4(y, eps4(a.eps, e, mlo));
         if (a.check_finite) bad |= !finite4(y);
@@ -647,7 +677,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
   }
   B2_TRACE(kTrP2Pass);
   if (cons && consumer_arrive<false>(a.cta_done + kMaxRanks, &s_flag) && ct == 0)
-    st_release_sys(&mine->ready2, a.epoch);
+    st_relaxed_sys(&mine->ready2, a.epoch);  // the last CTA's fence.sys in consumer_arrive orders it
   B2_TRACE(kTrP2Done);
 
   // ------------------------------------------------------ phase 3: pull + decode
@@ -720,6 +750,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   extern __shared__ __align__(128) uint8_t smem[];
   Ring r;
   r.init(smem, a.status, a.timeout_ns, a.sched);
+  r.dbg = a.dbg;
   central_body<CODEC, EC>(a, r);
   r.finish(a.sched_end);
 }
@@ -855,7 +886,7 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
       if (a.check_finite) bad |= !finite_f(a.x[e]);
     });
   }
-  if (cons && consumer_arrive<false>(a.cta_done + 0, &s_flag) && ct == 0) st_release_sys(&mine->dready[p], a.epoch);
+  if (cons && consumer_arrive<false>(a.cta_done + 0, &s_flag) && ct == 0) st_relaxed_sys(&mine->dready[p], a.epoch);
   B2_TRACE(kTrP1Done);
 
   // ----- gather: every neighbour's buffer (self included), ascending order
@@ -907,7 +938,7 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
   // ----- acknowledge the reads so each neighbour may reuse its buffer
   if (cons && consumer_arrive<false>(a.cta_done + 1, &s_flag) && ct == 0)
     for (int i = 0; i < a.nnb; ++i)
-      if (a.nbrs[i] != me) red_release_sys_add(&hdr_of(a.win[a.nbrs[i]])->dreads[p], 1ull);
+      if (a.nbrs[i] != me) red_relaxed_sys_add(&hdr_of(a.win[a.nbrs[i]])->dreads[p], 1ull);
   B2_TRACE(kTrEnd);
 }
 

@@ -20,12 +20,18 @@
 namespace b2 {
 
 // Warp roles: warp 0 = producer (TMA loads), warp 1 = signaller ("storer":
-// confirms the consumers' pushes to peers and signals their readers, see
-// slot_commit), warps 2.. = consumers.  20 warps = 5 per SM sub-partition at 96 registers.
-constexpr int kConsumerWarps = 18;
-constexpr int kConsumers = 32 * kConsumerWarps;          // 576 consumer threads
+// confirms the consumers' stores and signals their readers, see slot_commit),
+// warps 2..18 = consumers, warp 19 = second producer (split mode only, see
+// split_begin).  20 warps = 5 per SM sub-partition at 96 registers.
+constexpr int kConsumerWarps = 17;
+constexpr int kConsumers = 32 * kConsumerWarps;          // 544 consumer threads
 constexpr int kFirstConsumer = 64;                        // threadIdx of consumer 0
-constexpr int kRingThreads = kConsumers + kFirstConsumer; // 640
+constexpr int kProducer2 = kFirstConsumer + kConsumers;  // threadIdx of the second producer (608)
+constexpr int kRingThreads = kProducer2 + 32;             // 640
+// Split mode: pipe A = stages [0, kSplitStagesA) with consumer warps
+// [0, kSplitWarpsA), pipe B = the remaining stages and warps.
+constexpr int kSplitStagesA = 3;
+constexpr int kSplitWarpsA = 10;
 #ifndef B2_RING_STAGES  // overridable for the ring microbenchmark (tests/cpp/ring_bench.cu)
 #define B2_RING_STAGES 5
 #endif
@@ -34,8 +40,8 @@ constexpr int kRingThreads = kConsumers + kFirstConsumer; // 640
 #endif
 constexpr int kStages = B2_RING_STAGES;
 constexpr int kStageBytes = B2_RING_STAGE_BYTES;
-constexpr int kSlots = 16;                      // push credits: consumers -> signaller
-constexpr int kCtrlBytes = 2048;                // mbarriers + stage/slot metadata + producer state
+constexpr int kSlots = 64;                      // push credits: consumers -> signaller
+constexpr int kCtrlBytes = 4096;                // mbarriers + stage/slot metadata + producer state
 constexpr int kRingSmem = kCtrlBytes + kStages * kStageBytes;  // 162 KB by default
 constexpr int kConsumerBar = 1;                           // named barrier id
 
@@ -181,65 +187,131 @@ struct ProdPass {
   unsigned long long nun;   // 16-byte units
   unsigned long long u0;    // first unit
   unsigned long long rdy;   // gated passes: 1 + a region known to have landed (0: none)
+  unsigned long long first, last;  // traced: globaltimer of the first / last tile issued
   unsigned T;               // tile units
   unsigned tbytes;          // bytes of one source of a full tile (T * 16 * eb)
 };
 constexpr int kMaxPasses = kMaxRanks + 1;
+static_assert(2 * kMaxPasses * sizeof(ProdPass) <= 4096 - 2560, "producer state exceeds the control block");
 
-struct Ring {
+// One mbarrier-guarded ring of stage buffers (a view of the shared stages).
+struct Pipe {
   uint64_t* full;
   uint64_t* empty;
+  int first;  // first stage buffer of this pipe
+  int nst;    // stage buffers
+  int stage = 0;
+  unsigned phase = 0;
+  unsigned long long nissued = 0;  // producer: tiles (+ END markers) issued
+  __device__ __forceinline__ void advance() {
+    ++nissued;
+    if (++stage == nst) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+  // producer: wait until every issued stage has been released by the consumers
+  __device__ __forceinline__ void drain() {
+    for (int j = 0; j < nst; ++j) {
+      if (nissued < unsigned(j + 1)) break;
+      const unsigned long long k = nissued - 1 - j;  // issue number
+      mbar_wait(empty + int(k % nst), unsigned(k / nst) & 1u);
+    }
+  }
+};
+
+struct Ring {
   uint64_t* staged;  // consumers -> signaller: the pushes of a credit are issued
   uint64_t* sfree;   // signaller -> consumers: the credit is free again
   uint8_t* buf;
   unsigned* slot_len;  // smem [kSlots]: 0 = end marker
   unsigned long long** slot_sig;  // smem [kSlots]: counter to bump once the pushes have landed, or null
   unsigned* slot_sigv;            // smem [kSlots]: by how much
-  int stage = 0;
-  unsigned phase = 0;
+  // Pipe state stays in registers: named fields, no arrays / pointers into
+  // the Ring (either would put the whole per-thread Ring in local memory)
+  Pipe cp;        // the pipe this thread's role works on now
+  Pipe p0;        // the all-stage pipe, parked while in split mode
   int slot = 0;       // staging cursor (consumers and storer walk it in lock step)
   unsigned sphase = 0;
-  bool producer;
+  bool producer;      // warp 0 (lane 0 works)
+  bool producer2;     // warp 20 (lane 0 works, split mode only)
   bool storer;
-  int ct;  // consumer thread index 0..kConsumers-1 (producer / storer: -1)
-  TileInfo* info;                       // smem [kStages]: the tile a stage holds
+  bool split = false;
+  int ct;   // consumer thread index 0..kConsumers-1 (other roles: -1)
+  int gct;  // consumer index within its group (split mode) or ct
+  int gn;   // consumers in that group (split mode) or kConsumers
+  TileInfo* info;                       // smem [kStages]: the tile a stage buffer holds
   ProdPass* pst;                        // smem [kMaxPasses]: producer state of the current stream
+  ProdPass* pst2;                       // smem [kMaxPasses]: second producer's
+  volatile int* drained;                // smem: split-mode hand-over flags
   unsigned long long* sched = nullptr;  // global per-pass tile counters (dynamic mode) or null
   int npass = 0;                        // passes streamed so far (identical in every role)
   unsigned long long wt[4] = {0, 0, 0, 0};  // traced waits (ns): slot/gate, empty/retire, full
   bool timed = false;                   // accumulate wt[] (tracing only)
   int* status;
   unsigned long long timeout_ns;
+  int dbg = 0;  // experiment switch (B2_DBG): 1 = gpu-scope signal fence, 2 = none (unsound)
 
   __device__ void init(uint8_t* smem, int* st, unsigned long long to, unsigned long long* sched_ctrs = nullptr) {
     sched = sched_ctrs;
-    full = reinterpret_cast<uint64_t*>(smem);
-    empty = full + kStages;
-    staged = empty + kStages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+    // pipe barriers: [full, empty] x (kStages + kSplitStagesA + (kStages - kSplitStagesA)) = 4 kStages
+    staged = bars + 4 * kStages;
     sfree = staged + kSlots;
     info = reinterpret_cast<TileInfo*>(sfree + kSlots);
-    pst = reinterpret_cast<ProdPass*>(smem + 1024);
     slot_sig = reinterpret_cast<unsigned long long**>(info + kStages);
     slot_len = reinterpret_cast<unsigned*>(slot_sig + kSlots);
     slot_sigv = slot_len + kSlots;
+    drained = reinterpret_cast<volatile int*>(slot_sigv + kSlots);
+    pst = reinterpret_cast<ProdPass*>(smem + 2560);
+    pst2 = pst + kMaxPasses;
     buf = smem + kCtrlBytes;
+    cp = pipe_desc(0);
     producer = threadIdx.x < 32;
     storer = threadIdx.x >= 32 && threadIdx.x < kFirstConsumer;
-    ct = threadIdx.x >= kFirstConsumer ? int(threadIdx.x) - kFirstConsumer : -1;
+    producer2 = threadIdx.x >= kProducer2;
+    ct = threadIdx.x >= kFirstConsumer && threadIdx.x < kProducer2 ? int(threadIdx.x) - kFirstConsumer : -1;
+    gct = ct;
+    gn = kConsumers;
     status = st;
     timeout_ns = to;
     if (threadIdx.x == 0) {
-      for (int i = 0; i < kStages; ++i) {
-        mbar_init(full + i, 1);
-        mbar_init(empty + i, kConsumerWarps);
+      for (int k = 0; k < 3; ++k) {
+        const Pipe q = pipe_desc(k);
+        const unsigned warps = k == 0 ? kConsumerWarps : k == 1 ? kSplitWarpsA : kConsumerWarps - kSplitWarpsA;
+        for (int i = 0; i < q.nst; ++i) {
+          mbar_init(q.full + i, 1);
+          mbar_init(q.empty + i, warps);
+        }
       }
       for (int i = 0; i < kSlots; ++i) {
-        mbar_init(staged + i, kConsumerWarps);
+        mbar_init(staged + i, kSplitWarpsA);  // credits are committed by split group A
         mbar_init(sfree + i, 1);
       }
+      drained[0] = drained[1] = 0;
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+  }
+  // pipe k's barriers and stage buffers (0: all stages; 1, 2: split A, B)
+  __device__ __forceinline__ Pipe pipe_desc(int k) const {
+    uint64_t* bars = reinterpret_cast<uint64_t*>(buf - kCtrlBytes);
+    Pipe q;
+    if (k == 0) {
+      q.full = bars;
+      q.first = 0;
+      q.nst = kStages;
+    } else if (k == 1) {
+      q.full = bars + 2 * kStages;
+      q.first = 0;
+      q.nst = kSplitStagesA;
+    } else {
+      q.full = bars + 2 * kStages + 2 * kSplitStagesA;
+      q.first = kSplitStagesA;
+      q.nst = kStages - kSplitStagesA;
+    }
+    q.empty = q.full + q.nst;
+    return q;
   }
   __device__ __forceinline__ unsigned long long tnow() const { return timed ? globaltimer() : 0ull; }
   __device__ __forceinline__ void advance_slot() {
@@ -247,6 +319,56 @@ struct Ring {
       slot = 0;
       sphase ^= 1u;
     }
+  }
+  // consumers of split group A (split mode) / B
+  __device__ __forceinline__ bool group_a() const { return ct >= 0 && ct < 32 * kSplitWarpsA; }
+  __device__ __forceinline__ bool group_b() const { return ct >= 32 * kSplitWarpsA; }
+
+  // ------------------------------------------------ split mode
+  // Two independent pipelines in one CTA: pipe A (producer warp 0, consumer
+  // warps [0, kSplitWarpsA)) and pipe B (producer warp 19, the other consumer
+  // warps), each on its own stage buffers, so tiles that arrive slowly (TMA
+  // pulls over a saturated NVLink) never hold up the consumers of fast local
+  // tiles -- one in-order ring has head-of-line blocking.  Every thread calls
+  // split_begin / split_end at the same point; in between, stream_split()
+  // runs pass list A on pipe A and list B on pipe B.
+  __device__ void split_begin() {
+    split = true;
+    p0 = cp;
+    if (producer) {
+      if ((threadIdx.x & 31) == 0) {
+        cp.drain();  // every stage buffer is free
+        drained[0] = 1;
+      }
+      cp = pipe_desc(1);
+    } else if (producer2) {
+      if ((threadIdx.x & 31) == 0)
+        while (drained[0] == 0) __nanosleep(32);
+      cp = pipe_desc(2);
+    } else if (ct >= 0) {
+      const bool a = group_a();
+      cp = pipe_desc(a ? 1 : 2);
+      gct = a ? ct : ct - 32 * kSplitWarpsA;
+      gn = a ? 32 * kSplitWarpsA : kConsumers - 32 * kSplitWarpsA;
+    }
+  }
+  __device__ void split_end() {
+    split = false;
+    if (producer2) {
+      if ((threadIdx.x & 31) == 0) {
+        cp.drain();
+        drained[1] = 1;
+      }
+    } else if (producer) {
+      if ((threadIdx.x & 31) == 0) {
+        cp.drain();
+        while (drained[1] == 0) __nanosleep(32);
+        drained[0] = drained[1] = 0;
+      }
+    }
+    cp = p0;
+    gct = ct;
+    gn = kConsumers;
   }
   // ------------------------------------------------ push credits
   // Consumers store pushed payloads straight to the destination (STG over
@@ -271,7 +393,7 @@ struct Ring {
       slot_sigv[slot] = sigv;
       slot_len[slot] = marker ? 0u : 1u;
     }
-    fence_proxy_async();  // the stores will be read by TMA (async proxy)
+    if (dbg != 3) fence_proxy_async();  // the stores will be read by TMA (async proxy)
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(staged + slot);
     advance_slot();
@@ -295,7 +417,10 @@ struct Ring {
         }
       }
       const unsigned long long t0 = tnow();
-      fence_acq_rel_sys();
+      if (dbg == 0)
+        fence_acq_rel_sys();
+      else if (dbg == 1)
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
       if (timed) wt[1] += globaltimer() - t0;
       for (int j = 0; j < n; ++j) {
         if (slot_len[slot] == 0) done = true;
@@ -305,33 +430,12 @@ struct Ring {
       }
     }
   }
-  __device__ __forceinline__ void advance() {
-    if (++stage == kStages) {
-      stage = 0;
-      phase ^= 1u;
-    }
-  }
   // ---------------------------------------------------------------- passes
   // Stream one pass.  consume(stage_ptr, first_element, units, tile_units)
   // runs on every consumer thread for every tile handed to this CTA.
   template <class F>
   __device__ void run(const PassDesc& p, F&& consume) {
     stream(&p, 1, [&](int, const uint8_t* st, size_t e0, size_t units, int T) { consume(st, e0, units, T); },
-           [](int) {});
-  }
-
-  // Two passes with their tiles interleaved (a b a b ...), so e.g. an
-  // NVLink-bound push pass overlaps an HBM-bound min/max pass.
-  template <class FA, class FB>
-  __device__ void run2(const PassDesc& pa, FA&& fa, const PassDesc& pb, FB&& fb) {
-    const PassDesc ps[2] = {pa, pb};
-    stream(ps, 2,
-           [&](int i, const uint8_t* st, size_t e0, size_t units, int T) {
-             if (i == 0)
-               fa(st, e0, units, T);
-             else
-               fb(st, e0, units, T);
-           },
            [](int) {});
   }
 
@@ -366,12 +470,30 @@ struct Ring {
   __device__ void stream(const PassDesc* ps, int np, F&& consume, R&& ready) {
     const int pid0 = npass;
     npass += np;
-    if (storer) return;
-    if (producer) {
+    stream_at(ps, np, pid0, consume, ready);
+  }
+  // Split mode: pass list A streams on pipe A, list B on pipe B, at once.
+  template <class FA, class RA, class FB, class RB>
+  __device__ void stream_split(const PassDesc* pa, int npa, FA&& ca, RA&& ra, const PassDesc* pb, int npb, FB&& cb,
+                               RB&& rb) {
+    const int pid0 = npass;
+    npass += npa + npb;
+    if (producer || group_a())
+      stream_at(pa, npa, pid0, ca, ra);
+    else if (producer2 || group_b())
+      stream_at(pb, npb, pid0 + npa, cb, rb);
+  }
+  template <class F, class R>
+  __device__ void stream_at(const PassDesc* ps, int np, int pid0, F&& consume, R&& ready) {
+    if (storer || (producer2 && !split)) return;
+    Pipe& P = cp;
+    if (producer || producer2) {
       if ((threadIdx.x & 31) != 0) return;
+      ProdPass* const pst = producer2 ? pst2 : this->pst;
       const unsigned long long G = gridDim.x, b = blockIdx.x;
       unsigned live = 0, got = 0, rev = 0, gated = 0;  // bit i: pass i
       for (int i = 0; i < np; ++i) {
+        pst[i].first = pst[i].last = 0;
         const PassDesc& p = ps[i];
         ProdPass& q = pst[i];
         const int T = p.tile_units();
@@ -441,6 +563,11 @@ struct Ring {
             live &= ~bit;
             continue;
           }
+          if (timed) {
+            const unsigned long long now = globaltimer();
+            if (!pst[i].first) pst[i].first = now;
+            pst[i].last = now;
+          }
           const unsigned long long t = (rev & bit) ? pst[i].nt - 1 - c : c;
           if (gated & bit) {
             const PassDesc& p = ps[i];
@@ -453,54 +580,55 @@ struct Ring {
               pst[i].rdy = rg + 1;
             }
           }
-          issue(ps[i], pst[i], i, t);
+          issue(P, ps[i], pst[i], i, t);
           issued = true;
           force = false;
         }
         if (!issued && live) force = true;
       }
-      mbar_wait(empty + stage, phase ^ 1u);  // END marker
-      info[stage].pass = kEndPass;
-      mbar_arrive(full + stage);
-      advance();
+      mbar_wait(P.empty + P.stage, P.phase ^ 1u);  // END marker
+      info[P.first + P.stage].pass = kEndPass;
+      mbar_arrive(P.full + P.stage);
+      P.advance();
       return;
     }
     // consumers: everything they need travels in info[]; the pass table is
     // only read by the producer lane
     while (true) {
       const unsigned long long t0 = tnow();
-      mbar_wait(full + stage, phase);
+      mbar_wait(P.full + P.stage, P.phase);
       if (timed) wt[2] += globaltimer() - t0;
-      const TileInfo ti = info[stage];
+      const TileInfo ti = info[P.first + P.stage];
       if (ti.pass == kEndPass) {
         __syncwarp();
-        if ((threadIdx.x & 31) == 0) mbar_arrive(empty + stage);
-        advance();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(P.empty + P.stage);
+        P.advance();
         break;
       }
-      consume(int(ti.pass), buf + size_t(stage) * kStageBytes, size_t(ti.e0), size_t(ti.units), int(ti.T));
+      consume(int(ti.pass), buf + size_t(P.first + P.stage) * kStageBytes, size_t(ti.e0), size_t(ti.units),
+              int(ti.T));
       __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive(empty + stage);
-      advance();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(P.empty + P.stage);
+      P.advance();
     }
   }
 
   // producer lane: load tile t of pass p (index i) into the next stage
-  __device__ __forceinline__ void issue(const PassDesc& p, const ProdPass& q, int i, unsigned long long t) {
+  __device__ __forceinline__ void issue(Pipe& P, const PassDesc& p, const ProdPass& q, int i, unsigned long long t) {
     const unsigned long long left = q.nun - t * q.T;
     const unsigned units = left < q.T ? unsigned(left) : q.T;
     const unsigned long long u = q.u0 + t * q.T;
     const int nsrc = p.nsrc, eb = p.eb;
     const unsigned long long t0 = tnow();
-    mbar_wait(empty + stage, phase ^ 1u);
+    mbar_wait(P.empty + P.stage, P.phase ^ 1u);
     if (timed) wt[1] += globaltimer() - t0;
-    info[stage] = TileInfo{16ull * u, units, static_cast<unsigned short>(i), static_cast<unsigned short>(q.T)};
+    info[P.first + P.stage] = TileInfo{16ull * u, units, static_cast<unsigned short>(i), static_cast<unsigned short>(q.T)};
     const unsigned bytes = units * 16u * unsigned(eb);
-    mbar_expect_tx(full + stage, bytes * unsigned(nsrc));
-    uint8_t* dst = buf + size_t(stage) * kStageBytes;
+    mbar_expect_tx(P.full + P.stage, bytes * unsigned(nsrc));
+    uint8_t* dst = buf + size_t(P.first + P.stage) * kStageBytes;
     const unsigned long long off = 16ull * unsigned(eb) * u;
-    for (int s = 0; s < nsrc; ++s) bulk_g2s(dst + size_t(s) * q.tbytes, p.base[s] + off, bytes, full + stage);
-    advance();
+    for (int s = 0; s < nsrc; ++s) bulk_g2s(dst + size_t(s) * q.tbytes, p.base[s] + off, bytes, P.full + P.stage);
+    P.advance();
   }
 
   // Kernel epilogue (all threads): the last CTA resets the dynamic tile

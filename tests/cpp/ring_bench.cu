@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(float* x, uint8_t
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float2 red[32];
   __shared__ PassDesc s_p[2];
+  __shared__ PassDesc s_q[4];  // MODE 7: four quarter passes
   Ring r;
   r.init(smem, status, 1000000000ull, sched);
   if (threadIdx.x == 0) {
@@ -41,6 +42,11 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(float* x, uint8_t
     s_p[0] = p;
     p.reverse = true;
     s_p[1] = p;
+    for (int i = 0; i < 4; ++i) {
+      s_q[i] = s_p[0];
+      s_q[i].s = n / 4 * i;
+      s_q[i].n = n / 4;
+    }
   }
   __syncthreads();
   float lo = 1e30f, hi = -1e30f;
@@ -61,6 +67,36 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(float* x, uint8_t
       uint32_t* c32 = reinterpret_cast<uint32_t*>(codes + e0);
       for (int gi = ct; gi < int(units * 4); gi += kConsumers) c32[gi] = quantize4(xs[gi], -1.0f, 127.5f);
     });
+  }
+  if (MODE == 7) {  // the C_LP_S phase-1A shape: four chunk passes interleaved
+    r.run_multi(s_q, 4, [&](int, const uint8_t* st, size_t, size_t units, int) {
+      const float4* xs = reinterpret_cast<const float4*>(st);
+      for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
+        const float4 v = xs[gi];
+        lo = fmin_nan(lo, fmin_nan(fmin_nan(v.x, v.y), fmin_nan(v.z, v.w)));
+        hi = fmax_nan(hi, fmax_nan(fmax_nan(v.x, v.y), fmax_nan(v.z, v.w)));
+      }
+    });
+  }
+  if (MODE == 5 || MODE == 6) {  // split mode: pipe A quantizes (10 warps, 3 stages), pipe B idle
+    r.split_begin();
+    const int gct = r.gct, gn = r.gn;
+    r.stream_split(
+        s_p, 1,
+        [&](int, const uint8_t* st, size_t e0, size_t units, int) {
+          const float4* xs = reinterpret_cast<const float4*>(st);
+          uint32_t* c32 = reinterpret_cast<uint32_t*>(codes + e0);
+          if (MODE == 6) r.slot_acquire();
+          for (int gi = gct; gi < int(units * 4); gi += gn) c32[gi] = quantize4(xs[gi], -1.0f, 127.5f);
+          if (MODE == 6) r.slot_commit(nullptr, 0u);
+        },
+        [](int) {}, s_p, 0, [&](int, const uint8_t*, size_t, size_t, int) {}, [](int) {});
+    if (MODE == 6 && r.group_a()) {
+      r.slot_acquire();
+      r.slot_commit(nullptr, 0u, true);
+    }
+    if (MODE == 6 && r.storer && (threadIdx.x & 31) == 0) r.signal_loop();
+    r.split_end();
   }
   if (MODE == 3) {
     r.run(s_p[0], [&](const uint8_t* st, size_t e0, size_t units, int) {
@@ -173,6 +209,12 @@ int main() {
       float t1 = run<1>(x, c, n, out, st, nsm, 10, sc);
       float t2 = run<2>(x, c, n, out, st, nsm, 10, sc);
       float t3 = run<3>(x, c, n, out, st, nsm, 10, sc);
+      float t5 = run<5>(x, c, n, out, st, nsm, 10, sc);
+      float t7 = run<7>(x, c, n, out, st, nsm, 10, sc);
+      printf("  minmax as 4 interleaved chunk passes: %.1f us\n", t7 * 1e3);
+      float t6 = run<6>(x, c, n, out, st, nsm, 10, sc);
+      printf("  split pipe A quantize (10 warps, 3 stages): %.1f us; + credits/signaller: %.1f us\n", t5 * 1e3,
+             t6 * 1e3);
       printf("%s n=%zu (%.0f MB x): minmax %.1f us (%.0f GB/s) | quantize %.1f us (%.0f GB/s) | minmax+quantize(rev) "
              "%.1f us | decode %.1f us (%.0f GB/s)\n",
              dyn ? "dynamic" : "static ", n, mb, t0 * 1e3, mb / t0, t1 * 1e3, (n * 5.0 / 1e6) / t1, t2 * 1e3,
