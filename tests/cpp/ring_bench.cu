@@ -154,12 +154,16 @@ float run_ldg(const float* x, size_t n, float2* out, int nsm, int per_sm, int re
   return ms / reps;
 }
 
+float* g_cold[4] = {};  // when set: launches rotate over 4 inputs (> L2 each), so every read is cold
+
 template <int MODE>
 float run(float* x, uint8_t* c, size_t n, float2* out, int* st, int nsm, int reps, unsigned long long* sched) {
   CK(cudaFuncSetAttribute(ring_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingSmem));
   unsigned long long* sc = sched;
   void* args[] = {&x, &c, &n, &out, &st, &sc};
+  int launch = 0;
   auto go = [&] {
+    if (g_cold[0]) x = g_cold[launch++ % 4];
     CK(cudaLaunchCooperativeKernel((const void*)ring_kernel<MODE>, dim3(nsm), dim3(kRingThreads), args, kRingSmem, 0));
   };
   go();
@@ -199,6 +203,20 @@ int main() {
   CK(cudaMalloc(&sched, 65 * 8));
   CK(cudaMemset(sched, 0, 65 * 8));
   unsigned long long* endc = sched;  // static runs still need a valid end counter
+  for (int k = 0; k < 4; ++k) {
+    CK(cudaMalloc(&g_cold[k], nmax * 4));
+    CK(cudaMemset(g_cold[k], 0, nmax * 4));
+  }
+  {
+    const size_t n = nmax;
+    const double mb = n * 4.0 / 1e6;
+    float t0 = run<0>(x, c, n, out, st, nsm, 12, sched);
+    float t7 = run<7>(x, c, n, out, st, nsm, 12, sched);
+    float t1 = run<1>(x, c, n, out, st, nsm, 12, sched);
+    printf("COLD (4 rotating 400 MB inputs, dynamic): minmax %.1f us (%.0f GB/s) | 4 chunk passes %.1f us | quantize "
+           "%.1f us\n", t0 * 1e3, mb / t0, t7 * 1e3, t1 * 1e3);
+    g_cold[0] = nullptr;
+  }
   for (int dyn = 0; dyn < 2; ++dyn) {
     unsigned long long* sc = dyn ? sched : nullptr;
     (void)endc;
