@@ -192,16 +192,23 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     pf.n = msz;
     pf.eb = CODEC == kU8 ? 1 : 4;
     pf.nsrc = g;
+    // g >= 2: every rank writes its y of chunk k into ITS window (slot k) and
+    // the owner pulls them; g == 1 (identity): the old push into slot j
     for (int j = 0; j < g; ++j)
-      pf.base[j] = (CODEC == kU8 ? a.win[j] + a.off_recv1 + size_t(me) * a.slot_stride  // pulled from rank j
-                                 : a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride)  // pushed by rank j
-                   - size_t(pf.eb) * mbase;
-    pf.wait_flag = &mine->arrive1;  // uint8: every rank's header; identity: every rank's data
-    pf.wait_target = gmul;
-    if (CODEC == kU8) {  // uint8: each tile waits for its region's g contributions
+      pf.base[j] = (g >= 2 ? a.win[j] + a.off_recv1 + size_t(me) * a.slot_stride
+                           : a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride) -
+                   size_t(pf.eb) * mbase;
+    if (g >= 2) {  // each tile waits for its region's g contributions
       pf.gate = reinterpret_cast<const unsigned long long*>(a.win[me] + a.off_gate);
       pf.gate_mult = gmul;
+    }
+    if (CODEC == kU8) {
+      pf.wait_flag = &mine->arrive1;  // every rank's header
+      pf.wait_target = gmul;
       pf.reverse = true;
+    } else if (g == 1) {
+      pf.wait_flag = &mine->arrive1;  // my own push
+      pf.wait_target = gmul;
     }
   }
   __syncthreads();
@@ -368,8 +375,8 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
   auto fold1 = [&](size_t e) -> float {
     double acc = 0.0;
     for (int j = 0; j < g; ++j) {
-      const uint8_t* slot = CODEC == kU8 ? a.win[j] + a.off_recv1 + size_t(me) * a.slot_stride
-                                         : a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride;
+      const uint8_t* slot = g >= 2 ? a.win[j] + a.off_recv1 + size_t(me) * a.slot_stride
+                                   : a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride;
       const float d = CODEC == kU8 ? dequant1(__ldcg(slot + (e - mbase)), s_dec[j].lo, s_dec[j].step)
                                    : __ldcg(reinterpret_cast<const float*>(slot) + (e - mbase));
       acc = __dadd_rn(acc, double(d));
@@ -607,8 +614,86 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
       for (int gi = ct; gi < int(units * 4); gi += kConsumers) emit(e0 + 4 * size_t(gi), ys[gi]);
     });
     r.edges(ps, [&](size_t e) { emit1(e, a.x[e]); });
+  } else if (g >= 2) {
+    // -------------------------------- identity: copy to my window + pulled fold
+    // The uint8 phase-1B scheme without codes: pipe A copies y of chunk ck(i)
+    // into my window slot ck(i) and credits owner ck(i)'s region counters;
+    // pipe B folds my chunk from the g windows (TMA pulls) region by region
+    // as they land, straight into out2.
+    float* outf = reinterpret_cast<float*>(out2);
+    r.timed = a.trace != nullptr;
+    r.split_begin();
+    const int gct = r.gct, gn = r.gn;
+    if (r.storer && (threadIdx.x & 31) == 0) r.signal_loop();
+    r.stream_split(
+        s_pq, g,
+        [&](int i, const uint8_t* st, size_t e0, size_t units, int T) {
+          const int k = ck(i);
+          const float4* xs = reinterpret_cast<const float4*>(st);
+          const float4* ds = reinterpret_cast<const float4*>(st + size_t(T) * 64);
+          float4* dst = reinterpret_cast<float4*>(a.win[me] + a.off_recv1 + size_t(k) * a.slot_stride) +
+                        ((e0 - (pc[i].s & ~size_t(15))) >> 2);
+          r.slot_acquire();
+          for (int gi = gct; gi < int(units * 4); gi += gn) {
+            float4 y = xs[gi];
+            if (EC) y = sub4(y, ds[gi]);
+            dst[gi] = y;
+            if (a.check_finite) bad |= !finite4(y);
+            if (EC) dl4[(e0 >> 2) + gi] = sub4(y, y);
+          }
+          unsigned long long* sig = reinterpret_cast<unsigned long long*>(a.win[k] + a.off_gate) +
+                                    ((e0 >> 4) - pc[i].u0()) / kGateUnits;
+          r.slot_commit(sig, unsigned(units));
+        },
+        [](int) {}, s_pq + g, 1,
+        [&](int, const uint8_t* st, size_t e0, size_t units, int T) {
+          fold_pairs(st, units, T, true, gct, gn, [&](int gi, float4 y) {
+            const size_t e = e0 + 4 * size_t(gi);
+            if (EC) y = sub4(y, eps4(a.eps, e, mlo));
+            if (a.check_finite) bad |= !finite4(y);
+            if (EC) set_eps4(a.eps, e, mlo, sub4(y, y));
+            *reinterpret_cast<float4*>(outf + (e - mbase)) = y;
+          });
+        },
+        [](int) {});
+    if (r.group_a()) {  // marker: the signaller confirms everything and stops
+      r.slot_acquire();
+      r.slot_commit(nullptr, 0u, true);
+    }
+    r.split_end();
+    r.timed = false;
+    B2_TRACE(kTrP1Done);
+    // unaligned heads/tails (warp 0 of the last CTA): copies, announced on
+    // arrive_e; then the fold of my chunk's own heads/tails
+    if (cons && blockIdx.x == G - 1 && ct < 32) {
+      for (int i = 0; i < g; ++i) {
+        float* dstf = reinterpret_cast<float*>(a.win[me] + a.off_recv1 + size_t(ck(i)) * a.slot_stride);
+        const size_t ebase = pc[i].s & ~size_t(15);
+        r.edges(pc[i], [&](size_t e) {
+          float y = a.x[e];
+          if (EC) y = __fsub_rn(y, a.delta[e]);
+          dstf[e - ebase] = y;
+          if (a.check_finite) bad |= !finite_f(y);
+          if (EC) a.delta[e] = __fsub_rn(y, y);
+        });
+      }
+      __threadfence_system();
+      __syncwarp();
+      if (ct == 0) {
+        for (int i = 0; i < g; ++i) red_relaxed_sys_add(&hdr_of(a.win[ck(i)])->arrive_e, 1ull);
+        wait_geq(&mine->arrive_e, gmul, a.timeout_ns, a.status);
+      }
+      __syncwarp();
+      r.edges(pf, [&](size_t e) {
+        float y = fold1(e);
+        if (EC) y = __fsub_rn(y, a.eps[e - mlo]);
+        if (a.check_finite) bad |= !finite_f(y);
+        if (EC) a.eps[e - mlo] = __fsub_rn(y, y);
+        outf[e - mbase] = y;
+      });
+    }
   } else {
-    // ---------------------------------------------- identity: phase 1 push
+    // ------------------------------------- identity, one rank: phase 1 push
     // Step i stores chunk me+1+i into its owner's window (a permutation of
     // destinations across ranks); the last CTA to finish a step signals.
     for (int i = 0; i < g; ++i) {
