@@ -869,6 +869,9 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
     pg.eb = CODEC == kU8 ? 1 : 4;
     pg.nsrc = a.nnb;
     for (int i = 0; i < a.nnb; ++i) pg.base[i] = a.win[a.nbrs[i]] + a.off_dbuf;
+    pg.gate = reinterpret_cast<const unsigned long long*>(a.win[me] + a.off_gate);
+    pg.gate_mult = a.gate_mult;
+    pg.reverse = true;  // regions land in the order of the (reversed) encode
   }
   __syncthreads();
   const PassDesc& px = s_d[0];
@@ -921,7 +924,15 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
     return;
   }
 
-  // ----- publish: one encode of the whole bucket (collectives.cpp:266) or a stage copy
+  // ----- publish: one (min,max) of the whole bucket (collectives.cpp:266),
+  // the header, then -- in split mode -- pipe A encodes (or stages) the bucket
+  // into my parity buffer while pipe B gathers: each tile TMA-pulls the |N|
+  // encodings of one region (neighbours over NVLink, self locally) as soon as
+  // the region's counter says all |N| have landed, folds them in fp64 in
+  // ascending neighbour order, scales by 1/|N| and overwrites x (my own encode
+  // of that region has consumed it).  Counters are per call parity: a
+  // neighbour runs at most one call ahead.
+  U8Params q8{};
   if (CODEC == kU8) {
     float lo = kInf, hi = -kInf;
     r.run(px, [&](const uint8_t* st, size_t, size_t units, int) {
@@ -929,7 +940,6 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
       for (int gi = ct; gi < int(units * 4); gi += kConsumers) mm_acc(lo, hi, xs[gi]);
     });
     r.edges(px, [&](size_t e) { mm_acc1(lo, hi, a.x[e]); });
-    U8Params q8{};
     if (cons) {
       const float2 m0 = consumer_minmax(lo, hi, red);
       if (ct == 0) a.partials[blockIdx.x] = m0;
@@ -937,88 +947,121 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
       const float2 mm = reduce_partials(a.partials, G, red, ct);
       B2_TRACE(kTrP1FirstA);
       q8 = u8_params(mm.x, mm.y);
-      // the neighbours of two rounds ago must be done reading this buffer
       if (ct == 0) {
+        // the neighbours of two rounds ago must be done reading this buffer
         if (a.expected_reads) wait_geq(&mine->dreads[p], a.expected_reads, a.timeout_ns, a.status);
         if (blockIdx.x == 0) {
           mine->dhdr[p] = mm;
           if (a.n && !(finite_f(mm.x) && finite_f(mm.y))) latch(a.status, kStatusNonFinite);
+          __threadfence_system();
+          st_relaxed_sys(&mine->dready[p], a.epoch);  // header published
         }
       }
       consumer_sync();
     }
-    r.run(px, [&](const uint8_t* st, size_t e0, size_t units, int) {
-      const float4* xs = reinterpret_cast<const float4*>(st);
-      uint32_t* b32 = reinterpret_cast<uint32_t*>(mybuf + e0);
-      for (int gi = ct; gi < int(units * 4); gi += kConsumers) b32[gi] = quantize4(xs[gi], q8.lo, q8.inv);
-    });
-    r.edges(px, [&](size_t e) { mybuf[e] = quantize1(a.x[e], q8.lo, q8.inv); });
-  } else {
-    if (cons) {
-      if (ct == 0 && a.expected_reads) wait_geq(&mine->dreads[p], a.expected_reads, a.timeout_ns, a.status);
-      consumer_sync();
-    }
-    r.run(px, [&](const uint8_t* st, size_t e0, size_t units, int) {
-      const float4* xs = reinterpret_cast<const float4*>(st);
-      float4* b4 = reinterpret_cast<float4*>(mybuf + 4 * e0);
-      for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
-        b4[gi] = xs[gi];
-        if (a.check_finite) bad |= !finite4(xs[gi]);
-      }
-    });
-    r.edges(px, [&](size_t e) {
-      reinterpret_cast<float*>(mybuf)[e] = a.x[e];
-      if (a.check_finite) bad |= !finite_f(a.x[e]);
-    });
-  }
-  if (cons && consumer_arrive<false>(a.cta_done + 0, &s_flag) && ct == 0) st_relaxed_sys(&mine->dready[p], a.epoch);
-  B2_TRACE(kTrP1Done);
-
-  // ----- gather: every neighbour's buffer (self included), ascending order
-  const PassDesc& pg = s_d[2];
-  // producer: wait for every neighbour's publication before streaming
-  if (r.producer && (threadIdx.x & 31) == 0) {
-    for (int i = 0; i < a.nnb; ++i) wait_geq(&hdr_of(a.win[a.nbrs[i]])->dready[p], a.epoch, a.timeout_ns, a.status);
-    fence_proxy_async();
-  }
-  if (cons) {
-    if (ct == 0)
-      for (int i = 0; i < a.nnb; ++i)
-        wait_geq(&hdr_of(a.win[a.nbrs[i]])->dready[p], a.epoch, a.timeout_ns, a.status);
-    B2_TRACE(kTrP2Ready);
-    if (ct == 0) s_fast = 1;
-    consumer_sync();
-    if (CODEC == kU8 && ct < a.nnb) {
-      const float2 h = ld_peer_f2(&hdr_of(a.win[a.nbrs[ct]])->dhdr[p]);
-      const U8Params q = u8_params(h.x, h.y);
-      s_dec[ct] = SrcDec{q.lo, q.step, q.c23};
-      if (!(q.fastdec && fold_fast_ok(q.lo, q.step))) s_fast = 0;
-    }
+  } else if (cons) {
+    if (ct == 0 && a.expected_reads) wait_geq(&mine->dreads[p], a.expected_reads, a.timeout_ns, a.status);
     consumer_sync();
   }
   const double inv = a.inv;
-  const bool fast = s_fast != 0;
-  r.run(pg, [&](const uint8_t* st, size_t e0, size_t units, int T) {
-    const int ng = int(units * 4);
-    for (int gi = ct; gi < ng; gi += 2 * kConsumers) {
-      const int g1 = gi + kConsumers;
-      const bool has1 = g1 < ng;
-      float4 y0, y1;
-      fold2<CODEC>(a.nnb, fast, st, gi, has1 ? g1 : gi, T, s_dec, inv, y0, y1);
-      __stcs(x4 + ((e0 >> 2) + gi), y0);
-      if (has1) __stcs(x4 + ((e0 >> 2) + g1), y1);
+  r.split_begin();
+  const int gct = r.gct, gn = r.gn;
+  if (r.storer && (threadIdx.x & 31) == 0) {
+    // a credit's "sig" carries the region index: every neighbour's counter of
+    // that region (self included) gets the tile's units
+    r.signal_loop([&](unsigned long long* sig, unsigned v) {
+      const size_t region = reinterpret_cast<size_t>(sig) - 1;
+      for (int i = 0; i < a.nnb; ++i)
+        red_relaxed_sys_add(reinterpret_cast<unsigned long long*>(a.win[a.nbrs[i]] + a.off_gate) + region, v);
+    });
+  }
+  auto load_dec = [&]() {  // neighbours' headers -> smem (one thread)
+    if (CODEC != kU8) {
+      s_fast = 1;
+      return;
     }
-  });
-  r.edges(pg, [&](size_t e) {
-    double acc = 0.0;
-    for (int j = 0; j < a.nnb; ++j) {
-      const uint8_t* buf = a.win[a.nbrs[j]] + a.off_dbuf;
-      const float d = CODEC == kU8 ? dequant1(__ldcg(buf + e), s_dec[j].lo, s_dec[j].step)
-                                   : __ldcg(reinterpret_cast<const float*>(buf) + e);
-      acc = __dadd_rn(acc, double(d));
+    int fast = 1;
+    for (int i = 0; i < a.nnb; ++i) {
+      WinHdr* hk = hdr_of(a.win[a.nbrs[i]]);
+      wait_geq(&hk->dready[p], a.epoch, a.timeout_ns, a.status);
+      const float2 h = ld_peer_f2(&hk->dhdr[p]);
+      const U8Params q = u8_params(h.x, h.y);
+      s_dec[i] = SrcDec{q.lo, q.step, q.c23};
+      if (!(q.fastdec && fold_fast_ok(q.lo, q.step))) fast = 0;
     }
-    a.x[e] = __double2float_rn(__dmul_rn(acc, inv));
-  });
+    s_fast = fast;
+  };
+  r.stream_split(
+      &s_d[1], 1,
+      [&](int, const uint8_t* st, size_t e0, size_t units, int) {
+        const float4* xs = reinterpret_cast<const float4*>(st);
+        r.slot_acquire();
+        if (CODEC == kU8) {
+          uint32_t* b32 = reinterpret_cast<uint32_t*>(mybuf + e0);
+          for (int gi = gct; gi < int(units * 4); gi += gn) b32[gi] = quantize4(xs[gi], q8.lo, q8.inv);
+        } else {
+          float4* b4 = reinterpret_cast<float4*>(mybuf + 4 * e0);
+          for (int gi = gct; gi < int(units * 4); gi += gn) {
+            b4[gi] = xs[gi];
+            if (a.check_finite) bad |= !finite4(xs[gi]);
+          }
+        }
+        r.slot_commit(reinterpret_cast<unsigned long long*>((e0 >> 4) / kGateUnits + 1), unsigned(units));
+      },
+      [](int) {}, &s_d[2], 1,
+      [&](int, const uint8_t* st, size_t e0, size_t units, int T) {
+        const int ng = int(units * 4);
+        const bool fast = s_fast != 0;
+        for (int gi = gct; gi < ng; gi += 2 * gn) {
+          const int g1 = gi + gn;
+          const bool has1 = g1 < ng;
+          float4 y0, y1;
+          fold2<CODEC>(a.nnb, fast, st, gi, has1 ? g1 : gi, T, s_dec, inv, y0, y1);
+          __stcs(x4 + ((e0 >> 2) + gi), y0);
+          if (has1) __stcs(x4 + ((e0 >> 2) + g1), y1);
+        }
+      },
+      [&](int) { load_dec(); });
+  if (r.group_a()) {  // marker: the signaller confirms everything and stops
+    r.slot_acquire();
+    r.slot_commit(nullptr, 0u, true);
+  }
+  r.split_end();
+  B2_TRACE(kTrP1Done);
+  // unaligned tail (warp 0 of the last CTA): encode it, announce it on every
+  // neighbour's arrive_e, then fold it once every neighbour's tail is in
+  if (cons && blockIdx.x == G - 1 && ct < 32) {
+    r.edges(px, [&](size_t e) {
+      if (CODEC == kU8) {
+        mybuf[e] = quantize1(a.x[e], q8.lo, q8.inv);
+      } else {
+        reinterpret_cast<float*>(mybuf)[e] = a.x[e];
+        if (a.check_finite) bad |= !finite_f(a.x[e]);
+      }
+    });
+    __threadfence_system();
+    __syncwarp();
+    if (ct == 0) {
+      // per-parity tail counters (a neighbour may already be one call ahead);
+      // D_* windows do not use the C_* fields arrive1 / ready2
+      auto tail_ctr = [&](WinHdr* h) { return p ? &h->ready2 : &h->arrive1; };
+      for (int i = 0; i < a.nnb; ++i) red_relaxed_sys_add(tail_ctr(hdr_of(a.win[a.nbrs[i]])), 1ull);
+      wait_geq(tail_ctr(mine), a.gate_mult, a.timeout_ns, a.status);
+      load_dec();
+    }
+    __syncwarp();
+    const PassDesc& pg = s_d[2];
+    r.edges(pg, [&](size_t e) {
+      double acc = 0.0;
+      for (int j = 0; j < a.nnb; ++j) {
+        const uint8_t* buf = a.win[a.nbrs[j]] + a.off_dbuf;
+        const float d = CODEC == kU8 ? dequant1(__ldcg(buf + e), s_dec[j].lo, s_dec[j].step)
+                                     : __ldcg(reinterpret_cast<const float*>(buf) + e);
+        acc = __dadd_rn(acc, double(d));
+      }
+      a.x[e] = __double2float_rn(__dmul_rn(acc, inv));
+    });
+  }
   if (bad) latch(a.status, kStatusNonFinite);
   // ----- acknowledge the reads so each neighbour may reuse its buffer
   if (cons && consumer_arrive<false>(a.cta_done + 1, &s_flag) && ct == 0)

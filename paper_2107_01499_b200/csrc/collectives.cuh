@@ -85,6 +85,8 @@ struct DecentArgs {
   double inv;                   // 1/|N| (average) or 1.0 (sum), collectives.cpp:252-254
   uint8_t* win[kMaxRanks];
   size_t off_dbuf;              // offset of dbuf[parity]
+  size_t off_gate;              // arrival counters of my bucket's regions (all neighbours, cumulative)
+  unsigned long long gate_mult; // sum over this window's calls of |N|: counter target = gate_mult x units
   float2* partials;
   unsigned* cta_done;
   unsigned* gridbar;

@@ -398,8 +398,14 @@ struct Ring {
     if ((threadIdx.x & 31) == 0) mbar_arrive(staged + slot);
     advance_slot();
   }
-  // signaller lane 0: serve credits until the marker; returns after it
+  // signaller lane 0: serve credits until the marker; returns after it.
+  // emit(sig, value) performs one credit's signal after the batch fence
+  // (default: a relaxed system-scope red on sig).
   __device__ __forceinline__ void signal_loop() {
+    signal_loop([](unsigned long long* sig, unsigned v) { red_relaxed_sys_add(sig, v); });
+  }
+  template <class E>
+  __device__ __forceinline__ void signal_loop(E&& emit) {
     bool done = false;
     while (!done) {
       mbar_wait(staged + slot, sphase);
@@ -424,7 +430,7 @@ struct Ring {
       if (timed) wt[1] += globaltimer() - t0;
       for (int j = 0; j < n; ++j) {
         if (slot_len[slot] == 0) done = true;
-        if (slot_sig[slot]) red_relaxed_sys_add(slot_sig[slot], slot_sigv[slot]);
+        if (slot_sig[slot]) emit(slot_sig[slot], slot_sigv[slot]);
         mbar_arrive(sfree + slot);
         advance_slot();
       }
