@@ -835,7 +835,6 @@ __global__ void __launch_bounds__(kRingThreads, 1) central_kernel(CentralArgs a)
   extern __shared__ __align__(128) uint8_t smem[];
   Ring r;
   r.init(smem, a.status, a.timeout_ns, a.sched);
-  r.dbg = a.dbg;
   central_body<CODEC, EC>(a, r);
   r.finish(a.sched_end);
 }

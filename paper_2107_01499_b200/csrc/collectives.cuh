@@ -65,7 +65,6 @@ struct CentralArgs {
   int* status;                  // mapped host status word
   unsigned long long timeout_ns;
   unsigned long long* trace;    // [grid * kTraceSlots] globaltimer stamps, or null
-  int dbg;                      // experiment switch (B2_DBG env), 0 in production
 };
 
 // Dynamic tile counters per window: one per pass of a launch (C_*: at most

@@ -393,14 +393,6 @@ int b2_comm_sync(b2_comm_t c, void* stream) {
   return b2_comm_poll(c);
 }
 
-static int dbg_flag() {
-  static const int v = [] {
-    const char* e = getenv("B2_DBG");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 // B2_STATIC_SCHED=1: static round-robin tile assignment (A/B measurements)
 static bool static_sched() {
   static const bool v = [] {
@@ -448,7 +440,6 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   a.status = c->status_d;
   a.timeout_ns = c->timeout_ns;
   a.trace = c->trace;
-  a.dbg = dbg_flag();
   rc = launch_central(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity, delta != nullptr,
                       static_cast<cudaStream_t>(stream));
   if (rc == B2_OK) ++c->launches;

@@ -101,28 +101,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-// shared -> global (local HBM or a peer's window) bulk store, tracked by the
-// issuing thread's bulk async-group
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
-               "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-// the smem source of every committed bulk store but the N most recent has been read
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-// every committed bulk store but the N most recent has completed (writes performed)
-template <int N>
-__device__ __forceinline__ void bulk_wait() {
-  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { bulk_wait<0>(); }
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync %0, %1;" ::"n"(kConsumerBar), "n"(kConsumers) : "memory");
 }
@@ -250,7 +228,6 @@ struct Ring {
   bool timed = false;                   // accumulate wt[] (tracing only)
   int* status;
   unsigned long long timeout_ns;
-  int dbg = 0;  // experiment switch (B2_DBG): 1 = gpu-scope signal fence, 2 = none (unsound)
 
   __device__ void init(uint8_t* smem, int* st, unsigned long long to, unsigned long long* sched_ctrs = nullptr) {
     sched = sched_ctrs;
@@ -393,7 +370,7 @@ struct Ring {
       slot_sigv[slot] = sigv;
       slot_len[slot] = marker ? 0u : 1u;
     }
-    if (dbg != 3) fence_proxy_async();  // the stores will be read by TMA (async proxy)
+    fence_proxy_async();  // the stores will be read by TMA (async proxy)
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(staged + slot);
     advance_slot();
@@ -423,10 +400,7 @@ struct Ring {
         }
       }
       const unsigned long long t0 = tnow();
-      if (dbg == 0)
-        fence_acq_rel_sys();
-      else if (dbg == 1)
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      fence_acq_rel_sys();
       if (timed) wt[1] += globaltimer() - t0;
       for (int j = 0; j < n; ++j) {
         if (slot_len[slot] == 0) done = true;
