@@ -250,23 +250,46 @@ def run_b200(args, rank: int, world: int):
     barrier()
 
     # ---------------- end to end through the public API with host buffers
+    # Every step copies its input gradients from pinned host memory and reads
+    # its result back; steps are software-pipelined over two device buffers
+    # and three streams (H2D of step i+1 and D2H of step i-1 overlap the
+    # collective of step i: PCIe is full duplex), as a training loop would.
     host = torch.empty(n, dtype=torch.float32).pin_memory()   # the step's input gradients
     host.copy_(xs[-1].cpu())
-    host_out = torch.empty(n, dtype=torch.float32).pin_memory()  # the step's result
-    xd = torch.empty_like(x)
-    for _ in range(max(1, args.warmup // 2)):
-        xd.copy_(host, non_blocking=True)
-        step(xd)
-        host_out.copy_(xd, non_blocking=True)
+    host_out = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(2)]  # results
+    xd = [torch.empty_like(x) for _ in range(2)]
+    h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def e2e_run(steps, start_ev):
+        freed = [start_ev, start_ev]  # buffer b may be overwritten after this event
+        for i in range(steps):
+            bi = i % 2
+            with torch.cuda.stream(h2d_s):
+                h2d_s.wait_event(freed[bi])
+                xd[bi].copy_(host, non_blocking=True)
+                e_in = torch.cuda.Event()
+                e_in.record(h2d_s)
+            stream.wait_event(e_in)
+            step(xd[bi])
+            e_c = torch.cuda.Event()
+            e_c.record(stream)
+            with torch.cuda.stream(d2h_s):
+                d2h_s.wait_event(e_c)
+                host_out[bi].copy_(xd[bi], non_blocking=True)
+                freed[bi] = torch.cuda.Event()
+                freed[bi].record(d2h_s)
+        for ev in freed:
+            stream.wait_event(ev)
+
+    w0 = torch.cuda.Event()
+    w0.record(stream)
+    e2e_run(max(2, args.warmup // 2), w0)
     ep.sync()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e_steps = max(1, min(args.steps, args.e2e_steps))
+    e_steps = max(2, min(args.steps, args.e2e_steps))
     e0.record(stream)
-    for _ in range(e_steps):
-        xd.copy_(host, non_blocking=True)
-        step(xd)
-        host_out.copy_(xd, non_blocking=True)
+    e2e_run(e_steps, e0)
     e1.record(stream)
     e1.synchronize()
     ep.sync()
@@ -352,7 +375,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--prim", default="c_lp_s", choices=sorted(PRIMS))
     ap.add_argument("--n", type=int, default=None, help="elements per GPU (default: the BASELINE config size)")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--cpu-sample", type=int, default=25_000_000)
     ap.add_argument("--ref-sample", type=int, default=25_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -519,7 +519,9 @@ struct Ring {
             const PassDesc& p = ps[i];
             if (p.wait_flag && ld_acquire_sys(p.wait_flag) < p.wait_target) {
               if ((live & got) && !force) continue;
+              const unsigned long long t0 = tnow();
               wait_geq(p.wait_flag, p.wait_target, timeout_ns, status);
+              if (timed) wt[0] += globaltimer() - t0;
             }
             if (p.wait_flag) fence_proxy_async();
             ready(i);

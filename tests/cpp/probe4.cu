@@ -53,6 +53,7 @@ __global__ void a2a_kernel(uint8_t* const* dst, int ndst, size_t bytes_per_dst) 
 struct PullArgs {
   const uint8_t* src[8];
   int nsrc;
+  float4* out;  // non-null: decode-like expansion, 4 fp32 per code byte written here (like phase 3)
 };
 // pull `bytes` in total: nsrc sources of bytes/nsrc each, one tile = nsrc
 // bulk copies of 32 KB / nsrc (the fold's tile shape)
@@ -71,9 +72,18 @@ __global__ void __launch_bounds__(kRingThreads, 1) pull_kernel(PullArgs pa, size
   __syncthreads();
   const PassDesc& p = sp;
   float acc = 0.f;
-  r.run(p, [&](const uint8_t* s, size_t, size_t units, int) {
+  r.run(p, [&](const uint8_t* s, size_t e0, size_t units, int T) {
     const uint32_t* c = reinterpret_cast<const uint32_t*>(s);
-    for (int gi = r.ct; gi < int(units * 4); gi += kConsumers) acc += float(c[gi] & 1);
+    if (pa.out) {  // every source's codes -> fp32 at (source slice, e0)
+      for (int j = 0; j < pa.nsrc; ++j)
+        for (int gi = r.ct; gi < int(units * 4); gi += kConsumers) {
+          const uint32_t q = c[j * T * 4 + gi];
+          __stcs(pa.out + (size_t(j) * (bytes / pa.nsrc) / 4 + e0 / 4 + gi),
+                 make_float4(float(q & 255), float((q >> 8) & 255), float((q >> 16) & 255), float(q >> 24)));
+        }
+    } else {
+      for (int gi = r.ct; gi < int(units * 4); gi += kConsumers) acc += float(c[gi] & 1);
+    }
   });
   if (acc == 12345.f) out[0] = acc;
 }
@@ -234,6 +244,20 @@ int main(int argc, char** argv) {
     });
     printf("G=%d fold-shaped pull (1 local + %d peers per tile): %.0f GB/s remote ingress\n", G, G - 1,
            bytes * (G - 1) / G / t / 1e6);
+    std::vector<float4*> outs4(G);
+    for (int d = 0; d < G; ++d) {
+      CK(cudaSetDevice(d));
+      CK(cudaMalloc(&outs4[d], bytes * 4));
+    }
+    float t2 = timed([&](int d) {
+      PullArgs pa{};
+      pa.nsrc = G;
+      pa.out = outs4[d];
+      for (int j = 0; j < G; ++j) pa.src[j] = buf[(d + j) % G];
+      pull_kernel<<<nsm, kRingThreads, kRingSmem>>>(pa, bytes, outs[d], sts[d]);
+    });
+    printf("G=%d fold-shaped pull + 4x local fp32 writes (phase-3 shape): %.0f GB/s remote ingress, %.0f GB/s "
+           "written\n", G, bytes * (G - 1) / G / t2 / 1e6, bytes * 4.0 / t2 / 1e6);
   }
   {  // the C_LP_S phase-1B traffic mix at 100M fp32 per GPU
     const size_t n = 100000000;
