@@ -73,6 +73,8 @@ def algorithmic_bytes(prim: str, n: int, g: int):
     if prim == "c_lp_s":
         return 11 * n + n // g, 2 * n * (g - 1) // g
     if prim == "c_fp_s":
+        if g == 1:  # collectives.cpp:49: one worker returns x untouched -- no device work at all
+            return 0, 0
         return 4 * n + 4 * n // g + 8 * n * (g - 1) // g, 8 * n * (g - 1) // g
     if prim == "d_fp_s":
         return 4 * n * nb + 4 * n, 4 * n * (nb - 1)
@@ -318,13 +320,17 @@ def run_b200(args, rank: int, world: int):
     t_s = ms / 1e3
     t_roof_hbm = hbm_b / (hbm_peak * 1e9)
     t_roof_nvl = nvl_b / (NVL_PEER_GBS * 1e9)
-    if t_roof_nvl > t_roof_hbm:
+    if hbm_b == 0 and nvl_b == 0:
+        roof = {"bound": "none", "achieved": 0.0, "peak": hbm_peak, "unit": "GB/s", "peak_kind": "n/a",
+                "note": "no device work (C_FP_S with one worker returns x untouched, collectives.cpp:49); "
+                        "the step time is the host call"}
+    elif t_roof_nvl > t_roof_hbm:
         roof = {"bound": "nvlink", "achieved": round(nvl_b / t_s / 1e9, 2), "peak": NVL_PEER_GBS,
                 "unit": "GB/s", "peak_kind": "measured peer copy (B200_PROFILING.md); nominal 900"}
     else:
         roof = {"bound": "hbm", "achieved": round(hbm_b / t_s / 1e9, 2), "peak": hbm_peak, "unit": "GB/s",
                 "peak_kind": f"{peak_kind} HBM copy (MEASURED_PEAKS.json)"}
-    roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    roof["frac"] = round(roof["achieved"] / roof["peak"], 4) if roof["bound"] != "none" else None
     roof["traffic"] = args.traffic if args.traffic is not None else ncu_traffic(prim, g)
     roof["algorithmic_bytes"] = {"hbm": hbm_b, "nvlink_ingress": nvl_b}
     roof["t_roof_us"] = round(max(t_roof_hbm, t_roof_nvl) * 1e6, 1)
