@@ -120,7 +120,8 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
     // uint8 phase-1 region counters of my chunk (PassDesc::gate)
     w->off_gate = off;
     off += round_up(sizeof(unsigned long long) * (maxchunk / (16 * kGateUnits) + 2), 256);
-    w->slot_stride = round_up(size_t(elem) * (maxchunk + 8), 256);
+    // chunk k sits at slot offset e - (lo_k & ~15): up to 15 elements of head room
+    w->slot_stride = round_up(size_t(elem) * (maxchunk + 16), 256);
     w->off_recv1 = off;
     off += size_t(g) * w->slot_stride;
     w->off_out2 = off;

@@ -141,6 +141,43 @@ def run(args):
         orc.c_lp_s(want, codec=1)
         ck.eq(f"interleaved bucket {b}", ts[b].cpu().numpy(), want[rank])
 
+    # ---- back-to-back stress: many non-blocking calls on one bucket, two
+    # alternating buffers, one sync at the end (epoch counters, region
+    # counters, per-parity D_* buffers and counters with a random topology
+    # whose |N| changes every round, a neighbour running a call ahead)
+    n = 100_003
+    for prim in ("c_lp_s", "c_fp_s", "d_lp_s", "d_fp_s"):
+        bucket += 1
+        calls = 16
+        host = [[orc.synth(n, 900 + 10 * b + r) for r in range(g)] for b in range(2)]
+        ts = [torch.as_tensor(host[b][rank]).cuda() for b in range(2)]
+        topo = b2.Topology(b2.TopologyKind.random, g, 99)
+        for i in range(calls):
+            b = i % 2
+            if prim == "c_lp_s":
+                b2.c_lp_s(ep, 0.0, ts[b], U8, None, bucket=bucket, blocking=False)
+                want = [x.copy() for x in host[b]]
+                orc.c_lp_s(want, codec=1)
+            elif prim == "c_fp_s":
+                b2.c_fp_s(ep, 0.0, ts[b], bucket=bucket, blocking=False)
+                want = [x.copy() for x in host[b]]
+                orc.c_fp_s(want)
+            else:
+                fn = b2.d_lp_s if prim == "d_lp_s" else b2.d_fp_s
+                if prim == "d_lp_s":
+                    fn(ep, 0.0, ts[b], topo, i, U8, b2.ReduceMode.average, bucket=bucket, blocking=False)
+                else:
+                    fn(ep, 0.0, ts[b], topo, i, b2.ReduceMode.average, bucket=bucket, blocking=False)
+                want = []
+                for r in range(g):
+                    nb = topo.neighbors(r, i)
+                    srcs = [host[b][j] for j in nb]
+                    want.append(orc.d_lp_s_rank(srcs, 1, 1) if prim == "d_lp_s" else orc.d_fp_s_rank(srcs, 1))
+            host[b] = want
+        ep.sync()
+        for b in range(2):
+            ck.eq(f"stress {prim} buffer {b} after {calls} back-to-back calls", ts[b].cpu().numpy(), host[b][rank])
+
     # ---- large: owner-partition restatement + identical-replica digest
     if args.large:
         for n in (100_000_000,):
