@@ -145,8 +145,8 @@ def run(args):
     # alternating buffers, one sync at the end (epoch counters, region
     # counters, per-parity D_* buffers and counters with a random topology
     # whose |N| changes every round, a neighbour running a call ahead)
-    n = 100_003
-    for prim in ("c_lp_s", "c_fp_s", "d_lp_s", "d_fp_s"):
+    for n, prim in ((100_003, "c_lp_s"), (100_003, "c_fp_s"), (100_003, "d_lp_s"), (100_003, "d_fp_s"),
+                    (1_000_037, "c_lp_s"), (1_000_037, "d_lp_s")):
         bucket += 1
         calls = 16
         host = [[orc.synth(n, 900 + 10 * b + r) for r in range(g)] for b in range(2)]
@@ -177,6 +177,28 @@ def run(args):
         ep.sync()
         for b in range(2):
             ck.eq(f"stress {prim} buffer {b} after {calls} back-to-back calls", ts[b].cpu().numpy(), host[b][rank])
+
+    # ---- back-to-back with error feedback (uint8 and identity codec), state carried
+    for codec_kind, codec in ((1, U8), (0, ID)):
+        n = 70_001
+        bucket += 1
+        own = b2.owned_partition_len(n, g, rank)
+        es = b2.ErrorState(n, own)
+        deltas = [np.zeros(n, np.float32) for _ in range(g)]
+        eps = [np.zeros(b2.owned_partition_len(n, g, r), np.float32) for r in range(g)]
+        outs = []
+        for t_ in range(12):
+            grads = [orc.synth(n, 5000 + 100 * r + t_) for r in range(g)]
+            want = [x.copy() for x in grads]
+            orc.c_lp_s(want, codec=codec_kind, deltas=deltas, eps=eps)
+            t = torch.as_tensor(grads[rank]).cuda()
+            b2.c_lp_s(ep, 0.0, t, codec, es, bucket=bucket, blocking=False)
+            outs.append((t, want[rank]))
+        ep.sync()
+        for t_, (t, w) in enumerate(outs):
+            ck.eq(f"stress c_lp_s+EC codec={codec_kind} round={t_} x", t.cpu().numpy(), w)
+        ck.eq(f"stress c_lp_s+EC codec={codec_kind} delta", es.delta.cpu().numpy(), deltas[rank])
+        ck.eq(f"stress c_lp_s+EC codec={codec_kind} eps", es.epsilon.cpu().numpy(), eps[rank])
 
     # ---- large: owner-partition restatement + identical-replica digest
     if args.large:
