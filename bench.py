@@ -380,7 +380,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--prim", default="c_lp_s", choices=sorted(PRIMS))
-    ap.add_argument("--n", type=int, default=None, help="elements per GPU (default: the BASELINE config size)")
+    ap.add_argument("--n", "--elements", dest="n", type=int, default=None,
+                    help="elements per GPU (default: the BASELINE config size); use --elements under torchrun")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--cpu-sample", type=int, default=25_000_000)
     ap.add_argument("--ref-sample", type=int, default=25_000_000)
