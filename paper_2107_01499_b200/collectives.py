@@ -14,6 +14,7 @@ memory -- the end-to-end path a drop-in user of host vectors gets.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import enum
 import os
@@ -63,12 +64,27 @@ class Topology:
         self.kind, self.n, self.seed = TopologyKind(kind), int(n), int(seed)
 
     def neighbors(self, rank: int, round_: int) -> list[int]:
+        return list(self._neighbors_c(rank, round_)[0])
+
+    def _neighbors_c(self, rank: int, round_: int):
+        """-> (ctypes int array, count); ring / full do not depend on the round
+        and are cached (the per-call host cost matters for small buckets)."""
+        key = (int(self.kind), self.n, self.seed, rank, 0 if self.kind != TopologyKind.random else round_)
+        hit = _NBR_CACHE.get(key)
+        if hit is not None:
+            return hit
         out = (C.c_int * max(self.n, 3))()
         m = lib.b2_topology_neighbors(int(self.kind), self.n, self.seed & (2**64 - 1), rank,
                                       int(round_) & (2**64 - 1), out)
         if m < 0:
             raise Error(_lib.last_error())
-        return list(out[:m])
+        res = ((C.c_int * m)(*out[:m]), m)
+        if self.kind != TopologyKind.random:
+            _NBR_CACHE[key] = res
+        return res
+
+
+_NBR_CACHE: dict = {}
 
 
 # --------------------------------------------------------------- bootstrap
@@ -124,6 +140,7 @@ class B200Endpoint:
         self._bootstrap = bootstrap
         self._cb = _lib.ALLGATHER_FN(self._allgather)  # keep alive
         self._bytes_sent = 0
+        self._acct: dict = {}  # per-(primitive, codec, n) bytes sent, cached
         self._messages_sent = 0
         h = C.c_void_p()
         with torch.cuda.device(self.device):
@@ -244,6 +261,12 @@ class _Bucket:
     on exit when a staging copy was needed (host input or misalignment)."""
 
     def __init__(self, ep: B200Endpoint, x):
+        if (type(x) is torch.Tensor and x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
+                and x.data_ptr() % 16 == 0):  # the common case, no staging
+            self.orig = self.view = self.dev = x
+            self.host = False
+            self.n = x.numel()
+            return
         from .tensor import BucketArena, FlatTensor
         self.orig = x
         if isinstance(x, (FlatTensor, BucketArena)):
@@ -267,6 +290,8 @@ class _Bucket:
         self.n = self.dev.numel()
 
     def finish(self) -> None:
+        if self.dev is self.view:
+            return
         if self.host:
             res = self.dev.cpu()
             if isinstance(self.host_t, torch.Tensor):
@@ -275,6 +300,11 @@ class _Bucket:
                 np.copyto(self.host_t, res.numpy().reshape(np.shape(self.host_t)))
         elif self.dev is not self.view and self.dev.data_ptr() != self.view.data_ptr():
             self.view.copy_(self.dev.view_as(self.view))
+
+
+def _on_device(ep: B200Endpoint):
+    """torch.cuda.device(ep.device), skipped when it is already current."""
+    return contextlib.nullcontext() if torch.cuda.current_device() == ep.device else torch.cuda.device(ep.device)
 
 
 def _finish(ep: B200Endpoint, b: _Bucket, blocking: bool) -> None:
@@ -287,7 +317,7 @@ def c_fp_s(ep: B200Endpoint, now: float, x, bucket: int = 0, blocking: bool = Tr
     """Allreduce-equivalent; every rank ends with sum_j x_j folded in fp64 in
     ascending rank order (collectives.hpp:50-52)."""
     b = _Bucket(ep, x)
-    with torch.cuda.device(ep.device):
+    with _on_device(ep):
         check(lib.b2_c_fp_s(ep.handle, b.dev.data_ptr(), b.n, bucket, ep.stream()))
         _finish(ep, b, blocking)
     g, me = ep.world_size(), ep.rank()
@@ -316,13 +346,17 @@ def c_lp_s(ep: B200Endpoint, now: float, x, codec: Codec, es: ErrorState | None,
             raise Error("c_lp_s: delta must be 16-byte aligned")
         dptr, dlen = es.delta.data_ptr(), es.delta.numel()
         eptr, elen = (es.epsilon.data_ptr() if own else es.delta.data_ptr()), own
-    with torch.cuda.device(ep.device):
+    with _on_device(ep):
         check(lib.b2_c_lp_s(ep.handle, b.dev.data_ptr(), b.n, int(codec.kind), dptr, dlen, eptr, elen, bucket,
                             ep.stream()))
         _finish(ep, b, blocking)
     if g > 1:
-        per = lambda m: codec.payload_size(m)  # noqa: E731
-        sent = sum(per(partition_range(b.n, g, k)[1]) for k in range(g) if k != me) + (g - 1) * per(own)
+        key = ("c_lp_s", int(codec.kind), b.n)
+        sent = ep._acct.get(key)
+        if sent is None:
+            per = lambda m: codec.payload_size(m)  # noqa: E731
+            sent = sum(per(partition_range(b.n, g, k)[1]) for k in range(g) if k != me) + (g - 1) * per(own)
+            ep._acct[key] = sent
         ep._account(sent, 2 * (g - 1))
     return now
 
@@ -330,8 +364,7 @@ def c_lp_s(ep: B200Endpoint, now: float, x, codec: Codec, es: ErrorState | None,
 def _neighbors(ep: B200Endpoint, topo: Topology, round_: int):
     if topo.n != ep.world_size():
         raise Error("topology size mismatch")  # collectives.cpp:232
-    nb = topo.neighbors(ep.rank(), round_)
-    return (C.c_int * len(nb))(*nb), len(nb)
+    return topo._neighbors_c(ep.rank(), round_)
 
 
 def d_fp_s(ep: B200Endpoint, now: float, x, topo: Topology, round_: int, mode: ReduceMode,
@@ -339,7 +372,7 @@ def d_fp_s(ep: B200Endpoint, now: float, x, topo: Topology, round_: int, mode: R
     """Neighbourhood sum / average (collectives.hpp:63-66)."""
     arr, m = _neighbors(ep, topo, round_)
     b = _Bucket(ep, x)
-    with torch.cuda.device(ep.device):
+    with _on_device(ep):
         check(lib.b2_d_fp_s(ep.handle, b.dev.data_ptr(), b.n, arr, m, int(mode), bucket, ep.stream()))
         _finish(ep, b, blocking)
     ep._account((m - 1) * 4 * b.n, m - 1)
@@ -353,7 +386,7 @@ def d_lp_s(ep: B200Endpoint, now: float, x, topo: Topology, round_: int, codec: 
     codec._check_supported(rng)
     arr, m = _neighbors(ep, topo, round_)
     b = _Bucket(ep, x)
-    with torch.cuda.device(ep.device):
+    with _on_device(ep):
         check(lib.b2_d_lp_s(ep.handle, b.dev.data_ptr(), b.n, arr, m, int(codec.kind), int(mode), bucket,
                             ep.stream()))
         _finish(ep, b, blocking)
