@@ -869,7 +869,10 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
     pg.nsrc = a.nnb;
     for (int i = 0; i < a.nnb; ++i) pg.base[i] = a.win[a.nbrs[i]] + a.off_dbuf;
     pg.gate = reinterpret_cast<const unsigned long long*>(a.win[me] + a.off_gate);
-    pg.gate_mult = a.gate_mult;
+    pg.gate_mult = a.epoch;  // every neighbour's slot of the region >= this call's epoch
+    pg.gate_nsrc = a.nnb;
+    for (int i = 0; i < a.nnb; ++i) pg.gate_src[i] = a.nbrs[i];
+    pg.gate_stride = a.gate_stride;
     pg.reverse = true;  // regions land in the order of the (reversed) encode
   }
   __syncthreads();
@@ -966,12 +969,25 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
   r.split_begin();
   const int gct = r.gct, gn = r.gn;
   if (r.storer && (threadIdx.x & 31) == 0) {
-    // a credit's "sig" carries the region index: every neighbour's counter of
-    // that region (self included) gets the tile's units
+    // a credit's "sig" carries the region index.  My own counter of the
+    // region (cumulative over calls) collects every CTA's tiles; the credit
+    // that completes the region publishes this call's epoch into every
+    // neighbour's slot for me (self included).  Epochs, not counts: a
+    // neighbour with a different neighbourhood may run calls ahead of me
+    // and must not be mistaken for this call's writers.
+    unsigned long long* lctr = reinterpret_cast<unsigned long long*>(a.win[me] + a.off_lctr);
+    const size_t nun = a.n >> 4;
     r.signal_loop([&](unsigned long long* sig, unsigned v) {
       const size_t region = reinterpret_cast<size_t>(sig) - 1;
-      for (int i = 0; i < a.nnb; ++i)
-        red_relaxed_sys_add(reinterpret_cast<unsigned long long*>(a.win[a.nbrs[i]] + a.off_gate) + region, v);
+      const size_t left = nun - region * kGateUnits;
+      const unsigned long long units = left < size_t(kGateUnits) ? left : size_t(kGateUnits);
+      if (atomicAdd(lctr + region, static_cast<unsigned long long>(v)) + v == a.lctr_mult * units) {
+        __threadfence_system();  // every CTA's tiles of the region (fenced by their signallers) first
+        for (int i = 0; i < a.nnb; ++i)
+          st_relaxed_sys(reinterpret_cast<unsigned long long*>(a.win[a.nbrs[i]] + a.off_gate) +
+                             size_t(me) * a.gate_stride + region,
+                         a.epoch);
+      }
     });
   }
   auto load_dec = [&]() {  // neighbours' headers -> smem (one thread)
@@ -1041,11 +1057,16 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
     __threadfence_system();
     __syncwarp();
     if (ct == 0) {
-      // per-parity tail counters (a neighbour may already be one call ahead);
-      // D_* windows do not use the C_* fields arrive1 / ready2
-      auto tail_ctr = [&](WinHdr* h) { return p ? &h->ready2 : &h->arrive1; };
-      for (int i = 0; i < a.nnb; ++i) red_relaxed_sys_add(tail_ctr(hdr_of(a.win[a.nbrs[i]])), 1ull);
-      wait_geq(tail_ctr(mine), a.gate_mult, a.timeout_ns, a.status);
+      // the tail's slot (index gate_stride - 1) per source, epochs as for the regions
+      const size_t tail = a.gate_stride - 1;
+      for (int i = 0; i < a.nnb; ++i)
+        st_relaxed_sys(reinterpret_cast<unsigned long long*>(a.win[a.nbrs[i]] + a.off_gate) +
+                           size_t(me) * a.gate_stride + tail,
+                       a.epoch);
+      for (int i = 0; i < a.nnb; ++i)
+        wait_geq(reinterpret_cast<const unsigned long long*>(a.win[me] + a.off_gate) +
+                     size_t(a.nbrs[i]) * a.gate_stride + tail,
+                 a.epoch, a.timeout_ns, a.status);
       load_dec();
     }
     __syncwarp();

@@ -84,8 +84,10 @@ struct DecentArgs {
   double inv;                   // 1/|N| (average) or 1.0 (sum), collectives.cpp:252-254
   uint8_t* win[kMaxRanks];
   size_t off_dbuf;              // offset of dbuf[parity]
-  size_t off_gate;              // arrival counters of my bucket's regions (all neighbours, cumulative)
-  unsigned long long gate_mult; // sum over this window's calls of |N|: counter target = gate_mult x units
+  size_t off_gate;              // arrival slots [source rank][region + tail]: epoch of the source's last encode
+  size_t gate_stride;           // slots per source
+  size_t off_lctr;              // my cumulative per-region tile counters (units)
+  unsigned long long lctr_mult; // a region is complete at lctr_mult x its units (calls with |N| > 1 so far)
   float2* partials;
   unsigned* cta_done;
   unsigned* gridbar;

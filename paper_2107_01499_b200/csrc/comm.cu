@@ -42,10 +42,10 @@ struct Window {
   uint8_t* local = nullptr;
   uint8_t* peer[kMaxRanks] = {};
   bool ipc_opened[kMaxRanks] = {};
-  size_t off_gate = 0, gate_stride = 0, off_recv1 = 0, slot_stride = 0, off_out2 = 0, off_dbuf[2] = {0, 0};
+  size_t off_gate = 0, gate_stride = 0, off_lctr = 0, off_recv1 = 0, slot_stride = 0, off_out2 = 0, off_dbuf[2] = {0, 0};
   unsigned long long epoch = 0;
   unsigned long long exp_reads[2] = {0, 0};
-  unsigned long long gate_total[2] = {0, 0};  // D_*: sum of |N| over this window's calls, per parity
+  unsigned long long encodes = 0;  // D_*: calls that published (|N| > 1): my region counters' multiplier
   float2* partials = nullptr;
   unsigned* cta_done = nullptr;
   unsigned long long* sched = nullptr;  // [kSchedPasses] tile counters + end counter
@@ -127,11 +127,16 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
     w->off_out2 = off;
     off += w->slot_stride;
   } else {
-    // region counters of my bucket, one array per call parity (a neighbour
-    // can run at most one call ahead): every neighbour adds what it encoded
-    w->gate_stride = round_up(sizeof(unsigned long long) * (n / (16 * kGateUnits) + 2), 256);
+    // arrival slots: for every source rank one epoch per region of the
+    // bucket (+ one for the unaligned tail), written by that rank once it has
+    // encoded the region for the call of that epoch; then my own cumulative
+    // per-region tile counters (only I touch them)
+    const size_t nreg = n / (16 * kGateUnits) + 1;
+    w->gate_stride = nreg + 1;  // slots per source
     w->off_gate = off;
-    off += 2 * w->gate_stride;
+    off += round_up(sizeof(unsigned long long) * w->gate_stride * size_t(g), 256);
+    w->off_lctr = off;
+    off += round_up(sizeof(unsigned long long) * nreg, 256);
     const size_t b = round_up(size_t(elem) * (n + 8), 256);
     w->off_dbuf[0] = off;
     off += b;
@@ -495,8 +500,10 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
   a.inv = mode == B2_REDUCE_AVERAGE ? 1.0 / static_cast<double>(n_nbrs) : 1.0;
   for (int j = 0; j < c->world; ++j) a.win[j] = w->peer[j];
   a.off_dbuf = w->off_dbuf[a.parity];
-  a.off_gate = w->off_gate + size_t(a.parity) * w->gate_stride;
-  a.gate_mult = w->gate_total[a.parity] + static_cast<unsigned long long>(n_nbrs);
+  a.off_gate = w->off_gate;
+  a.gate_stride = w->gate_stride;
+  a.off_lctr = w->off_lctr;
+  a.lctr_mult = w->encodes + (n_nbrs > 1 ? 1 : 0);
   a.partials = w->partials;
   a.cta_done = w->cta_done;
   a.gridbar = w->cta_done + kMaxRanks + 2;
@@ -509,7 +516,7 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
                      static_cast<cudaStream_t>(stream));
   if (rc == B2_OK) {
     w->exp_reads[a.parity] += static_cast<unsigned long long>(n_nbrs - 1);
-    if (n_nbrs > 1) w->gate_total[a.parity] = a.gate_mult;
+    w->encodes = a.lctr_mult;
     ++c->launches;
   }
   return rc;

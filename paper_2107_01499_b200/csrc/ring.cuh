@@ -118,6 +118,13 @@ struct PassDesc {  // trivially constructible (lives in shared memory); build wi
   unsigned long long wait_target;
   const unsigned long long* gate;  // per-region arrival counters, or null
   unsigned long long gate_mult;
+  // gate_nsrc > 0: per-SOURCE epoch slots instead of one cumulative counter:
+  // region r is ready once gate[gate_src[s] * gate_stride + r] >= gate_mult
+  // for every s < gate_nsrc (writers that may run calls ahead -- D_* with a
+  // changing topology -- cannot be mistaken for the current call's writers)
+  int gate_nsrc;
+  int gate_src[kMaxRanks];
+  size_t gate_stride;
   bool reverse;  // walk the tiles backwards: re-reads the tail of a range
                  // that was streamed forwards just before from L2
   static __host__ __device__ PassDesc make() {
@@ -139,6 +146,20 @@ struct PassDesc {  // trivially constructible (lives in shared memory); build wi
   __host__ __device__ size_t body_begin() const { return nunits() ? 16 * u0() : s + n; }
   __host__ __device__ size_t body_end() const { return nunits() ? 16 * u1() : s + n; }
   __host__ __device__ size_t region_of(size_t t) const { return t * size_t(tile_units()) / kGateUnits; }
+  // all sources of region r have landed (acquire: the caller's TMA loads follow)
+  __device__ __forceinline__ bool gate_ready(size_t r, bool acquire) const {
+    if (gate_nsrc == 0) {
+      const unsigned long long v = acquire ? ld_acquire_sys(gate + r)
+                                           : *reinterpret_cast<const volatile unsigned long long*>(gate + r);
+      return v >= gate_target(r);
+    }
+    for (int s = 0; s < gate_nsrc; ++s) {
+      const unsigned long long* q = gate + size_t(gate_src[s]) * gate_stride + r;
+      const unsigned long long v = acquire ? ld_acquire_sys(q) : *reinterpret_cast<const volatile unsigned long long*>(q);
+      if (v < gate_mult) return false;
+    }
+    return true;
+  }
   __host__ __device__ unsigned long long gate_target(size_t r) const {
     const size_t left = nunits() - r * kGateUnits;
     return gate_mult * (left < size_t(kGateUnits) ? left : size_t(kGateUnits));
@@ -535,9 +556,7 @@ struct Ring {
             if (c != ~0ull) {
               const PassDesc& p = ps[i];
               const size_t rg = p.region_of((rev & bit) ? pst[i].nt - 1 - c : c);
-              if (pst[i].rdy != rg + 1 &&
-                  *reinterpret_cast<const volatile unsigned long long*>(p.gate + rg) < p.gate_target(rg))
-                continue;
+              if (pst[i].rdy != rg + 1 && !p.gate_ready(rg, false)) continue;
             }
           }
           const unsigned long long c = next(i, true);
@@ -556,7 +575,12 @@ struct Ring {
             const size_t rg = p.region_of(t);
             if (pst[i].rdy != rg + 1) {
               const unsigned long long t0 = tnow();
-              wait_geq(p.gate + rg, p.gate_target(rg), timeout_ns, status);
+              if (p.gate_nsrc == 0) {
+                wait_geq(p.gate + rg, p.gate_target(rg), timeout_ns, status);
+              } else {
+                for (int q = 0; q < p.gate_nsrc; ++q)
+                  wait_geq(p.gate + size_t(p.gate_src[q]) * p.gate_stride + rg, p.gate_mult, timeout_ns, status);
+              }
               if (timed) wt[0] += globaltimer() - t0;
               fence_proxy_async();
               pst[i].rdy = rg + 1;
