@@ -869,9 +869,12 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
     pg.nsrc = a.nnb;
     for (int i = 0; i < a.nnb; ++i) pg.base[i] = a.win[a.nbrs[i]] + a.off_dbuf;
     pg.gate = reinterpret_cast<const unsigned long long*>(a.win[me] + a.off_gate);
-    pg.gate_mult = a.epoch;  // every neighbour's slot of the region >= this call's epoch
+    pg.gate_mult = 1;  // units(r) = gate_target(r)
     pg.gate_nsrc = a.nnb;
-    for (int i = 0; i < a.nnb; ++i) pg.gate_src[i] = a.nbrs[i];
+    for (int i = 0; i < a.nnb; ++i) {
+      pg.gate_src[i] = a.nbrs[i];
+      pg.gate_tgt[i] = a.sends[i];
+    }
     pg.gate_stride = a.gate_stride;
     pg.reverse = true;  // regions land in the order of the (reversed) encode
   }
@@ -966,28 +969,18 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
     consumer_sync();
   }
   const double inv = a.inv;
+  r.timed = a.trace != nullptr;
   r.split_begin();
   const int gct = r.gct, gn = r.gn;
   if (r.storer && (threadIdx.x & 31) == 0) {
-    // a credit's "sig" carries the region index.  My own counter of the
-    // region (cumulative over calls) collects every CTA's tiles; the credit
-    // that completes the region publishes this call's epoch into every
-    // neighbour's slot for me (self included).  Epochs, not counts: a
-    // neighbour with a different neighbourhood may run calls ahead of me
-    // and must not be mistaken for this call's writers.
-    unsigned long long* lctr = reinterpret_cast<unsigned long long*>(a.win[me] + a.off_lctr);
-    const size_t nun = a.n >> 4;
+    // a credit's "sig" carries the region index: every neighbour's counter of
+    // that region for me (self included) gets the tile's units
     r.signal_loop([&](unsigned long long* sig, unsigned v) {
       const size_t region = reinterpret_cast<size_t>(sig) - 1;
-      const size_t left = nun - region * kGateUnits;
-      const unsigned long long units = left < size_t(kGateUnits) ? left : size_t(kGateUnits);
-      if (atomicAdd(lctr + region, static_cast<unsigned long long>(v)) + v == a.lctr_mult * units) {
-        __threadfence_system();  // every CTA's tiles of the region (fenced by their signallers) first
-        for (int i = 0; i < a.nnb; ++i)
-          st_relaxed_sys(reinterpret_cast<unsigned long long*>(a.win[a.nbrs[i]] + a.off_gate) +
-                             size_t(me) * a.gate_stride + region,
-                         a.epoch);
-      }
+      for (int i = 0; i < a.nnb; ++i)
+        red_relaxed_sys_add(reinterpret_cast<unsigned long long*>(a.win[a.nbrs[i]] + a.off_gate) +
+                                size_t(me) * a.gate_stride + region,
+                            v);
     });
   }
   auto load_dec = [&]() {  // neighbours' headers -> smem (one thread)
@@ -1042,6 +1035,25 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
     r.slot_commit(nullptr, 0u, true);
   }
   r.split_end();
+  if (a.trace) {
+    unsigned long long* tw = a.trace + size_t(blockIdx.x) * kTraceSlots + kTrWait;
+    if (ct == 0) {
+      tw[0] = r.wt[0];  // encode consumers: free credit
+      tw[4] = r.wt[2];  // encode consumers: full stage
+    } else if (ct == 32 * kSplitWarpsA) {
+      tw[5] = r.wt[2];  // gather consumers: full stage
+    } else if (r.producer && threadIdx.x == 0) {
+      tw[2] = r.wt[1];  // encode producer: free stage
+    } else if (r.producer2 && threadIdx.x == kProducer2) {
+      tw[1] = r.wt[0];  // gather producer: arrival slots
+      unsigned long long* ts = a.trace + size_t(blockIdx.x) * kTraceSlots + kTrP1Step;
+      ts[5] = r.pst2[0].first;  // p1_step5: first gather tile issued
+      ts[6] = r.pst2[0].last;   // p1_step6: last gather tile issued
+    } else if (r.storer && threadIdx.x == 32) {
+      tw[3] = r.wt[1];  // signaller: fences
+    }
+  }
+  r.timed = false;
   B2_TRACE(kTrP1Done);
   // unaligned tail (warp 0 of the last CTA): encode it, announce it on every
   // neighbour's arrive_e, then fold it once every neighbour's tail is in
@@ -1057,16 +1069,16 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
     __threadfence_system();
     __syncwarp();
     if (ct == 0) {
-      // the tail's slot (index gate_stride - 1) per source, epochs as for the regions
+      // the tail's counter (index gate_stride - 1) per source, counted like the regions
       const size_t tail = a.gate_stride - 1;
       for (int i = 0; i < a.nnb; ++i)
-        st_relaxed_sys(reinterpret_cast<unsigned long long*>(a.win[a.nbrs[i]] + a.off_gate) +
-                           size_t(me) * a.gate_stride + tail,
-                       a.epoch);
+        red_relaxed_sys_add(reinterpret_cast<unsigned long long*>(a.win[a.nbrs[i]] + a.off_gate) +
+                                size_t(me) * a.gate_stride + tail,
+                            1ull);
       for (int i = 0; i < a.nnb; ++i)
         wait_geq(reinterpret_cast<const unsigned long long*>(a.win[me] + a.off_gate) +
                      size_t(a.nbrs[i]) * a.gate_stride + tail,
-                 a.epoch, a.timeout_ns, a.status);
+                 a.sends[i], a.timeout_ns, a.status);
       load_dec();
     }
     __syncwarp();

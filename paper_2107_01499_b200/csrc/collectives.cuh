@@ -84,10 +84,9 @@ struct DecentArgs {
   double inv;                   // 1/|N| (average) or 1.0 (sum), collectives.cpp:252-254
   uint8_t* win[kMaxRanks];
   size_t off_dbuf;              // offset of dbuf[parity]
-  size_t off_gate;              // arrival slots [source rank][region + tail]: epoch of the source's last encode
-  size_t gate_stride;           // slots per source
-  size_t off_lctr;              // my cumulative per-region tile counters (units)
-  unsigned long long lctr_mult; // a region is complete at lctr_mult x its units (calls with |N| > 1 so far)
+  size_t off_gate;              // arrival counters [source rank][region + tail], cumulative units (tail: calls)
+  size_t gate_stride;           // counters per source
+  unsigned long long sends[kMaxRanks];  // per neighbour i: calls so far in which nbrs[i] sent to me (incl. this one)
   float2* partials;
   unsigned* cta_done;
   unsigned* gridbar;

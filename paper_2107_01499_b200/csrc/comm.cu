@@ -42,10 +42,10 @@ struct Window {
   uint8_t* local = nullptr;
   uint8_t* peer[kMaxRanks] = {};
   bool ipc_opened[kMaxRanks] = {};
-  size_t off_gate = 0, gate_stride = 0, off_lctr = 0, off_recv1 = 0, slot_stride = 0, off_out2 = 0, off_dbuf[2] = {0, 0};
+  size_t off_gate = 0, gate_stride = 0, off_recv1 = 0, slot_stride = 0, off_out2 = 0, off_dbuf[2] = {0, 0};
   unsigned long long epoch = 0;
   unsigned long long exp_reads[2] = {0, 0};
-  unsigned long long encodes = 0;  // D_*: calls that published (|N| > 1): my region counters' multiplier
+  unsigned long long sends_from[kMaxRanks] = {};  // D_*: calls (|N| > 1) in which rank j sent to me
   float2* partials = nullptr;
   unsigned* cta_done = nullptr;
   unsigned long long* sched = nullptr;  // [kSchedPasses] tile counters + end counter
@@ -127,16 +127,13 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
     w->off_out2 = off;
     off += w->slot_stride;
   } else {
-    // arrival slots: for every source rank one epoch per region of the
-    // bucket (+ one for the unaligned tail), written by that rank once it has
-    // encoded the region for the call of that epoch; then my own cumulative
-    // per-region tile counters (only I touch them)
+    // arrival counters: for every source rank one per region of the bucket
+    // (+ one for the unaligned tail), cumulative over the calls in which that
+    // rank was my neighbour (the relation is symmetric, so I know how many)
     const size_t nreg = n / (16 * kGateUnits) + 1;
-    w->gate_stride = nreg + 1;  // slots per source
+    w->gate_stride = nreg + 1;  // counters per source
     w->off_gate = off;
     off += round_up(sizeof(unsigned long long) * w->gate_stride * size_t(g), 256);
-    w->off_lctr = off;
-    off += round_up(sizeof(unsigned long long) * nreg, 256);
     const size_t b = round_up(size_t(elem) * (n + 8), 256);
     w->off_dbuf[0] = off;
     off += b;
@@ -502,8 +499,8 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
   a.off_dbuf = w->off_dbuf[a.parity];
   a.off_gate = w->off_gate;
   a.gate_stride = w->gate_stride;
-  a.off_lctr = w->off_lctr;
-  a.lctr_mult = w->encodes + (n_nbrs > 1 ? 1 : 0);
+  for (int i = 0; i < n_nbrs; ++i)
+    a.sends[i] = w->sends_from[nbrs[i]] + (n_nbrs > 1 ? 1 : 0);
   a.partials = w->partials;
   a.cta_done = w->cta_done;
   a.gridbar = w->cta_done + kMaxRanks + 2;
@@ -516,7 +513,8 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
                      static_cast<cudaStream_t>(stream));
   if (rc == B2_OK) {
     w->exp_reads[a.parity] += static_cast<unsigned long long>(n_nbrs - 1);
-    w->encodes = a.lctr_mult;
+    if (n_nbrs > 1)
+      for (int i = 0; i < n_nbrs; ++i) w->sends_from[nbrs[i]] = a.sends[i];
     ++c->launches;
   }
   return rc;

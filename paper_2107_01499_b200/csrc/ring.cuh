@@ -118,12 +118,15 @@ struct PassDesc {  // trivially constructible (lives in shared memory); build wi
   unsigned long long wait_target;
   const unsigned long long* gate;  // per-region arrival counters, or null
   unsigned long long gate_mult;
-  // gate_nsrc > 0: per-SOURCE epoch slots instead of one cumulative counter:
-  // region r is ready once gate[gate_src[s] * gate_stride + r] >= gate_mult
-  // for every s < gate_nsrc (writers that may run calls ahead -- D_* with a
-  // changing topology -- cannot be mistaken for the current call's writers)
+  // gate_nsrc > 0: one cumulative counter per SOURCE instead of one for all:
+  // region r is ready once gate[gate_src[s] * gate_stride + r] >=
+  // gate_tgt[s] * units(r) for every s < gate_nsrc.  (D_* with a changing
+  // topology: a rank that is not my neighbour in this call may run calls
+  // ahead and add to my counters; only my current neighbours' counters are
+  // checked, each against the number of calls in which it sent to me.)
   int gate_nsrc;
   int gate_src[kMaxRanks];
+  unsigned long long gate_tgt[kMaxRanks];
   size_t gate_stride;
   bool reverse;  // walk the tiles backwards: re-reads the tail of a range
                  // that was streamed forwards just before from L2
@@ -153,10 +156,11 @@ struct PassDesc {  // trivially constructible (lives in shared memory); build wi
                                            : *reinterpret_cast<const volatile unsigned long long*>(gate + r);
       return v >= gate_target(r);
     }
+    const unsigned long long u = gate_target(r) / (gate_mult ? gate_mult : 1);  // units of region r
     for (int s = 0; s < gate_nsrc; ++s) {
       const unsigned long long* q = gate + size_t(gate_src[s]) * gate_stride + r;
       const unsigned long long v = acquire ? ld_acquire_sys(q) : *reinterpret_cast<const volatile unsigned long long*>(q);
-      if (v < gate_mult) return false;
+      if (v < gate_tgt[s] * u) return false;
     }
     return true;
   }
@@ -578,8 +582,10 @@ struct Ring {
               if (p.gate_nsrc == 0) {
                 wait_geq(p.gate + rg, p.gate_target(rg), timeout_ns, status);
               } else {
+                const unsigned long long u = p.gate_target(rg) / (p.gate_mult ? p.gate_mult : 1);
                 for (int q = 0; q < p.gate_nsrc; ++q)
-                  wait_geq(p.gate + size_t(p.gate_src[q]) * p.gate_stride + rg, p.gate_mult, timeout_ns, status);
+                  wait_geq(p.gate + size_t(p.gate_src[q]) * p.gate_stride + rg, p.gate_tgt[q] * u, timeout_ns,
+                           status);
               }
               if (timed) wt[0] += globaltimer() - t0;
               fence_proxy_async();
