@@ -218,7 +218,7 @@ def run_b200(args, rank: int, world: int):
             s_ = torch.cuda.current_stream().cuda_stream
             b2._lib.check(b2.lib.b2_u8_encode(buf.data_ptr(), n, codes.data_ptr(), hdr.data_ptr(), s_))
             b2._lib.check(b2.lib.b2_u8_decode(codes.data_ptr(), hdr.data_ptr(), n, buf.data_ptr(), s_))
-            launches_box[0] += 4  # init keys, minmax, quantize, decode
+            launches_box[0] += 2  # encode_ring_kernel (one cooperative launch) + decode_ring_kernel
 
     def n_launches():
         return launches_box[0] if prim == "codec" else ep.launches()
@@ -338,7 +338,7 @@ def run_b200(args, rank: int, world: int):
                       "c_fp_s": "central_kernel<identity> (one fused launch per step)",
                       "d_fp_s": "decent_kernel<identity> (one fused launch per step)",
                       "d_lp_s": "decent_kernel<uint8> (one fused launch per step)",
-                      "codec": "minmax_keys_kernel + quantize_kernel + decode_kernel"}[prim]
+                      "codec": "encode_ring_kernel (min/max, grid barrier, quantize) + decode_ring_kernel"}[prim]
 
     per_gpu = 4 * n / t_s / 1e9
     label = PRIMS[prim][2]
