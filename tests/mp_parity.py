@@ -200,6 +200,30 @@ def run(args):
         ck.eq(f"stress c_lp_s+EC codec={codec_kind} delta", es.delta.cpu().numpy(), deltas[rank])
         ck.eq(f"stress c_lp_s+EC codec={codec_kind} eps", es.epsilon.cpu().numpy(), eps[rank])
 
+    # ---- engine: bucketed C_LP_S overlapping a synthetic backward on the
+    # compute stream (comm on its own stream); every bucket == the oracle's
+    # c_lp_s over that bucket's arena of every rank
+    from paper_2107_01499_b200.engine import OverlapEngine
+    sizes = [3000, 17, 70_001, 5, 250_000, 1024, 33_333]
+    eng = OverlapEngine(ep, sizes, capacity_bytes=4 * 100_000)
+    host = {}
+    for it in range(2):
+        for layer in reversed(range(len(sizes))):
+            vals = orc.synth(sizes[layer], 31_000 + 100 * it + 10 * layer + rank)
+            host[layer] = vals
+            torch.cuda._sleep(20_000)  # "backward" of this layer on the compute stream
+            eng.grad(layer).copy_(torch.as_tensor(vals), non_blocking=False)
+            eng.layer_done(layer)
+        eng.finish()
+        torch.cuda.synchronize()
+        for b in eng.buckets:
+            xs_b = []
+            for r in range(g):
+                parts = [orc.synth(sizes[layer], 31_000 + 100 * it + 10 * layer + r) for layer in b.layers]
+                xs_b.append(np.concatenate(parts).astype(np.float32))
+            orc.c_lp_s(xs_b, codec=1)
+            ck.eq(f"engine it={it} bucket {b.id} layers {b.layers}", eng.arenas[b.id].cpu().numpy(), xs_b[rank])
+
     # ---- large: owner-partition restatement + identical-replica digest
     if args.large:
         for n in (100_000_000,):
