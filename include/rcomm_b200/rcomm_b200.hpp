@@ -218,4 +218,50 @@ class BucketArena {
   std::vector<TensorView> members_;
 };
 
+// ----------------------------------------------------------------- engine
+// engine.hpp / engine.cpp:76-107: greedy reverse-order gradient bucketing
+// (layer L-1 first; a bucket closes when the next layer would exceed the
+// capacity; fusion off = one bucket per layer), and communication overlapping
+// backward: at a bucket's trigger layer (its last member to finish backward)
+// the bucket's collective is issued on a dedicated stream behind an event of
+// the compute stream.
+struct EngineBucket {
+  std::size_t id = 0;
+  std::vector<std::size_t> layers;  // backward order
+  std::size_t trigger_layer = 0;
+  std::size_t elements = 0;
+};
+std::vector<EngineBucket> plan_buckets(const std::vector<std::size_t>& layer_sizes,
+                                       std::size_t capacity_bytes = std::size_t(8) << 20, bool fusion = true);
+
+class OverlapEngine {
+ public:
+  enum class Primitive { c_lp_s, c_fp_s };
+  OverlapEngine(B200Endpoint& ep, std::vector<std::size_t> layer_sizes,
+                std::size_t capacity_bytes = std::size_t(8) << 20, bool fusion = true,
+                Primitive prim = Primitive::c_lp_s, std::uint32_t bucket_base = 1u << 20);
+  ~OverlapEngine();
+  OverlapEngine(const OverlapEngine&) = delete;
+  OverlapEngine& operator=(const OverlapEngine&) = delete;
+
+  const std::vector<EngineBucket>& buckets() const { return buckets_; }
+  float* grad(std::size_t layer);                // device view into the bucket arena
+  std::span<float> arena(std::size_t bucket);    // device span of one bucket
+  // layer's gradient is complete on compute_stream (cudaStream_t)
+  void layer_done(std::size_t layer, void* compute_stream);
+  // compute_stream waits for every bucket issued since the last finish()
+  void finish(void* compute_stream);
+
+ private:
+  B200Endpoint& ep_;
+  Primitive prim_;
+  std::uint32_t base_;
+  std::vector<std::size_t> sizes_;
+  std::vector<EngineBucket> buckets_;
+  std::vector<std::size_t> bucket_of_, offset_;
+  std::vector<float*> arenas_;
+  void* comm_ = nullptr;  // cudaStream_t
+  std::size_t pending_ = 0;
+};
+
 }  // namespace rcomm::b200

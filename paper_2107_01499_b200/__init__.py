@@ -22,8 +22,10 @@ from .collectives import (  # noqa: F401
     phase,
 )
 from .tensor import BucketArena, FlatTensor, TensorView  # noqa: F401
+from .engine import OverlapEngine, plan_buckets  # noqa: F401
 
 __all__ = [
+    "OverlapEngine", "plan_buckets",
     "B200Endpoint", "BucketArena", "Codec", "CodecKind", "Error", "ErrorState", "FlatTensor", "ReduceMode",
     "Rounding", "TensorView", "ThreadBootstrap", "Topology", "TopologyKind", "TorchBootstrap", "c_fp_s",
     "c_lp_s", "compensate_encode", "d_fp_s", "d_lp_s", "owned_partition_len", "partition_range", "phase",

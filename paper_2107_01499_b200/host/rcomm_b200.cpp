@@ -464,3 +464,103 @@ BucketArena BucketArena::flatten(std::span<FlatTensor*> tensors) {  // tensor.cp
 }
 
 }  // namespace rcomm::b200
+
+// ------------------------------------------------------------------- engine
+namespace rcomm::b200 {
+
+std::vector<EngineBucket> plan_buckets(const std::vector<std::size_t>& layer_sizes, std::size_t capacity_bytes,
+                                       bool fusion) {
+  if (layer_sizes.empty()) throw Error(B2_ERR_INVALID, "engine: model has no parameter tensors");  // engine.cpp:40
+  const std::size_t cap = fusion ? capacity_bytes : 0;
+  std::vector<EngineBucket> out;
+  std::size_t used = 0;
+  const std::size_t L = layer_sizes.size();
+  for (std::size_t i = 0; i < L; ++i) {  // engine.cpp:80-95
+    const std::size_t l = L - 1 - i;
+    const std::size_t bytes = 4 * layer_sizes[l];
+    if (out.empty() || used + bytes > cap) {
+      EngineBucket b;
+      b.id = out.size();
+      out.push_back(std::move(b));
+      used = 0;
+    }
+    out.back().layers.push_back(l);
+    out.back().trigger_layer = l;
+    out.back().elements += layer_sizes[l];
+    used += bytes;
+  }
+  return out;
+}
+
+OverlapEngine::OverlapEngine(B200Endpoint& ep, std::vector<std::size_t> layer_sizes, std::size_t capacity_bytes,
+                             bool fusion, Primitive prim, std::uint32_t bucket_base)
+    : ep_(ep), prim_(prim), base_(bucket_base), sizes_(std::move(layer_sizes)) {
+  buckets_ = plan_buckets(sizes_, capacity_bytes, fusion);
+  DeviceScope ds(ep_.device());
+  bucket_of_.assign(sizes_.size(), 0);
+  offset_.assign(sizes_.size(), 0);
+  for (const auto& b : buckets_) {
+    float* p = nullptr;
+    cuda_check(cudaMalloc(&p, std::max<std::size_t>(b.elements, 4) * sizeof(float)), "cudaMalloc bucket arena");
+    cuda_check(cudaMemset(p, 0, b.elements * sizeof(float)), "cudaMemset bucket arena");
+    arenas_.push_back(p);
+    std::size_t off = 0;
+    for (std::size_t l : b.layers) {
+      bucket_of_[l] = b.id;
+      offset_[l] = off;
+      off += sizes_[l];
+    }
+  }
+  cudaStream_t s;
+  cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate comm");
+  comm_ = s;
+}
+
+OverlapEngine::~OverlapEngine() {
+  DeviceScope ds(ep_.device());
+  if (comm_) {
+    cudaStreamSynchronize(static_cast<cudaStream_t>(comm_));
+    cudaStreamDestroy(static_cast<cudaStream_t>(comm_));
+  }
+  for (float* p : arenas_) cudaFree(p);
+}
+
+float* OverlapEngine::grad(std::size_t layer) { return arenas_.at(bucket_of_.at(layer)) + offset_[layer]; }
+
+std::span<float> OverlapEngine::arena(std::size_t bucket) {
+  return {arenas_.at(bucket), buckets_.at(bucket).elements};
+}
+
+void OverlapEngine::layer_done(std::size_t layer, void* compute_stream) {
+  const EngineBucket& b = buckets_.at(bucket_of_.at(layer));
+  if (layer != b.trigger_layer) return;
+  DeviceScope ds(ep_.device());
+  cudaEvent_t ev;
+  cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+  cuda_check(cudaEventRecord(ev, static_cast<cudaStream_t>(compute_stream)), "cudaEventRecord");
+  auto cs = static_cast<cudaStream_t>(comm_);
+  cuda_check(cudaStreamWaitEvent(cs, ev, 0), "cudaStreamWaitEvent");
+  cudaEventDestroy(ev);  // released once the wait is satisfied
+  const std::uint32_t bucket = base_ + static_cast<std::uint32_t>(b.id);
+  if (prim_ == Primitive::c_lp_s)
+    check(b2_c_lp_s(ep_.handle(), arenas_[b.id], b.elements, B2_CODEC_UNIFORM8, nullptr, 0, nullptr, 0, bucket, cs));
+  else
+    check(b2_c_fp_s(ep_.handle(), arenas_[b.id], b.elements, bucket, cs));
+  ++pending_;
+}
+
+void OverlapEngine::finish(void* compute_stream) {
+  if (pending_ != buckets_.size())
+    throw Error(B2_ERR_INVALID, "engine: " + std::to_string(pending_) + " of " + std::to_string(buckets_.size()) +
+                                    " buckets issued this iteration");
+  DeviceScope ds(ep_.device());
+  cudaEvent_t ev;
+  cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+  cuda_check(cudaEventRecord(ev, static_cast<cudaStream_t>(comm_)), "cudaEventRecord");
+  cuda_check(cudaStreamWaitEvent(static_cast<cudaStream_t>(compute_stream), ev, 0), "cudaStreamWaitEvent");
+  cudaEventDestroy(ev);
+  check(b2_comm_poll(ep_.handle()));  // a latched device error of an earlier bucket
+  pending_ = 0;
+}
+
+}  // namespace rcomm::b200

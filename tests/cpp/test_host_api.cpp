@@ -251,6 +251,67 @@ static void test_multi(int g) {
   report(ok, "c_lp_s + error feedback, 50 rounds, g=" + std::to_string(g));
 }
 
+// engine: plan KAT (test_engine.cpp:65-93) + bucketed C_LP_S overlapping a
+// compute stream, every bucket vs the oracle over that bucket of every rank
+void test_engine(int g) {
+  if (g == 1) {
+    auto b = plan_buckets({32, 8, 8, 1}, 40);
+    bool ok = b.size() == 3 && b[0].layers == std::vector<std::size_t>{3, 2} &&
+              b[1].layers == std::vector<std::size_t>{1} && b[2].layers == std::vector<std::size_t>{0} &&
+              b[0].trigger_layer == 2 && b[0].elements == 9 && b[2].elements == 32;
+    ok &= plan_buckets({32, 8, 8, 1}, 40, false).size() == 4;
+    report(ok, "engine plan_buckets (reference KATs)");
+    return;
+  }
+  const std::vector<std::size_t> sizes = {3000, 17, 70001, 5, 25000, 1024};
+  const auto plan = plan_buckets(sizes, 4 * 30000);
+  std::vector<std::vector<std::vector<float>>> got(g);  // [rank][bucket]
+  {
+    ThreadGroup group(g);
+    std::vector<std::thread> th;
+    for (int r = 0; r < g; ++r)
+      th.emplace_back([&, r] {
+        cudaSetDevice(r);
+        B200Endpoint ep(r, g, r, group.allgather(r));
+        OverlapEngine eng(ep, sizes, 4 * 30000);
+        cudaStream_t compute;
+        cudaStreamCreateWithFlags(&compute, cudaStreamNonBlocking);
+        for (std::size_t i = 0; i < sizes.size(); ++i) {
+          const std::size_t l = sizes.size() - 1 - i;
+          auto v = synth(sizes[l], 41000 + 10 * l + r);
+          cudaMemcpyAsync(eng.grad(l), v.data(), 4 * v.size(), cudaMemcpyHostToDevice, compute);
+          cudaStreamSynchronize(compute);  // v dies here
+          eng.layer_done(l, compute);
+        }
+        eng.finish(compute);
+        cudaStreamSynchronize(compute);
+        for (const auto& b : eng.buckets()) {
+          std::vector<float> h(b.elements);
+          cudaMemcpy(h.data(), eng.arena(b.id).data(), 4 * h.size(), cudaMemcpyDeviceToHost);
+          got[r].push_back(std::move(h));
+        }
+        cudaStreamDestroy(compute);
+      });
+    for (auto& t : th) t.join();
+  }
+  bool ok = true;
+  for (const auto& b : plan) {
+    std::vector<std::vector<float>> xs(g);
+    std::vector<float*> xp;
+    for (int r = 0; r < g; ++r) {
+      for (std::size_t l : b.layers) {
+        auto v = synth(sizes[l], 41000 + 10 * l + r);
+        xs[r].insert(xs[r].end(), v.begin(), v.end());
+      }
+      xp.push_back(xs[r].data());
+    }
+    orc_c_lp_s(g, b.elements, xp.data(), ORC_CODEC_UNIFORM8, nullptr, nullptr);
+    for (int r = 0; r < g; ++r) ok &= bitwise(got[r][b.id], xs[r]);
+  }
+  report(ok, "engine: bucketed c_lp_s overlapping a compute stream, g=" + std::to_string(g) + ", " +
+                 std::to_string(plan.size()) + " buckets");
+}
+
 int main() {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -262,6 +323,8 @@ int main() {
     test_tensor();
     test_single_rank();
     for (int g = 2; g <= std::min(ndev, 4); g *= 2) test_multi(g);
+    test_engine(1);
+    for (int g = 2; g <= std::min(ndev, 4); g *= 2) test_engine(g);
   } catch (const std::exception& e) {
     report(false, std::string("exception: ") + e.what());
   }
