@@ -1,16 +1,20 @@
 // ring.cuh -- warp-specialized TMA streaming for the persistent collective
-// kernels: one producer warp issues cp.async.bulk copies (global -- local
-// HBM or a peer GPU's window over NVLink -- into shared memory) into a ring
-// of kStages x kStageBytes stages guarded by mbarriers; kConsumerWarps
-// consumer warps compute from shared memory.  Memory-level parallelism is the
-// ring size (192 KB per SM in flight), independent of register count.
+// kernels: a producer warp issues cp.async.bulk copies (global -- local HBM
+// or a peer GPU's window over NVLink -- into shared memory) into a ring of
+// kStages x kStageBytes stages guarded by mbarriers; kConsumerWarps consumer
+// warps compute from shared memory.  Memory-level parallelism is the ring
+// (160 KB per SM in flight), independent of register count.
 //
 // A "pass" streams an element range [s, s+n) of up to kMaxRanks equally
 // shaped sources; its 16-element-aligned body is cut into tiles of
-// tile_units * 16 elements handed to CTAs round-robin.  The (< 16 element)
-// unaligned head and tail are processed by the consumers of the last CTA
-// with plain loads.  Producer and consumers walk identical tile sequences,
-// so the ring cursor (stage, phase) stays in lock step across passes.
+// tile_units * 16 elements.  Tiles are handed out "guided" (a static share
+// per CTA, the tail by a global atomic counter per pass), optionally gated on
+// arrival counters (PassDesc::gate); the producer tells the consumers which
+// tile a stage holds through shared memory (TileInfo), so several passes can
+// be interleaved tile by tile.  The (< 16 element) unaligned head and tail
+// are processed by the consumers of the last CTA with plain loads.  Split
+// mode runs two such pipelines side by side (split_begin); push credits hand
+// the consumers' stores to a signaller warp that publishes them (slot_commit).
 #pragma once
 
 #include <cstdint>
