@@ -96,6 +96,17 @@ int b2_u8_compensate_encode(const float* x, float* delta, size_t n, uint8_t* cod
 /* Exact reference wire bytes [min f32 LE][max f32 LE][u8 x n] (codec.hpp:21-24)
  * into a device buffer of 8 + n bytes, and back. */
 int b2_u8_pack_wire(const uint8_t* codes, const float* hdr, size_t n, uint8_t* wire, void* stream);
+
+/* Codec onebit (codec.cpp:81-88, 110-114): wire = [scale f32][ceil(n/8)
+ * bytes], scale = (float)(sum |x| in fp64) / (float)n, bit k (LE) = x[k] is
+ * not negative (signbit).  The fp64 sum is deterministic but not in the
+ * reference's order: scale is identical whenever that sum is exact and within
+ * one float rounding otherwise.  A non-finite input gives a NaN scale (the
+ * reference throws).  x, out, wire 16-byte aligned; wire holds 4 + ceil(n/8)
+ * bytes rounded up to 4.  (Replaces Codec{onebit}.encode / decode; C_LP_S with
+ * onebit still returns B2_ERR_UNSUPPORTED.) */
+int b2_onebit_encode(const float* x, size_t n, uint8_t* wire, void* stream);
+int b2_onebit_decode(const uint8_t* wire, size_t n, float* out, void* stream);
 int b2_u8_unpack_wire(const uint8_t* wire, size_t n, uint8_t* codes, float* hdr, void* stream);
 
 /* ----------------------------------------------------- bucket arena

@@ -47,6 +47,8 @@ class Oracle:
         L.orc_u8_encode.argtypes = [_f32p, _sz, _f32p, _f32p, _u8p]
         L.orc_u8_decode.argtypes = [C.c_float, C.c_float, _u8p, _sz, _f32p]
         L.orc_u8_encode_wire.argtypes = [_f32p, _sz, _u8p]
+        L.orc_onebit_encode_wire.argtypes = [_f32p, _sz, _u8p]
+        L.orc_onebit_decode_wire.argtypes = [_u8p, _sz, _f32p]
         L.orc_u8_compensate_encode.argtypes = [_f32p, _f32p, _sz, _f32p, _f32p, _u8p, _f32p]
         L.orc_c_fp_s.argtypes = [C.c_int, _sz, C.POINTER(_f32p)]
         L.orc_c_lp_s.argtypes = [C.c_int, _sz, C.POINTER(_f32p), C.c_int, C.POINTER(_f32p), C.POINTER(_f32p)]
@@ -94,6 +96,20 @@ class Oracle:
         if self.lib.orc_u8_encode_wire(_f(x), x.size, wire.ctypes.data_as(_u8p)):
             raise ValueError("encode: non-finite input value")
         return wire
+
+    def onebit_encode_wire(self, x):
+        """codec.cpp:81-88 (scalar kernels): [scale f32][ceil(n/8) sign bytes]."""
+        x = np.ascontiguousarray(x, np.float32)
+        wire = np.zeros(4 + (x.size + 7) // 8, np.uint8)
+        if self.lib.orc_onebit_encode_wire(_f(x), x.size, wire.ctypes.data_as(_u8p)):
+            raise ValueError("encode: non-finite input value")
+        return wire
+
+    def onebit_decode_wire(self, wire, n):
+        wire = np.ascontiguousarray(wire, np.uint8)
+        out = np.zeros(max(n, 1), np.float32)
+        self.lib.orc_onebit_decode_wire(wire.ctypes.data_as(_u8p), n, _f(out))
+        return out[:n]
 
     def compensate_encode(self, x, delta):
         """delta is updated in place; returns (lo, hi, codes, decoded)."""
@@ -186,9 +202,10 @@ class Reference:
 
     def encode(self, x, codec=1):
         x = np.ascontiguousarray(x, np.float32)
-        wire = np.zeros((8 + x.size) if codec == 1 else 4 * x.size + 1, np.uint8)
+        size = {0: 4 * x.size, 1: 8 + x.size, 2: 4 + (x.size + 7) // 8}[codec]
+        wire = np.zeros(size + 1, np.uint8)
         self._check(self.lib.ref_encode(codec, _f(x), x.size, wire.ctypes.data_as(_u8p)))
-        return wire[: (8 + x.size) if codec == 1 else 4 * x.size]
+        return wire[:size]
 
     def decode(self, wire, n, codec=1):
         wire = np.ascontiguousarray(wire, np.uint8)

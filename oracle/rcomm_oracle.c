@@ -246,3 +246,27 @@ void orc_synth(float* x, size_t n, uint64_t seed, uint64_t offset) {
     x[i] = (float)(m - 8388608) * 1.1920928955078125e-07f;
   }
 }
+
+/* ------------------------------------------------------------- onebit */
+/* codec.cpp:81-88 + kernels.cpp:26-32 (sum_abs, scalar: sequential fp64) and
+ * 58-63 (sign_pack) */
+int orc_onebit_encode_wire(const float* x, size_t n, uint8_t* wire) {
+  for (size_t k = 0; k < n; ++k)
+    if (!isfinite(x[k])) return ORC_ERR_NONFINITE; /* codec.cpp:24-27 */
+  double s = 0.0;
+  for (size_t k = 0; k < n; ++k) s += fabs((double)x[k]);
+  const float scale = n ? (float)s / (float)n : 0.0f;
+  memcpy(wire, &scale, 4);
+  const size_t nbytes = (n + 7) / 8;
+  for (size_t b = 0; b < nbytes; ++b) wire[4 + b] = 0;
+  for (size_t k = 0; k < n; ++k)
+    if (!signbit(x[k])) wire[4 + k / 8] |= (uint8_t)(1u << (k % 8));
+  return 0;
+}
+
+/* codec.cpp:110-114, kernels.cpp:65-69 (sign_unpack) */
+void orc_onebit_decode_wire(const uint8_t* wire, size_t n, float* out) {
+  float scale;
+  memcpy(&scale, wire, 4);
+  for (size_t k = 0; k < n; ++k) out[k] = ((wire[4 + k / 8] >> (k % 8)) & 1u) ? scale : -scale;
+}

@@ -42,6 +42,13 @@ void orc_dequantize_u8(const uint8_t* in, float* out, float min, float step, siz
 /* codec.cpp:24-27,40-80 (uniform8, nearest).  Returns ORC_ERR_NONFINITE where
  * the reference throws "encode: non-finite input value". */
 int orc_u8_encode(const float* x, size_t n, float* lo, float* hi, uint8_t* codes);
+/* codec.cpp:81-88 (onebit) with the scalar kernels (kernels.cpp:26-32,
+ * 58-63): scale = (float)(sequential fp64 sum of |x|) / (float)n; wire =
+ * [scale f32][ceil(n/8) bytes, bit k (LE) = !signbit(x[k])].  Returns
+ * ORC_ERR_NONFINITE where the reference throws. */
+int orc_onebit_encode_wire(const float* x, size_t n, uint8_t* wire);
+/* codec.cpp:110-114, kernels.cpp:65-69 */
+void orc_onebit_decode_wire(const uint8_t* wire, size_t n, float* out);
 /* codec.cpp:93-109 (uniform8) */
 void orc_u8_decode(float lo, float hi, const uint8_t* codes, size_t n, float* out);
 /* codec.cpp:31-38 + 58-59: exact wire bytes [min f32][max f32][u8 x n] */

@@ -70,7 +70,7 @@ int guarded(F fn) {
 }
 
 Codec make_codec(int kind) {
-  return Codec{kind == 0 ? CodecKind::identity : CodecKind::uniform8,
+  return Codec{kind == 0 ? CodecKind::identity : kind == 2 ? CodecKind::onebit : CodecKind::uniform8,
                Rounding::nearest};
 }
 

@@ -63,9 +63,9 @@ class Codec:
     def payload_size(self, n: int) -> int:
         return int(lib.b2_payload_size(int(self.kind), n))
 
-    def _check_supported(self, rng) -> None:
-        if self.kind == CodecKind.onebit:
-            raise _lib.B2Error(_lib.B2_ERR_UNSUPPORTED, "onebit codec is not implemented on the B200 path")
+    def _check_supported(self, rng, collective: bool = True) -> None:
+        if self.kind == CodecKind.onebit and collective:
+            raise _lib.B2Error(_lib.B2_ERR_UNSUPPORTED, "the onebit codec is not implemented in the B200 collectives")
         if self.kind == CodecKind.uniform8 and self.rounding == Rounding.stochastic:
             if rng is None:  # codec.cpp:70 wording
                 raise Error("uniform8 stochastic rounding needs a generator")
@@ -104,10 +104,19 @@ class Codec:
     def encode(self, x, rng=None):
         """Payload bytes.  Device input -> device uint8 tensor; host input ->
         numpy uint8 array (the reference's Payload)."""
-        self._check_supported(rng)
+        self._check_supported(rng, collective=False)
         xd, host = _as_device(x)
         xd = xd.reshape(-1)
         n = xd.numel()
+        if self.kind == CodecKind.onebit:  # codec.cpp:81-88
+            if not _aligned(xd):
+                xd = xd.clone()
+            wire = torch.empty(((4 + (n + 7) // 8) + 15) // 16 * 16, dtype=torch.uint8, device=xd.device)
+            check(lib.b2_onebit_encode(xd.data_ptr() if n else 0, n, wire.data_ptr(), _stream(xd.device)))
+            wire = wire[:self.payload_size(n)]
+            if bool(torch.isnan(wire[:4].view(torch.float32)).all()):  # the kernel's non-finite mark
+                raise Error("encode: non-finite input value")  # codec.cpp:24-27
+            return wire.cpu().numpy() if host is not None else wire
         if self.kind == CodecKind.identity:
             if n and not bool(torch.isfinite(xd).all()):
                 raise Error("encode: non-finite input value")
@@ -127,15 +136,17 @@ class Codec:
         else:
             out = n_or_out
             n = out.numel() if isinstance(out, torch.Tensor) else np.asarray(out).size
-        if self.kind == CodecKind.onebit:
-            raise _lib.B2Error(_lib.B2_ERR_UNSUPPORTED, "onebit codec is not implemented on the B200 path")
         size = payload.numel() if isinstance(payload, torch.Tensor) else len(payload)
         if size != self.payload_size(n):  # codec.cpp:96-97
             raise Error("decode: malformed payload (length mismatch)")
         dev = payload.device if not host else torch.device("cuda", torch.cuda.current_device())
         p = payload if not host else torch.as_tensor(np.asarray(payload, dtype=np.uint8)).to(dev)
         res = torch.empty(n, dtype=torch.float32, device=dev)
-        if n:
+        if n and self.kind == CodecKind.onebit:  # codec.cpp:110-114
+            w = torch.zeros(((size + 15) // 16) * 16, dtype=torch.uint8, device=dev)
+            w[:size].copy_(p.reshape(-1))
+            check(lib.b2_onebit_decode(w.data_ptr(), n, res.data_ptr(), _stream(dev)))
+        elif n:
             if self.kind == CodecKind.identity:
                 res.copy_(p.contiguous().view(torch.float32))
             else:
@@ -165,7 +176,7 @@ class ErrorState:
 def compensate_encode(codec: Codec, x, delta, rng=None, decoded: list | None = None):
     """codec.hpp:49-54 / codec.cpp:125-137: encodes Q(x - delta) and replaces
     delta by the exact residual (x - delta) - D(Q(x - delta))."""
-    codec._check_supported(rng)
+    codec._check_supported(rng, collective=False)
     xd, host = _as_device(x)
     n = xd.numel()
     host_delta = not (isinstance(delta, torch.Tensor) and delta.is_cuda)
@@ -177,6 +188,11 @@ def compensate_encode(codec: Codec, x, delta, rng=None, decoded: list | None = N
         payload = codec.encode(y)
         dec = y.clone()
         dd.copy_(y - dec)
+    elif codec.kind == CodecKind.onebit:  # y = x - delta; P = Q(y); delta = y - D(P), all exact fp32
+        y = xd.reshape(-1) - dd.reshape(-1)
+        payload = codec.encode(y)
+        dec = codec.decode(payload, n)
+        dd.copy_((y - dec).view_as(dd))
     else:
         xa = xd if _aligned(xd) else xd.clone()
         da = dd if _aligned(dd) and dd.is_contiguous() else dd.clone()

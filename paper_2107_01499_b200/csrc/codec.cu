@@ -13,6 +13,8 @@
 // element: 4 (pass 1) + 4 (pass 2, 0 when L2-resident) + 1 (codes).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -237,6 +239,117 @@ int grid_for(const void* f) { return persistent_grid(f, kThreads); }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// ---------------------------------------------------------------- onebit
+// Codec::encode onebit (codec.cpp:81-88): scale = (float)(sum |x| in fp64) /
+// (float)n, bit k of the LE bit string = !signbit(x[k]) (kernels.cpp:26-32,
+// 58-63); wire = [scale f32][ceil(n/8) bytes].  One thread per 32 elements
+// (one 32-bit word of bits); per-block fp64 partials are summed by the last
+// block in block order, so the result is deterministic -- but the fp64 sum's
+// order differs from the reference's (scalar: sequential; AVX2: 4 lanes), so
+// the scale equals the reference's whenever that sum is exact in fp64 (e.g.
+// inputs on a common 2^-k grid) and is within one float rounding otherwise
+// (the reference's own backends differ the same way).  A non-finite input
+// makes the scale NaN: the reference throws (codec.cpp:24-27).
+constexpr int kObThreads = 256;
+__global__ void __launch_bounds__(kObThreads) onebit_encode_kernel(const float* __restrict__ x, size_t n,
+                                                                  uint8_t* __restrict__ wire, double* partials,
+                                                                  unsigned* counter) {
+  __shared__ double red[kObThreads / 32];
+  __shared__ int bad_s[kObThreads / 32];
+  __shared__ bool last;
+  const size_t nwords = (n + 31) / 32, nbytes = (n + 7) / 8;
+  double acc = 0.0;
+  int bad = 0;
+  for (size_t w = size_t(blockIdx.x) * kObThreads + threadIdx.x; w < nwords; w += size_t(gridDim.x) * kObThreads) {
+    const size_t e0 = 32 * w;
+    unsigned bits = 0;
+    if (e0 + 32 <= n) {
+      const float4* x4 = reinterpret_cast<const float4*>(x + e0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 v = __ldcs(x4 + q);
+        const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          bits |= (__float_as_uint(e[j]) >> 31 ? 0u : 1u) << (4 * q + j);
+          acc = __dadd_rn(acc, fabs(double(e[j])));
+          bad |= !finite_f(e[j]);
+        }
+      }
+      *reinterpret_cast<unsigned*>(wire + 4 + 4 * w) = bits;
+    } else {
+      for (size_t k = e0; k < n; ++k) {
+        const float v = x[k];
+        bits |= (__float_as_uint(v) >> 31 ? 0u : 1u) << (k - e0);
+        acc = __dadd_rn(acc, fabs(double(v)));
+        bad |= !finite_f(v);
+      }
+      for (size_t b = 4 * w; b < nbytes; ++b) wire[4 + b] = uint8_t(bits >> (8 * (b - 4 * w)));
+    }
+  }
+  // block: fp64 partial (fixed tree order) and the non-finite flag
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+    bad |= __shfl_down_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = acc;
+    bad_s[threadIdx.x >> 5] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum = 0.0;
+    int any = 0;
+    for (int i = 0; i < kObThreads / 32; ++i) {
+      sum = __dadd_rn(sum, red[i]);
+      any |= bad_s[i];
+    }
+    partials[2 * blockIdx.x] = sum;
+    partials[2 * blockIdx.x + 1] = any ? 1.0 : 0.0;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {  // the last block: partials in block order, then the scale
+    __threadfence();
+    double sum = 0.0;
+    bool anybad = false;
+    for (unsigned i = 0; i < gridDim.x; ++i) {
+      sum = __dadd_rn(sum, __ldcg(partials + 2 * i));
+      anybad |= __ldcg(partials + 2 * i + 1) != 0.0;
+    }
+    const float scale = n ? __fdiv_rn(__double2float_rn(sum), float(n)) : 0.0f;
+    *reinterpret_cast<float*>(wire) = anybad ? __int_as_float(0x7fc00000) : scale;
+    *counter = 0u;
+  }
+}
+
+// Codec::decode onebit (codec.cpp:110-114, kernels.cpp:65-69)
+__global__ void __launch_bounds__(kObThreads) onebit_decode_kernel(const uint8_t* __restrict__ wire, size_t n,
+                                                                  float* __restrict__ out) {
+  const float scale = *reinterpret_cast<const float*>(wire);
+  const size_t nwords = (n + 31) / 32;
+  for (size_t w = size_t(blockIdx.x) * kObThreads + threadIdx.x; w < nwords; w += size_t(gridDim.x) * kObThreads) {
+    const size_t e0 = 32 * w;
+    if (e0 + 32 <= n) {
+      const unsigned bits = *reinterpret_cast<const unsigned*>(wire + 4 + 4 * w);
+      float4* o4 = reinterpret_cast<float4*>(out + e0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 v;
+        v.x = (bits >> (4 * q)) & 1u ? scale : -scale;
+        v.y = (bits >> (4 * q + 1)) & 1u ? scale : -scale;
+        v.z = (bits >> (4 * q + 2)) & 1u ? scale : -scale;
+        v.w = (bits >> (4 * q + 3)) & 1u ? scale : -scale;
+        __stcs(o4 + q, v);
+      }
+    } else {
+      for (size_t k = e0; k < n; ++k) out[k] = (wire[4 + k / 8] >> (k % 8)) & 1u ? scale : -scale;
+    }
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------- shared host utils
@@ -303,6 +416,56 @@ int b2_u8_encode(const float* x, size_t n, uint8_t* codes, float* hdr, void* str
   B2_REQUIRE(n == 0 || aligned16(x), "b2_u8_encode: x must be 16-byte aligned");
   B2_REQUIRE(n == 0 || aligned16(codes), "b2_u8_encode: codes must be 16-byte aligned");
   return launch_encode(x, nullptr, n, codes, hdr, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+// onebit scratch: per-block fp64 partials + the last-block counter, per device
+// (per device AND stream: encodes on different streams may run concurrently)
+static int onebit_scratch(double** partials, unsigned** counter, int grid, void* stream) {
+  static std::mutex mu;
+  static std::map<std::pair<int, void*>, std::pair<double*, unsigned*>> per_dev;
+  int dev = 0;
+  B2_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto& e = per_dev[{dev, stream}];
+  if (!e.first) {
+    B2_CUDA_TRY(cudaMalloc(&e.first, sizeof(double) * 2 * 4096));
+    B2_CUDA_TRY(cudaMalloc(&e.second, sizeof(unsigned)));
+    B2_CUDA_TRY(cudaMemset(e.second, 0, sizeof(unsigned)));
+  }
+  (void)grid;
+  *partials = e.first;
+  *counter = e.second;
+  return B2_OK;
+}
+
+int b2_onebit_encode(const float* x, size_t n, uint8_t* wire, void* stream) {
+  B2_REQUIRE(wire, "b2_onebit_encode: wire is null");
+  B2_REQUIRE(n == 0 || x, "b2_onebit_encode: x is null");
+  B2_REQUIRE(n == 0 || aligned16(x), "b2_onebit_encode: x must be 16-byte aligned");
+  B2_REQUIRE(aligned16(wire), "b2_onebit_encode: wire must be 16-byte aligned");
+  double* partials = nullptr;
+  unsigned* counter = nullptr;
+  const size_t nwords = (n + 31) / 32;
+  const int grid = int(std::min<size_t>(std::max<size_t>((nwords + kObThreads - 1) / kObThreads, 1),
+                                        size_t(sm_count()) * 4));
+  int rc = onebit_scratch(&partials, &counter, grid, stream);
+  if (rc) return rc;
+  onebit_encode_kernel<<<grid, kObThreads, 0, static_cast<cudaStream_t>(stream)>>>(x, n, wire, partials, counter);
+  B2_CUDA_TRY(cudaGetLastError());
+  return B2_OK;
+}
+
+int b2_onebit_decode(const uint8_t* wire, size_t n, float* out, void* stream) {
+  B2_REQUIRE(wire, "b2_onebit_decode: wire is null");
+  if (n == 0) return B2_OK;
+  B2_REQUIRE(out, "b2_onebit_decode: out is null");
+  B2_REQUIRE(aligned16(out), "b2_onebit_decode: out must be 16-byte aligned");
+  B2_REQUIRE(aligned16(wire), "b2_onebit_decode: wire must be 16-byte aligned");
+  const size_t nwords = (n + 31) / 32;
+  const int grid = int(std::min<size_t>((nwords + kObThreads - 1) / kObThreads, size_t(sm_count()) * 4));
+  onebit_decode_kernel<<<grid, kObThreads, 0, static_cast<cudaStream_t>(stream)>>>(wire, n, out);
+  B2_CUDA_TRY(cudaGetLastError());
+  return B2_OK;
 }
 
 int b2_u8_decode(const uint8_t* codes, const float* hdr, size_t n, float* out, void* stream) {

@@ -85,11 +85,58 @@ def test_nonfinite_raises():
         U8.decode(torch.tensor([1, 2, 3], dtype=torch.uint8).cuda(), 10)
 
 
-def test_stochastic_and_onebit_are_rejected():
+def test_stochastic_and_onebit_collective_are_rejected():
     with pytest.raises(b2.Error):
         b2.Codec(b2.CodecKind.uniform8, b2.Rounding.stochastic).encode(dev([1.0, 2.0]))
+    ep = b2.B200Endpoint(0, 1, 0)
+    with pytest.raises(b2.Error):  # C_LP_S with onebit: not on the B200 path yet
+        b2.c_lp_s(ep, 0.0, dev([1.0, 2.0]), b2.Codec(b2.CodecKind.onebit), None)
+    ep.close()
+
+
+# ------------------------------------------------------------------ onebit
+OB = b2.Codec(b2.CodecKind.onebit)
+
+
+def test_onebit_kats():
+    # test_codec.cpp:103-132
+    w = OB.encode(np.array([1, -1, 1, 1, -1, 1, 1, 1, -1], np.float32))
+    assert len(w) == 6 and w[:4].view(np.float32)[0] == 1.0 and w[4] == 0b11101101 and w[5] == 0
+    assert list(OB.decode(OB.encode(np.array([1, -2, 3], np.float32)), 3)) == [2.0, -2.0, 2.0]
+    assert list(OB.decode(OB.encode(np.array([-1, -3], np.float32)), 2)) == [-2.0, -2.0]
+    w0 = OB.encode(np.zeros(0, np.float32))
+    assert len(w0) == 4 and w0.view(np.float32)[0] == 0.0
     with pytest.raises(b2.Error):
-        b2.Codec(b2.CodecKind.onebit).encode(dev([1.0, 2.0]))
+        OB.encode(dev([1.0, float("inf")]))
+    with pytest.raises(b2.Error):
+        OB.encode(dev([float("nan")] * 40))
+
+
+@pytest.mark.parametrize("n", [1, 3, 31, 32, 33, 64, 1000, 4097, 100_003, 4_000_000])
+def test_onebit_vs_oracle(oracle, n):
+    # splitmix grid inputs: the fp64 |x| sum is exact in every order -> bit-exact wire
+    x = oracle.synth(n, 900 + n)
+    w = OB.encode(torch.as_tensor(x).cuda()).cpu().numpy()
+    assert np.array_equal(w, oracle.onebit_encode_wire(x))
+    y = OB.decode(torch.as_tensor(w).cuda(), n).cpu().numpy()
+    assert np.array_equal(y.view(np.uint32), oracle.onebit_decode_wire(w, n).view(np.uint32))
+    # signed zeros: bit = !signbit, so -0.0 decodes to -scale (kernels.cpp:58-63)
+    z = np.array([0.0, -0.0, 1.0, -1.0] * 9, np.float32)
+    assert np.array_equal(OB.encode(z), oracle.onebit_encode_wire(z))
+
+
+def test_onebit_compensate_encode(oracle):
+    n = 100_003
+    x = oracle.synth(n, 4242)
+    d0 = (oracle.synth(n, 4243) * np.float32(0.25)).astype(np.float32)
+    d = torch.as_tensor(d0).cuda()
+    dec = []
+    w = b2.compensate_encode(OB, torch.as_tensor(x).cuda(), d, decoded=dec)
+    y = (x - d0).astype(np.float32)
+    w_ref = oracle.onebit_encode_wire(y)
+    assert np.array_equal(w.cpu().numpy(), w_ref)
+    dref = oracle.onebit_decode_wire(w_ref, n)
+    assert np.array_equal(d.cpu().numpy().view(np.uint32), (y - dref).astype(np.float32).view(np.uint32))
 
 
 SIZES = [0, 1, 3, 7, 8, 9, 15, 16, 17, 64, 1000, 4097, 65537, 1_000_003]

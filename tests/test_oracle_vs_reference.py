@@ -68,3 +68,32 @@ def test_wire_counts_match_reference(ref):
     assert all(v == 4 * n * 2 * (g - 1) // g for v in b)
     bl = ref.c_lp_s([x.copy() for x in xs], codec=1)
     assert all(v == 2 * (g - 1) * (8 + n // g) for v in bl)
+
+
+@pytest.mark.parametrize("n", [1, 3, 8, 9, 37, 100_003])
+def test_onebit_codec_matches_reference(oracle, ref, n):
+    # codec.cpp:81-88, 110-114: sign bytes bit-exact; the scale from the
+    # reference's active backend (AVX2 sums |x| in 4 fp64 lanes, the scalar
+    # path sequentially) equals the oracle's (sequential) exactly when the
+    # fp64 sum is exact -- always for the splitmix grid inputs -- and within
+    # one float rounding for gaussians
+    x = ref.synth(n, 77 + n)
+    w_ref = ref.encode(x, codec=2)
+    w_orc = oracle.onebit_encode_wire(x)
+    assert np.array_equal(w_ref, w_orc)
+    assert np.array_equal(bits(ref.decode(w_ref, n, codec=2)), bits(oracle.onebit_decode_wire(w_orc, n)))
+    g = ref.random_normal(n, 5 + n) if hasattr(ref, "random_normal") else x
+    a, b = ref.encode(g, codec=2), oracle.onebit_encode_wire(g)
+    assert np.array_equal(a[4:], b[4:])
+    sa, sb = a[:4].view(np.float32)[0], b[:4].view(np.float32)[0]
+    assert abs(sa - sb) <= np.spacing(np.float32(max(abs(sa), abs(sb))))
+
+
+def test_onebit_reference_kats(oracle):
+    # test_codec.cpp:103-132, transcribed
+    w = oracle.onebit_encode_wire(np.array([1, -1, 1, 1, -1, 1, 1, 1, -1], np.float32))
+    assert w[:4].view(np.float32)[0] == 1.0 and w[4] == 0b11101101 and w[5] == 0
+    assert list(oracle.onebit_decode_wire(oracle.onebit_encode_wire(np.array([1, -2, 3], np.float32)), 3)) == \
+        [2.0, -2.0, 2.0]
+    assert list(oracle.onebit_decode_wire(oracle.onebit_encode_wire(np.array([-1, -3], np.float32)), 2)) == \
+        [-2.0, -2.0]
