@@ -59,6 +59,7 @@ PRIMS = {  # name -> (default elements, reference time_primitive id, metric labe
     "d_fp_s": (25_000_000, 3, "D_FP_S ring averaging"),
     "d_lp_s": (25_000_000, 4, "D_LP_S ring averaging"),
     "codec": (4_000_000, 0, "MinMaxUInt8 compress+decompress"),
+    "onebit": (4_000_000, 5, "Onebit compress+decompress"),
 }
 
 
@@ -80,6 +81,8 @@ def algorithmic_bytes(prim: str, n: int, g: int):
         return 4 * n * nb + 4 * n, 4 * n * (nb - 1)
     if prim == "d_lp_s":
         return 4 * n + n + n * nb + 4 * n, n * (nb - 1)
+    if prim == "onebit":  # read x, write bits, read bits, write x
+        return 8 * n + 2 * ((n + 7) // 8), 0
     return 10 * n, 0  # codec: read x, write codes, read codes, write x
 
 
@@ -152,7 +155,7 @@ def run_reference(args, rank: int, world: int):
     g = world
     n_sample = min(args.n, args.ref_sample)
     prim_id, label = PRIMS[args.prim][1], PRIMS[args.prim][2]
-    if args.prim == "codec":
+    if args.prim in ("codec", "onebit"):
         g = 1
     secs, backend = cpu_reference_gbs(prim_id, g, n_sample, args.warmup + args.steps)
     timed = secs[args.warmup:] or secs
@@ -194,13 +197,13 @@ def run_b200(args, rank: int, world: int):
     # needed either) pre-scaled by an exact power of two so that no buffer
     # overflows over its uses (quantization is scale-equivariant: same codes).
     total_calls = args.warmup + args.steps + 2
-    nbuf = 1 if prim.startswith("d_") or prim == "codec" else max(1, min(args.steps, 32))
+    nbuf = 1 if prim.startswith("d_") or prim in ("codec", "onebit") else max(1, min(args.steps, 32))
     uses = -(-total_calls // nbuf) + 1
     shrink = 0 if nbuf == 1 else min(120, int(math.ceil(uses * math.log2(max(g, 2)))) + 1)
     x.mul_(2.0 ** -shrink)
     xs = [x] + [x.clone() for _ in range(nbuf - 1)]
     ring = b2.Topology(b2.TopologyKind.ring, g, 0)
-    if prim == "codec":  # one GPU, the standalone codec kernels
+    if prim in ("codec", "onebit"):  # one GPU, the standalone codec kernels
         codes = torch.empty(n + 64, dtype=torch.uint8, device="cuda")
         hdr = torch.empty(4, dtype=torch.float32, device="cuda")
         launches_box = [0]
@@ -214,6 +217,11 @@ def run_b200(args, rank: int, world: int):
             b2.d_fp_s(ep, 0.0, buf, ring, 0, b2.ReduceMode.average, blocking=False)
         elif prim == "d_lp_s":
             b2.d_lp_s(ep, 0.0, buf, ring, 0, codec, b2.ReduceMode.average, blocking=False)
+        elif prim == "onebit":
+            s_ = torch.cuda.current_stream().cuda_stream
+            b2._lib.check(b2.lib.b2_onebit_encode(buf.data_ptr(), n, codes.data_ptr(), s_))
+            b2._lib.check(b2.lib.b2_onebit_decode(codes.data_ptr(), n, buf.data_ptr(), s_))
+            launches_box[0] += 2  # onebit_encode_kernel + onebit_decode_kernel
         else:
             s_ = torch.cuda.current_stream().cuda_stream
             b2._lib.check(b2.lib.b2_u8_encode(buf.data_ptr(), n, codes.data_ptr(), hdr.data_ptr(), s_))
@@ -221,7 +229,7 @@ def run_b200(args, rank: int, world: int):
             launches_box[0] += 2  # encode_ring_kernel (one cooperative launch) + decode_ring_kernel
 
     def n_launches():
-        return launches_box[0] if prim == "codec" else ep.launches()
+        return launches_box[0] if prim in ("codec", "onebit") else ep.launches()
 
     def barrier():
         if world > 1:
@@ -302,7 +310,7 @@ def run_b200(args, rank: int, world: int):
         ems = float(t.item())
 
     trace = None
-    if args.trace and prim != "codec":
+    if args.trace and prim not in ("codec", "onebit"):
         ep.enable_trace(True)
         barrier()
         for i in range(8):  # steady state: the last of 8 back-to-back calls is the one recorded
@@ -338,7 +346,8 @@ def run_b200(args, rank: int, world: int):
                       "c_fp_s": "central_kernel<identity> (one fused launch per step)",
                       "d_fp_s": "decent_kernel<identity> (one fused launch per step)",
                       "d_lp_s": "decent_kernel<uint8> (one fused launch per step)",
-                      "codec": "encode_ring_kernel (min/max, grid barrier, quantize) + decode_ring_kernel"}[prim]
+                      "codec": "encode_ring_kernel (min/max, grid barrier, quantize) + decode_ring_kernel",
+                      "onebit": "onebit_encode_kernel (fp64 |x| sum + sign bits) + onebit_decode_kernel"}[prim]
 
     per_gpu = 4 * n / t_s / 1e9
     label = PRIMS[prim][2]

@@ -275,9 +275,10 @@ int ref_time_primitive(int prim, int g, std::size_t len, int reps,
       for (int r = 0; r < g; ++r)
         synth(xs[static_cast<std::size_t>(r)].data(), len, 2026u + r);
       const auto t0 = std::chrono::steady_clock::now();
-      if (prim == 0) {
-        Payload p = u8.encode(xs[0]);
-        u8.decode(p, std::span<float>(xs[0]));
+      if (prim == 0 || prim == 5) {  // standalone codec: uniform8 (0) or onebit (5)
+        const Codec c = make_codec(prim == 0 ? 1 : 2);
+        Payload p = c.encode(xs[0]);
+        c.decode(p, std::span<float>(xs[0]));
       } else {
         SimCluster cluster(g, fast_profile());
         run_workers(cluster, g, [&](Endpoint& ep, int r) {
