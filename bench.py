@@ -60,6 +60,7 @@ PRIMS = {  # name -> (default elements, reference time_primitive id, metric labe
     "d_lp_s": (25_000_000, 4, "D_LP_S ring averaging"),
     "codec": (4_000_000, 0, "MinMaxUInt8 compress+decompress"),
     "onebit": (4_000_000, 5, "Onebit compress+decompress"),
+    "c_lp_s_onebit": (100_000_000, 6, "C_LP_S onebit allreduce"),
 }
 
 
@@ -81,6 +82,8 @@ def algorithmic_bytes(prim: str, n: int, g: int):
         return 4 * n * nb + 4 * n, 4 * n * (nb - 1)
     if prim == "d_lp_s":
         return 4 * n + n + n * nb + 4 * n, n * (nb - 1)
+    if prim == "c_lp_s_onebit":  # x 4N; bits N/8 out, N/8 folded, N/8g second bits, N/8 gathered; x' 4N
+        return 8 * n + 3 * n // 8 + n // (8 * g), n * (g - 1) // (4 * g)
     if prim == "onebit":  # read x, write bits, read bits, write x
         return 8 * n + 2 * ((n + 7) // 8), 0
     return 10 * n, 0  # codec: read x, write codes, read codes, write x
@@ -188,7 +191,7 @@ def run_b200(args, rank: int, world: int):
     n = args.n
     prim = args.prim
     ep = b2.B200Endpoint(rank, world, dev)
-    codec = b2.Codec(b2.CodecKind.uniform8)
+    codec = b2.Codec(b2.CodecKind.onebit if prim == "c_lp_s_onebit" else b2.CodecKind.uniform8)
     stream = torch.cuda.current_stream()
     x = torch.empty(n, dtype=torch.float32, device="cuda")
     b2._lib.check(b2.lib.b2_fill_synthetic(x.data_ptr(), n, 2026 + rank, 0, stream.cuda_stream))
@@ -209,7 +212,7 @@ def run_b200(args, rank: int, world: int):
         launches_box = [0]
 
     def step(buf):
-        if prim == "c_lp_s":
+        if prim in ("c_lp_s", "c_lp_s_onebit"):
             b2.c_lp_s(ep, 0.0, buf, codec, None, blocking=False)
         elif prim == "c_fp_s":
             b2.c_fp_s(ep, 0.0, buf, blocking=False)
@@ -343,6 +346,7 @@ def run_b200(args, rank: int, world: int):
     roof["algorithmic_bytes"] = {"hbm": hbm_b, "nvlink_ingress": nvl_b}
     roof["t_roof_us"] = round(max(t_roof_hbm, t_roof_nvl) * 1e6, 1)
     roof["kernel"] = {"c_lp_s": "central_kernel<uint8> (one fused launch per step)",
+                      "c_lp_s_onebit": "onebit_central_kernel<false> (one cooperative launch per step)",
                       "c_fp_s": "central_kernel<identity> (one fused launch per step)",
                       "d_fp_s": "decent_kernel<identity> (one fused launch per step)",
                       "d_lp_s": "decent_kernel<uint8> (one fused launch per step)",

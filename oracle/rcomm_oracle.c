@@ -132,6 +132,13 @@ static int enc_dec(int codec, const float* x, size_t n, float* out) {
     memcpy(out, x, n * sizeof(float));
     return ORC_OK;
   }
+  if (codec == ORC_CODEC_ONEBIT) { /* codec.cpp:81-88, 110-114 */
+    uint8_t* w = (uint8_t*)malloc(4 + (n + 7) / 8);
+    int rc = orc_onebit_encode_wire(x, n, w);
+    if (rc == ORC_OK) orc_onebit_decode_wire(w, n, out);
+    free(w);
+    return rc;
+  }
   uint8_t* c = (uint8_t*)malloc(n ? n : 1);
   float lo, hi;
   int rc = orc_u8_encode(x, n, &lo, &hi, c);

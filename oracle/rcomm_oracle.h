@@ -26,7 +26,7 @@ extern "C" {
 #endif
 
 enum { ORC_OK = 0, ORC_ERR_NONFINITE = -1, ORC_ERR_SIZE = -2 };
-enum { ORC_CODEC_IDENTITY = 0, ORC_CODEC_UNIFORM8 = 1 };
+enum { ORC_CODEC_IDENTITY = 0, ORC_CODEC_UNIFORM8 = 1, ORC_CODEC_ONEBIT = 2 };
 enum { ORC_REDUCE_SUM = 0, ORC_REDUCE_AVERAGE = 1 };
 
 /* collectives.cpp:167-175 */
@@ -63,7 +63,7 @@ int orc_u8_compensate_encode(const float* x, float* delta, size_t n, float* lo,
 void orc_c_fp_s(int g, size_t len, float* const* xs);
 
 /* c_lp_s -> scatter_reduce_lp, collectives.cpp:91-163 / 222-227, restated
- * partition by partition.  codec: ORC_CODEC_IDENTITY or ORC_CODEC_UNIFORM8.
+ * partition by partition.  codec: ORC_CODEC_IDENTITY, ORC_CODEC_UNIFORM8 or ORC_CODEC_ONEBIT.
  * deltas/eps NULL = stateless; else deltas[r] has len floats and eps[r] has
  * owned_partition_len(len, g, r) floats (ErrorState, codec.hpp:40-47). */
 int orc_c_lp_s(int g, size_t len, float* const* xs, int codec,

@@ -263,13 +263,15 @@ void ref_synth(float* x, std::size_t n, std::uint64_t seed) { synth(x, n, seed);
 // from thread spawn to join and therefore includes the reference's own
 // allocations and first touch.  Inputs are regenerated (untimed) before each
 // repetition.  prim: 0 codec(encode+decode, g must be 1), 1 c_fp_s,
-// 2 c_lp_s (uint8, no EC), 3 d_fp_s ring, 4 d_lp_s ring (uint8).
+// 2 c_lp_s (uint8, no EC), 3 d_fp_s ring, 4 d_lp_s ring (uint8),
+// 5 onebit codec (encode+decode, g must be 1), 6 c_lp_s (onebit, no EC).
 int ref_time_primitive(int prim, int g, std::size_t len, int reps,
                        double* seconds) {
   return guarded([&] {
     std::vector<std::vector<float>> xs(static_cast<std::size_t>(g),
                                        std::vector<float>(len));
     const Codec u8 = make_codec(1);
+    const Codec ob = make_codec(2);
     const Topology ring = make_topo(0, g, 0);
     for (int t = 0; t < reps; ++t) {
       for (int r = 0; r < g; ++r)
@@ -288,6 +290,7 @@ int ref_time_primitive(int prim, int g, std::size_t len, int reps,
             case 2: c_lp_s(ep, 0.0, x, u8, nullptr); break;
             case 3: d_fp_s(ep, 0.0, x, ring, 0, ReduceMode::average); break;
             case 4: d_lp_s(ep, 0.0, x, ring, 0, u8, ReduceMode::average); break;
+            case 6: c_lp_s(ep, 0.0, x, ob, nullptr); break;
             default: throw Error("unknown primitive");
           }
         });

@@ -63,9 +63,9 @@ class Codec:
     def payload_size(self, n: int) -> int:
         return int(lib.b2_payload_size(int(self.kind), n))
 
-    def _check_supported(self, rng, collective: bool = True) -> None:
-        if self.kind == CodecKind.onebit and collective:
-            raise _lib.B2Error(_lib.B2_ERR_UNSUPPORTED, "the onebit codec is not implemented in the B200 collectives")
+    def _check_supported(self, rng, collective: bool = True, onebit_ok: bool = False) -> None:
+        if self.kind == CodecKind.onebit and collective and not onebit_ok:
+            raise _lib.B2Error(_lib.B2_ERR_UNSUPPORTED, "the onebit codec is implemented for c_lp_s only")
         if self.kind == CodecKind.uniform8 and self.rounding == Rounding.stochastic:
             if rng is None:  # codec.cpp:70 wording
                 raise Error("uniform8 stochastic rounding needs a generator")

@@ -330,8 +330,9 @@ def c_fp_s(ep: B200Endpoint, now: float, x, bucket: int = 0, blocking: bool = Tr
 def c_lp_s(ep: B200Endpoint, now: float, x, codec: Codec, es: ErrorState | None, rng=None,
            bucket: int = 0, blocking: bool = True) -> float:
     """Compressed ScatterReduce with two compression phases
-    (collectives.hpp:54-61).  es != None applies error compensation."""
-    codec._check_supported(rng)
+    (collectives.hpp:54-61).  es != None applies error compensation.
+    Codec{onebit} is the 1-bit Adam aggregation (algorithms.cpp:141-148)."""
+    codec._check_supported(rng, onebit_ok=True)
     b = _Bucket(ep, x)
     g, me = ep.world_size(), ep.rank()
     own = owned_partition_len(b.n, g, me)

@@ -71,6 +71,23 @@ struct CentralArgs {
 // 3g+2 passes, D_*: 3), reset by the last CTA of every launch.
 constexpr int kSchedPasses = 64;
 
+// C_LP_S with the onebit codec (onebit_coll.cu).  Own window family: slot j
+// of recv1 = rank j's payload of my chunk, out2 = my phase-2 payload; every
+// payload is [scale f32 | 12 B pad][sign words] so the words are 16-aligned.
+struct OnebitArgs {
+  float* x;
+  size_t n;
+  int g, me;
+  unsigned long long epoch;     // 1-based call counter of this window
+  float* delta;                 // ErrorState::delta (n) or null
+  float* eps;                   // ErrorState::epsilon (owned len) or null
+  uint8_t* win[kMaxRanks];
+  size_t off_recv1, slot_stride, off_out2;
+  double* partials;             // local workspace [(g + 1) * grid] fp64 |y| partial sums
+  int* status;
+  unsigned long long timeout_ns;
+};
+
 // Decentralized neighbourhood reduce (D_FP_S, D_LP_S).
 struct DecentArgs {
   float* x;

@@ -29,13 +29,15 @@ namespace b2 {
 int launch_central(const CentralArgs& a, int codec, bool ec, cudaStream_t s);
 int launch_decent(const DecentArgs& a, int codec, cudaStream_t s);
 int max_persistent_grid();
+int launch_onebit_central(const OnebitArgs& a, bool ec, cudaStream_t s);
+size_t onebit_slot_bytes(size_t maxchunk);
 }  // namespace b2
 
 using namespace b2;
 
 namespace {
 
-enum Family { kCentral = 0, kDecentral = 1 };
+enum Family { kCentral = 0, kDecentral = 1, kOnebit = 2 };
 
 struct Window {
   size_t bytes = 0;
@@ -126,6 +128,13 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
     off += size_t(g) * w->slot_stride;
     w->off_out2 = off;
     off += w->slot_stride;
+  } else if (family == kOnebit) {
+    // slot j = rank j's onebit payload of my chunk; out2 = my phase-2 payload
+    w->slot_stride = onebit_slot_bytes((n + g - 1) / g);
+    w->off_recv1 = off;
+    off += size_t(g) * w->slot_stride;
+    w->off_out2 = off;
+    off += w->slot_stride;
   } else {
     // arrival counters: for every source rank one per region of the bucket
     // (+ one for the unaligned tail), cumulative over the calls in which that
@@ -146,7 +155,7 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
     return rc;
   };
   if (cudaMalloc(&w->local, w->bytes) != cudaSuccess ||
-      cudaMemset(w->local, 0, family == kCentral ? w->off_recv1 : w->off_dbuf[0]) != cudaSuccess ||
+      cudaMemset(w->local, 0, family == kDecentral ? w->off_dbuf[0] : w->off_recv1) != cudaSuccess ||
       cudaMalloc(&w->partials, sizeof(float2) * (kMaxRanks + 1) * max_persistent_grid()) !=
           cudaSuccess ||
       cudaMalloc(&w->cta_done, sizeof(unsigned) * (kMaxRanks + 4)) != cudaSuccess ||
@@ -449,6 +458,42 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   return rc;
 }
 
+// c_lp_s with Codec{onebit} (the 1-bit Adam aggregation, algorithms.cpp:141-148)
+static int onebit_central(b2_comm_t c, float* x, size_t n, float* delta, size_t delta_len, float* eps,
+                          size_t eps_len, uint32_t bucket, void* stream) {
+  int rc = check_comm(c, x, n);
+  if (rc) return rc;
+  B2_REQUIRE((delta == nullptr) == (eps == nullptr), "delta and eps must both be set or both null");
+  const size_t own = b2_owned_partition_len(n, c->world, c->rank);
+  if (delta) {  // collectives.cpp:102-107
+    B2_REQUIRE(delta_len == n, "c_lp_s: delta length does not match bucket length");
+    B2_REQUIRE(eps_len == own, "c_lp_s: epsilon length does not match owned partition");
+  }
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  Window* w = nullptr;
+  rc = get_window(c, bucket, kOnebit, n, 1, &w);
+  if (rc) return rc;
+  OnebitArgs a{};
+  a.x = x;
+  a.n = n;
+  a.g = c->world;
+  a.me = c->rank;
+  a.epoch = ++w->epoch;
+  a.delta = delta;
+  a.eps = eps;
+  for (int j = 0; j < c->world; ++j) a.win[j] = w->peer[j];
+  a.off_recv1 = w->off_recv1;
+  a.slot_stride = w->slot_stride;
+  a.off_out2 = w->off_out2;
+  a.partials = reinterpret_cast<double*>(w->partials);
+  a.status = c->status_d;
+  a.timeout_ns = c->timeout_ns;
+  rc = launch_onebit_central(a, delta != nullptr, static_cast<cudaStream_t>(stream));
+  if (rc == B2_OK) ++c->launches;
+  return rc;
+}
+
 int b2_c_fp_s(b2_comm_t c, float* x, size_t n, uint32_t bucket, void* stream) {
   int rc = check_comm(c, x, n);
   if (rc) return rc;
@@ -458,10 +503,7 @@ int b2_c_fp_s(b2_comm_t c, float* x, size_t n, uint32_t bucket, void* stream) {
 
 int b2_c_lp_s(b2_comm_t c, float* x, size_t n, int codec, float* delta, size_t delta_len,
               float* eps, size_t eps_len, uint32_t bucket, void* stream) {
-  if (codec == B2_CODEC_ONEBIT) {
-    set_error("c_lp_s: onebit codec is not implemented on the B200 path");
-    return B2_ERR_UNSUPPORTED;
-  }
+  if (codec == B2_CODEC_ONEBIT) return onebit_central(c, x, n, delta, delta_len, eps, eps_len, bucket, stream);
   B2_REQUIRE(codec == B2_CODEC_UNIFORM8 || codec == B2_CODEC_IDENTITY, "unknown codec %d", codec);
   return central(c, x, n, codec, 1, delta, delta_len, eps, eps_len, bucket, stream);
 }

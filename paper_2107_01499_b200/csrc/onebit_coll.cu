@@ -1,0 +1,278 @@
+// onebit_coll.cu -- C_LP_S with the onebit codec: the aggregation the
+// reference's 1-bit Adam runs on its momentum every compressed step
+// (algorithms.cpp:141-148 -> aggregate_centralized -> c_lp_s with
+// Codec{onebit} and the bucket's ErrorState).
+//
+// Same structure as scatter_reduce_lp (collectives.cpp:91-163), one
+// cooperative launch per call:
+//   phase 1  every chunk k of (x - delta): sign bits (kernels.cpp:58-63) are
+//            stored straight into owner k's window slot [me] over NVLink while
+//            the fp64 sum |y| (kernels.cpp:26-32) accumulates; grid barrier;
+//            scale_k = (float)sum / (float)n_k (codec.cpp:81-88) goes to the
+//            slot header, then one release per owner.  With error feedback a
+//            second local pass writes delta = y - D(P) (codec.cpp:125-137).
+//   phase 2  (owner) fold D(P_j) in fp64, ranks ascending (collectives.cpp:
+//            125-142), y2 = (float)acc - eps, sign bits + fp64 sum |y2| into
+//            my out2, grid barrier, scale2, publish; eps = y2 - D(P2).
+//   phase 3  every owner's out2 decoded into x (collectives.cpp:154-161).
+//
+// Layout: a warp tile is 1024 consecutive chunk elements; lane l of row r
+// holds element 32r + l, so one __ballot_sync per row yields the row's
+// 32-bit LE sign word exactly as sign_pack lays it out (bit k%8 of byte
+// k/8), and decode is one shuffle per row.  Loads/stores are 128 B per warp
+// instruction; the words of a tile are one 128 B line.
+//
+// Exactness: signs, the ascending fp64 fold and every fp32 expression are
+// the reference's.  The fp64 |y| sums are summed in a fixed tree order, not
+// sequentially, so a scale can differ from the reference's by one float
+// rounding when the fp64 sum is inexact (the reference's scalar and AVX2
+// backends differ the same way); on inputs whose fp64 sums are exact the
+// whole result is bit-identical (tests/mp_parity.py).
+#include <cooperative_groups.h>
+
+#include "b2_host.h"
+#include "collectives.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace b2 {
+namespace {
+
+constexpr int kThr = 256;
+constexpr int kWarps = kThr / 32;
+constexpr size_t kTile = 1024;  // elements per warp tile = 32 sign words
+
+__device__ __forceinline__ void chunk_range(size_t n, int g, int k, size_t& lo, size_t& sz) {
+  const size_t base = n / size_t(g), extra = n % size_t(g), uk = size_t(k);  // collectives.cpp:167-175
+  lo = uk * base + (uk < extra ? uk : extra);
+  sz = base + (uk < extra ? 1 : 0);
+}
+
+// Block sum in a fixed order (warp tree, then warps ascending); result on thread 0.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kWarps; ++i) s = __dadd_rn(s, red[i]);
+  __syncthreads();
+  return s;
+}
+
+// Every CTA reduces the same partials in the same order -> the same scale,
+// returned to every thread of the CTA.
+__device__ __forceinline__ float scale_of(const double* partials, size_t nk, double* red) {
+  double v = 0.0;
+  for (unsigned c = threadIdx.x; c < gridDim.x; c += kThr) v = __dadd_rn(v, __ldcg(partials + c));
+  const double s = block_sum(v, red);
+  if (threadIdx.x == 0) red[0] = s;
+  __syncthreads();
+  const double all = red[0];
+  __syncthreads();
+  return nk ? __fdiv_rn(__double2float_rn(all), float(nk)) : 0.0f;  // codec.cpp:82-83
+}
+
+__device__ __forceinline__ float sign_value(float y, float s) {  // D(Q(y)) for onebit
+  return (__float_as_uint(y) >> 31) ? -s : s;
+}
+
+template <bool EC>
+__global__ void __launch_bounds__(kThr) onebit_central_kernel(OnebitArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[kWarps];
+  __shared__ float sc[kMaxRanks];
+  __shared__ int bad_s;
+  const int lane = threadIdx.x & 31;
+  const size_t warp = (size_t(blockIdx.x) * kThr + threadIdx.x) >> 5;
+  const size_t nwarps = (size_t(gridDim.x) * kThr) >> 5;
+  const int g = a.g, me = a.me;
+  WinHdr* myhdr = reinterpret_cast<WinHdr*>(a.win[me]);
+  if (threadIdx.x == 0) bad_s = 0;
+  int bad = 0;
+
+  // ---- phase 1: signs of y = x - delta to the owners, fp64 sum |y| per chunk
+  for (int i = 0; i < g; ++i) {
+    const int k = (me + 1 + i) % g;  // peers first, my own chunk last
+    size_t lo, nk;
+    chunk_range(a.n, g, k, lo, nk);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(a.win[k] + a.off_recv1 + size_t(me) * a.slot_stride + 16);
+    const float* xk = a.x + lo;
+    const float* dk = EC ? a.delta + lo : nullptr;
+    double acc = 0.0;
+    for (size_t t = warp; t * kTile < nk; t += nwarps) {
+      const size_t base = t * kTile;
+      float y[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const size_t e = base + 32 * r + lane;
+        float v = 0.0f;
+        if (e < nk) {
+          v = __ldcs(xk + e);
+          if (EC) v = __fsub_rn(v, __ldcs(dk + e));  // codec.cpp:131
+        }
+        y[r] = v;
+      }
+      uint32_t word = 0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const bool in = base + 32 * r + lane < nk;
+        const uint32_t b = __ballot_sync(0xffffffffu, in && !(__float_as_uint(y[r]) >> 31));
+        if (lane == r) word = b;
+        acc = __dadd_rn(acc, fabs(double(y[r])));  // out-of-range lanes hold +0
+        bad |= !finite_f(y[r]);
+      }
+      dst[t * 32 + lane] = word;
+    }
+    const double s = block_sum(acc, red);
+    if (threadIdx.x == 0) a.partials[size_t(k) * gridDim.x + blockIdx.x] = s;
+  }
+  // my NVLink stores precede CTA 0's release below (cumulativity through the barrier)
+  __syncthreads();
+  if (threadIdx.x == 0) fence_acq_rel_sys();
+  grid.sync();
+  for (int k = 0; k < g; ++k) {
+    size_t lo, nk;
+    chunk_range(a.n, g, k, lo, nk);
+    const float s = scale_of(a.partials + size_t(k) * gridDim.x, nk, red);
+    if (threadIdx.x == 0) sc[k] = s;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    if (threadIdx.x < g) {
+      const int k = threadIdx.x;
+      *reinterpret_cast<float*>(a.win[k] + a.off_recv1 + size_t(me) * a.slot_stride) = sc[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_acq_rel_sys();
+      for (int k = 0; k < g; ++k) red_relaxed_sys_add(&reinterpret_cast<WinHdr*>(a.win[k])->arrive1, 1ull);
+    }
+  }
+  if (EC) {  // delta = y - D(Q(y)), local (codec.cpp:135)
+    for (int k = 0; k < g; ++k) {
+      size_t lo, nk;
+      chunk_range(a.n, g, k, lo, nk);
+      const float s = sc[k];
+      for (size_t e = size_t(blockIdx.x) * kThr + threadIdx.x; e < nk; e += size_t(gridDim.x) * kThr) {
+        const float y = __fsub_rn(__ldcs(a.x + lo + e), a.delta[lo + e]);
+        a.delta[lo + e] = __fsub_rn(y, sign_value(y, s));
+      }
+    }
+  }
+
+  // ---- phase 2 (owner of chunk me): fold, second compression
+  size_t mlo, mn;
+  chunk_range(a.n, g, me, mlo, mn);
+  if (threadIdx.x == 0) wait_geq(&myhdr->arrive1, a.epoch * unsigned(g), a.timeout_ns, a.status);
+  __syncthreads();
+  float s_in[kMaxRanks];
+  const uint32_t* src[kMaxRanks];
+#pragma unroll
+  for (int j = 0; j < kMaxRanks; ++j) {
+    if (j < g) {
+      const uint8_t* slot = a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride;
+      s_in[j] = __ldcg(reinterpret_cast<const float*>(slot));
+      src[j] = reinterpret_cast<const uint32_t*>(slot + 16);
+    }
+  }
+  uint32_t* out2 = reinterpret_cast<uint32_t*>(a.win[me] + a.off_out2 + 16);
+  {
+    double acc2 = 0.0;
+    for (size_t t = warp; t * kTile < mn; t += nwarps) {
+      const size_t base = t * kTile;
+      uint32_t w[kMaxRanks];
+#pragma unroll
+      for (int j = 0; j < kMaxRanks; ++j) w[j] = j < g ? __ldcg(src[j] + t * 32 + lane) : 0u;
+      uint32_t word = 0;
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r) {
+        const size_t e = base + 32 * r + lane;
+        const bool in = e < mn;
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < kMaxRanks; ++j) {
+          if (j < g) {
+            const uint32_t bit = (__shfl_sync(0xffffffffu, w[j], r) >> lane) & 1u;
+            acc = __dadd_rn(acc, double(bit ? s_in[j] : -s_in[j]));  // kernels.cpp:14-16
+          }
+        }
+        float y2 = __double2float_rn(acc);  // collectives.cpp:140-142
+        if (EC && in) {
+          y2 = __fsub_rn(y2, a.eps[e]);  // compensate_encode with epsilon
+          a.eps[e] = y2;                 // stash y2 until scale2 is known
+        }
+        if (!in) y2 = 0.0f;
+        const uint32_t b = __ballot_sync(0xffffffffu, in && !(__float_as_uint(y2) >> 31));
+        if (lane == r) word = b;
+        acc2 = __dadd_rn(acc2, fabs(double(y2)));
+        bad |= !finite_f(y2);
+      }
+      out2[t * 32 + lane] = word;
+    }
+    const double s = block_sum(acc2, red);
+    if (threadIdx.x == 0) a.partials[size_t(g) * gridDim.x + blockIdx.x] = s;
+  }
+  if (bad) atomicOr(&bad_s, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (bad_s) latch(a.status, kStatusNonFinite);  // codec.cpp:24-27 (the reference throws)
+    fence_acq_rel_sys();
+  }
+  grid.sync();
+  const float s2 = scale_of(a.partials + size_t(g) * gridDim.x, mn, red);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __stcg(reinterpret_cast<float*>(a.win[me] + a.off_out2), s2);
+    fence_acq_rel_sys();
+    st_release_sys(&myhdr->ready2, a.epoch);  // publish (collectives.cpp:150-151)
+  }
+  if (EC) {  // epsilon = y2 - D(Q(y2))
+    for (size_t e = size_t(blockIdx.x) * kThr + threadIdx.x; e < mn; e += size_t(gridDim.x) * kThr) {
+      const float y2 = __ldcg(a.eps + e);  // stashed by another CTA: read through L2
+      a.eps[e] = __fsub_rn(y2, sign_value(y2, s2));
+    }
+  }
+
+  // ---- phase 3: decode every owner's second payload into x
+  for (int i = 0; i < g; ++i) {
+    const int k = (me + i) % g;  // my own (local) first
+    size_t lo, nk;
+    chunk_range(a.n, g, k, lo, nk);
+    if (threadIdx.x == 0) wait_geq(&reinterpret_cast<WinHdr*>(a.win[k])->ready2, a.epoch, a.timeout_ns, a.status);
+    __syncthreads();
+    const float s = __ldcg(reinterpret_cast<const float*>(a.win[k] + a.off_out2));
+    const uint32_t* bits = reinterpret_cast<const uint32_t*>(a.win[k] + a.off_out2 + 16);
+    float* xk = a.x + lo;
+    for (size_t t = warp; t * kTile < nk; t += nwarps) {
+      const size_t base = t * kTile;
+      const uint32_t w = __ldcg(bits + t * 32 + lane);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const size_t e = base + 32 * r + lane;
+        const uint32_t bit = (__shfl_sync(0xffffffffu, w, r) >> lane) & 1u;
+        if (e < nk) __stcs(xk + e, bit ? s : -s);  // kernels.cpp:65-69
+      }
+    }
+  }
+}
+
+}  // namespace
+
+int launch_onebit_central(const OnebitArgs& a, bool ec, cudaStream_t s) {
+  const void* fn = ec ? reinterpret_cast<const void*>(onebit_central_kernel<true>)
+                      : reinterpret_cast<const void*>(onebit_central_kernel<false>);
+  const int grid = persistent_grid(fn, kThr);
+  OnebitArgs args = a;
+  void* params[] = {&args};
+  B2_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThr), params, 0, s));
+  return B2_OK;
+}
+
+// bytes of one onebit window slot for chunks of at most maxchunk elements
+size_t onebit_slot_bytes(size_t maxchunk) {
+  const size_t words = (maxchunk + kTile - 1) / kTile * 32;
+  return (16 + 4 * words + 255) / 256 * 256;
+}
+
+}  // namespace b2

@@ -96,9 +96,9 @@ std::vector<float> to_host(std::span<const float> x) {
   return h;
 }
 
-void check_codec(const Codec& c, std::mt19937* rng) {
-  if (c.kind == CodecKind::onebit)
-    throw Error(B2_ERR_UNSUPPORTED, "onebit codec is not implemented on the B200 path");
+void check_codec(const Codec& c, std::mt19937* rng, bool onebit_ok = true) {
+  if (c.kind == CodecKind::onebit && !onebit_ok)
+    throw Error(B2_ERR_UNSUPPORTED, "onebit codec is implemented for c_lp_s only on the B200 path");
   if (c.kind == CodecKind::uniform8 && c.rounding == Rounding::stochastic) {
     if (!rng) throw Error(B2_ERR_INVALID, "uniform8 stochastic rounding needs a generator");  // codec.cpp:70
     throw Error(B2_ERR_UNSUPPORTED, "uniform8 stochastic rounding is not implemented on the B200 path");
@@ -119,6 +119,18 @@ Payload Codec::encode(std::span<const float> x, std::mt19937* rng) const {
     if (n) std::memcpy(p.data(), h.data(), 4 * n);
     return p;
   }
+  if (kind == CodecKind::onebit) {  // codec.cpp:81-88
+    const std::size_t ps = payload_size(n);
+    DevBuf xs((n ? n : 1) * 4), wire((ps + 15) / 16 * 16);
+    if (n) cuda_check(cudaMemcpy(xs.p, x.data(), 4 * n, cudaMemcpyDefault), "stage in");
+    check(b2_onebit_encode(xs.as<float>(), n, wire.as<std::uint8_t>(), nullptr));
+    Payload p(ps);
+    cuda_check(cudaMemcpy(p.data(), wire.p, ps, cudaMemcpyDeviceToHost), "copy payload");
+    float scale;
+    std::memcpy(&scale, p.data(), 4);
+    if (std::isnan(scale)) throw Error(B2_ERR_NONFINITE, "encode: non-finite input value");  // the kernel's mark
+    return p;
+  }
   DevBuf xs((n ? n : 1) * 4), codes(n + 64), hdr(B2_U8_HDR_BYTES), wire(8 + n);
   if (n) cuda_check(cudaMemcpy(xs.p, x.data(), 4 * n, cudaMemcpyDefault), "stage in");
   check(b2_u8_encode(xs.as<float>(), n, codes.as<std::uint8_t>(), hdr.as<float>(), nullptr));
@@ -134,9 +146,15 @@ Payload Codec::encode(std::span<const float> x, std::mt19937* rng) const {
 
 void Codec::decode(std::span<const std::uint8_t> payload, std::span<float> out) const {
   const std::size_t n = out.size();
-  if (kind == CodecKind::onebit) throw Error(B2_ERR_UNSUPPORTED, "onebit codec is not implemented on the B200 path");
   if (payload.size() != payload_size(n)) throw Error(B2_ERR_INVALID, "decode: malformed payload (length mismatch)");
   if (n == 0) return;
+  if (kind == CodecKind::onebit) {  // codec.cpp:110-114
+    DevBuf wire((payload.size() + 15) / 16 * 16), res(4 * n);
+    cuda_check(cudaMemcpy(wire.p, payload.data(), payload.size(), cudaMemcpyDefault), "stage payload");
+    check(b2_onebit_decode(wire.as<std::uint8_t>(), n, res.as<float>(), nullptr));
+    cuda_check(cudaMemcpy(out.data(), res.p, 4 * n, cudaMemcpyDefault), "copy out");
+    return;
+  }
   if (kind == CodecKind::identity) {
     cuda_check(cudaMemcpy(out.data(), payload.data(), 4 * n, cudaMemcpyDefault), "decode copy");
     return;
@@ -159,6 +177,16 @@ Payload compensate_encode(const Codec& codec, std::span<const float> x, std::spa
   check_codec(codec, rng);
   const std::size_t n = x.size();
   if (delta.size() != n) throw Error(B2_ERR_INVALID, "compensate_encode: length mismatch");  // codec.cpp:129
+  if (codec.kind == CodecKind::onebit) {  // y = x - delta, P = Q(y), delta = y - D(P) (codec.cpp:130-136)
+    std::vector<float> y = to_host(x), d = to_host(delta);
+    for (std::size_t k = 0; k < n; ++k) y[k] -= d[k];
+    Payload p = codec.encode(y);
+    std::vector<float> dec = codec.decode(p, n);
+    for (std::size_t k = 0; k < n; ++k) d[k] = y[k] - dec[k];
+    if (n) cuda_check(cudaMemcpy(delta.data(), d.data(), 4 * n, cudaMemcpyDefault), "delta out");
+    if (decoded) *decoded = std::move(dec);
+    return p;
+  }
   if (codec.kind == CodecKind::identity) {
     std::vector<float> h = to_host(x), d = to_host(delta);
     for (std::size_t k = 0; k < n; ++k) h[k] -= d[k];
@@ -367,7 +395,7 @@ double d_fp_s(B200Endpoint& ep, double now, std::span<float> x, const Topology& 
 
 double d_lp_s(B200Endpoint& ep, double now, std::span<float> x, const Topology& topo, std::uint64_t round,
               const Codec& codec, ReduceMode mode, std::mt19937* rng, std::uint32_t bucket) {
-  check_codec(codec, rng);
+  check_codec(codec, rng, /*onebit_ok=*/false);
   const auto nb = nbrs_of(ep, topo, round);
   DeviceScope ds(ep.device());
   auto s = static_cast<cudaStream_t>(ep.stream());

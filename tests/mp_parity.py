@@ -33,6 +33,7 @@ from oracle import Oracle  # noqa: E402  (test infrastructure: the checker)
 
 U8 = b2.Codec(b2.CodecKind.uniform8)
 ID = b2.Codec(b2.CodecKind.identity)
+OB = b2.Codec(b2.CodecKind.onebit)
 
 
 def bits(a):
@@ -53,6 +54,22 @@ class Checker:
             self.fail.append(f"rank{self.rank} {name}: {bad.size} mismatches, first at {bad[:5].tolist()} "
                              f"got {np.asarray(got).ravel()[bad[:3]].tolist()} "
                              f"want {np.asarray(want).ravel()[bad[:3]].tolist()}")
+
+    def close(self, name, got, want, ulps=4):
+        """Onebit scales come from fp64 |y| sums whose order differs from the
+        reference's (codec.cpp:82-83); inexact sums may round one float apart.
+        Bound: ulps x spacing(max |want|).  Exact matches are counted."""
+        got, want = np.asarray(got, np.float32), np.asarray(want, np.float32)
+        if np.array_equal(bits(got), bits(want)):
+            self.passed += 1
+            self.exact = getattr(self, "exact", 0) + 1
+            return
+        tol = ulps * float(np.spacing(np.float32(np.abs(want).max(initial=1.0))))
+        err = float(np.abs(got.astype(np.float64) - want).max(initial=0.0))
+        if err <= tol:
+            self.passed += 1
+        else:
+            self.fail.append(f"rank{self.rank} {name}: max err {err} > {tol}")
 
 
 def run(args):
@@ -127,6 +144,45 @@ def run(args):
             ck.eq(f"c_lp_s+EC n={n} round={t_} x", t.cpu().numpy(), want[rank])
             ck.eq(f"c_lp_s+EC n={n} round={t_} delta", es.delta.cpu().numpy(), deltas[rank])
             ck.eq(f"c_lp_s+EC n={n} round={t_} eps", es.epsilon.cpu().numpy(), eps[rank])
+
+    # ---- C_LP_S onebit (the 1-bit Adam aggregation, algorithms.cpp:141-148)
+    ob_sizes = [1, 3, 5, 37, 1000, 4097, 65536 + 7, 1_000_003] + ([] if args.quick else [4_000_000])
+    for n in ob_sizes:
+        bucket += 1
+        for it in range(2):
+            xs_it = [orc.synth(n, 9100 + 31 * it + r) for r in range(g)]
+            want = [x.copy() for x in xs_it]
+            orc.c_lp_s(want, codec=2)
+            t = torch.as_tensor(xs_it[rank]).cuda()
+            b2.c_lp_s(ep, 0.0, t, OB, None, bucket=bucket)
+            ck.close(f"c_lp_s onebit n={n} it={it}", t.cpu().numpy(), want[rank])
+    for n, rounds in ((37, 20), (100_003, 5)):
+        bucket += 1
+        own = b2.owned_partition_len(n, g, rank)
+        es = b2.ErrorState(n, own)
+        deltas = [np.zeros(n, np.float32) for _ in range(g)]
+        eps = [np.zeros(b2.owned_partition_len(n, g, r), np.float32) for r in range(g)]
+        for t_ in range(rounds):
+            grads = [orc.synth(n, 9500 + 1000 * r + t_) for r in range(g)]
+            want = [x.copy() for x in grads]
+            orc.c_lp_s(want, codec=2, deltas=deltas, eps=eps)
+            t = torch.as_tensor(grads[rank]).cuda()
+            b2.c_lp_s(ep, 0.0, t, OB, es, bucket=bucket, blocking=False)
+            ck.close(f"c_lp_s onebit+EC n={n} round={t_} x", t.cpu().numpy(), want[rank])
+            ck.close(f"c_lp_s onebit+EC n={n} round={t_} delta", es.delta.cpu().numpy(), deltas[rank])
+            ck.close(f"c_lp_s onebit+EC n={n} round={t_} eps", es.epsilon.cpu().numpy(), eps[rank])
+    # back-to-back non-blocking onebit calls on one bucket, one sync at the end
+    bucket += 1
+    n = 200_003
+    ts = [torch.as_tensor(orc.synth(n, 60 + r)).cuda() for r in range(2)]
+    for i in range(6):
+        b2.c_lp_s(ep, 0.0, ts[i % 2], OB, None, bucket=bucket, blocking=False)
+    ep.sync()
+    for r in range(2):  # each buffer went through 3 calls; every rank starts from the same x
+        w = [orc.synth(n, 60 + r) for _ in range(g)]
+        for _ in range(3):
+            orc.c_lp_s(w, codec=2)
+        ck.close(f"c_lp_s onebit back-to-back buf{r}", ts[r].cpu().numpy(), w[rank])
 
     # ---- interleaved buckets, non-blocking issue, one sync (overlap of buckets)
     bucket += 1
@@ -248,6 +304,22 @@ def run(args):
                 ck.fail.append(f"rank{rank} c_lp_s n={n}: replicas differ {allv}")
             else:
                 ck.passed += 1
+            # the same bucket through C_LP_S onebit: own partition vs the restatement, replicas identical
+            b2.lib.b2_fill_synthetic(t.data_ptr(), n, 2026 + rank, 0, torch.cuda.current_stream().cuda_stream)
+            b2.c_lp_s(ep, 0.0, t, OB, None, bucket=bucket + 1)
+            acc = np.zeros(sz, np.float64)
+            for p in parts:
+                acc += orc.onebit_decode_wire(orc.onebit_encode_wire(p), sz).astype(np.float64)
+            s = acc.astype(np.float32)
+            ck.close(f"c_lp_s onebit n={n} own partition", t[lo:lo + sz].cpu().numpy(),
+                     orc.onebit_decode_wire(orc.onebit_encode_wire(s), sz))
+            digest = hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest()
+            allv = [None] * g
+            dist.all_gather_object(allv, digest)
+            if len(set(allv)) != 1:
+                ck.fail.append(f"rank{rank} c_lp_s onebit n={n}: replicas differ {allv}")
+            else:
+                ck.passed += 1
 
     return ck, ep.launches()
 
@@ -261,18 +333,19 @@ def main():
     t0 = time.time()
     try:
         ck, launches = run(args)
-        fails, passed = ck.fail, ck.passed
+        fails, passed, exact = ck.fail, ck.passed, getattr(ck, "exact", 0)
     except Exception:
-        fails, passed, launches = [f"rank{dist.get_rank()} exception: {traceback.format_exc()}"], 0, 0
+        fails, passed, launches, exact = [f"rank{dist.get_rank()} exception: {traceback.format_exc()}"], 0, 0, 0
     allres = [None] * dist.get_world_size()
-    dist.all_gather_object(allres, (passed, fails, launches))
+    dist.all_gather_object(allres, (passed, fails, launches, exact))
     if dist.get_rank() == 0:
-        total_pass = sum(p for p, _, _ in allres)
-        all_fail = [f for _, fs, _ in allres for f in fs]
+        total_pass = sum(p for p, _, _, _ in allres)
+        all_fail = [f for _, fs, _, _ in allres for f in fs]
         print(json.dumps({"world": dist.get_world_size(), "passed": total_pass, "failed": len(all_fail),
-                          "launches": [l for _, _, l in allres], "seconds": round(time.time() - t0, 1),
+                          "onebit_bit_exact": sum(e for _, _, _, e in allres),
+                          "launches": [l for _, _, l, _ in allres], "seconds": round(time.time() - t0, 1),
                           "failures": all_fail[:40]}))
-    ok = all(not fs for _, fs, _ in allres)
+    ok = all(not fs for _, fs, _, _ in allres)
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)

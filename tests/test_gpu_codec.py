@@ -89,8 +89,9 @@ def test_stochastic_and_onebit_collective_are_rejected():
     with pytest.raises(b2.Error):
         b2.Codec(b2.CodecKind.uniform8, b2.Rounding.stochastic).encode(dev([1.0, 2.0]))
     ep = b2.B200Endpoint(0, 1, 0)
-    with pytest.raises(b2.Error):  # C_LP_S with onebit: not on the B200 path yet
-        b2.c_lp_s(ep, 0.0, dev([1.0, 2.0]), b2.Codec(b2.CodecKind.onebit), None)
+    with pytest.raises(b2.Error):  # D_LP_S with onebit: not on the B200 path
+        b2.d_lp_s(ep, 0.0, dev([1.0, 2.0]), b2.Topology(b2.TopologyKind.ring, 1, 0), 0,
+                  b2.Codec(b2.CodecKind.onebit), b2.ReduceMode.average)
     ep.close()
 
 

@@ -175,3 +175,52 @@ def test_c_lp_s_g1_edge_inputs(ep, oracle, case):
     else:
         b2.c_lp_s(ep, 0.0, t, U8, None, bucket=20)
         assert np.array_equal(bits(t.cpu().numpy()), bits(want))
+
+
+# ---------------------------------------------------------- C_LP_S onebit
+OB = b2.Codec(b2.CodecKind.onebit)
+
+
+def test_c_lp_s_onebit_reference_kat(ep):
+    # test_collectives.cpp:209-225: single-worker sign compression with EC
+    t = torch.tensor([0.3, -0.1], dtype=torch.float32).cuda()
+    es = b2.ErrorState(2, 2)
+    b2.c_lp_s(ep, 0.0, t, OB, es, bucket=40)
+    x, d, e = t.cpu().numpy(), es.delta.cpu().numpy(), es.epsilon.cpu().numpy()
+    assert x[0] == pytest.approx(0.2) and x[1] == pytest.approx(-0.2)
+    assert d[0] == pytest.approx(0.1, rel=1e-6) and d[1] == pytest.approx(0.1, rel=1e-6)
+    assert e[0] == pytest.approx(0.0) and e[1] == pytest.approx(0.0)
+
+
+@pytest.mark.parametrize("n", [1, 5, 37, 1023, 1025, 4096, 1_000_003, 4_000_000])
+def test_c_lp_s_onebit_g1(ep, oracle, n):
+    # splitmix grid inputs: every fp64 |x| sum is exact, so bit-exact
+    x = oracle.synth(n, 3030 + n)
+    want = x.copy()
+    oracle.c_lp_s([want], codec=2)
+    t = torch.as_tensor(x).cuda()
+    b2.c_lp_s(ep, 0.0, t, OB, None, bucket=41)
+    assert np.array_equal(bits(t.cpu().numpy()), bits(want))
+
+
+def test_c_lp_s_onebit_g1_ec_rounds(ep, oracle):
+    # y = x - delta makes the |y| sums inexact: scales within a float
+    # rounding of the oracle's (sequential fp64, as the reference's scalar path)
+    n = 100_003
+    es = b2.ErrorState(n, n)
+    d_or, e_or = [np.zeros(n, np.float32)], [np.zeros(n, np.float32)]
+    for r in range(6):
+        g = oracle.synth(n, 400 + r)
+        w = g.copy()
+        oracle.c_lp_s([w], codec=2, deltas=d_or, eps=e_or)
+        t = torch.as_tensor(g).cuda()
+        b2.c_lp_s(ep, 0.0, t, OB, es, bucket=42)
+        for got, want in ((t, w), (es.delta, d_or[0]), (es.epsilon, e_or[0])):
+            tol = 4 * np.spacing(np.float32(np.abs(want).max()))
+            assert np.abs(got.cpu().numpy() - want).max() <= tol
+
+
+def test_c_lp_s_onebit_nonfinite_raises(ep):
+    t = torch.tensor([1.0, float("inf"), 2.0], dtype=torch.float32).cuda()
+    with pytest.raises(b2.Error):
+        b2.c_lp_s(ep, 0.0, t, OB, None, bucket=43)

@@ -97,3 +97,37 @@ def test_onebit_reference_kats(oracle):
         [2.0, -2.0, 2.0]
     assert list(oracle.onebit_decode_wire(oracle.onebit_encode_wire(np.array([-1, -3], np.float32)), 2)) == \
         [-2.0, -2.0]
+
+
+@pytest.mark.parametrize("g", [1, 2, 3, 8])
+@pytest.mark.parametrize("n", [5, 37, 100_003])
+def test_onebit_c_lp_s_matches_reference(oracle, ref, g, n):
+    # c_lp_s with Codec{onebit} (the 1-bit Adam aggregation, algorithms.cpp:
+    # 141-148).  Without EC on splitmix grid inputs every fp64 |x| sum is
+    # exact, so the restatement must be bitwise equal to the reference.
+    xs = [ref.synth(n, 4040 + r) for r in range(g)]
+    a = [x.copy() for x in xs]
+    b = [x.copy() for x in xs]
+    oracle.c_lp_s(a, codec=2)
+    ref.c_lp_s(b, codec=2)
+    assert all(np.array_equal(bits(p), bits(q)) for p, q in zip(a, b))
+
+
+def test_onebit_ec_rounds_match_reference(oracle, ref):
+    # with error feedback the |y| sums stop being exact (y = x - delta), so
+    # the scales agree within a float rounding: values within 4 ulp of the
+    # reference's scale magnitude, residual state likewise
+    g, n = 3, 1001
+    da = [np.zeros(n, np.float32) for _ in range(g)]
+    db = [np.zeros(n, np.float32) for _ in range(g)]
+    ea = [np.zeros(oracle.partition_range(n, g, r)[1], np.float32) for r in range(g)]
+    eb = [e.copy() for e in ea]
+    for t in range(5):
+        xs = [ref.synth(n, 700 + 10 * t + r) for r in range(g)]
+        a = [x.copy() for x in xs]
+        b = [x.copy() for x in xs]
+        oracle.c_lp_s(a, codec=2, deltas=da, eps=ea)
+        ref.c_lp_s(b, codec=2, deltas=db, eps=eb)
+        for p, q in zip(a + da + ea, b + db + eb):
+            tol = 4 * np.spacing(np.float32(np.abs(q).max() if q.size else 1.0))
+            assert np.abs(p - q).max(initial=0) <= tol
