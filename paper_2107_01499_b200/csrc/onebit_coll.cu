@@ -74,20 +74,39 @@ __device__ __forceinline__ float scale_of(const double* partials, size_t nk, dou
   return nk ? __fdiv_rn(__double2float_rn(all), float(nk)) : 0.0f;  // codec.cpp:82-83
 }
 
+// 32x32 bit transpose across a warp: lane i holds row word i on entry and
+// column i on exit (bit r of the result = bit i of lane r's word).  Block
+// swap at 16, then recursively within the 16x16, 8x8, ... blocks.
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const int sft = 16 >> i;
+    const uint32_t m = masks[i];
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, sft);
+    x = (lane & sft) ? (x & ~m) | ((y & ~m) >> sft) : (x & m) | ((y & m) << sft);
+  }
+  return x;
+}
+
 __device__ __forceinline__ float sign_value(float y, float s) {  // D(Q(y)) for onebit
   return (__float_as_uint(y) >> 31) ? -s : s;
 }
 
-template <bool EC>
+// G = the number of ranks (compile time: the fold's bit gathering unrolls).
+template <int G, bool EC>
 __global__ void __launch_bounds__(kThr) onebit_central_kernel(OnebitArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[kWarps];
   __shared__ float sc[kMaxRanks];
+  __shared__ float fold_tab[1 << kMaxRanks];
+  __shared__ float s_in[kMaxRanks];
   __shared__ int bad_s;
   const int lane = threadIdx.x & 31;
   const size_t warp = (size_t(blockIdx.x) * kThr + threadIdx.x) >> 5;
   const size_t nwarps = (size_t(gridDim.x) * kThr) >> 5;
-  const int g = a.g, me = a.me;
+  constexpr int g = G;
+  const int me = a.me;
   WinHdr* myhdr = reinterpret_cast<WinHdr*>(a.win[me]);
   if (threadIdx.x == 0) bad_s = 0;
   int bad = 0;
@@ -103,28 +122,34 @@ __global__ void __launch_bounds__(kThr) onebit_central_kernel(OnebitArgs a) {
     double acc = 0.0;
     for (size_t t = warp; t * kTile < nk; t += nwarps) {
       const size_t base = t * kTile;
+      const bool full = base + kTile <= nk;
       float y[32];
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
         const size_t e = base + 32 * r + lane;
         float v = 0.0f;
-        if (e < nk) {
+        if (full || e < nk) {
           v = __ldcs(xk + e);
           if (EC) v = __fsub_rn(v, __ldcs(dk + e));  // codec.cpp:131
         }
-        y[r] = v;
+        y[r] = v;  // out-of-range lanes hold +0: no bit, no |y|
       }
       uint32_t word = 0;
+      double acc_odd = 0.0;
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
-        const bool in = base + 32 * r + lane < nk;
+        const bool in = full || base + 32 * r + lane < nk;
         const uint32_t b = __ballot_sync(0xffffffffu, in && !(__float_as_uint(y[r]) >> 31));
         if (lane == r) word = b;
-        acc = __dadd_rn(acc, fabs(double(y[r])));  // out-of-range lanes hold +0
-        bad |= !finite_f(y[r]);
+        if (r & 1)
+          acc_odd = __dadd_rn(acc_odd, fabs(double(y[r])));
+        else
+          acc = __dadd_rn(acc, fabs(double(y[r])));
       }
+      acc = __dadd_rn(acc, acc_odd);  // a non-finite y makes the chunk's sum non-finite
       dst[t * 32 + lane] = word;
     }
+    bad |= !isfinite(acc);  // finite |y| cannot overflow an fp64 sum
     const double s = block_sum(acc, red);
     if (threadIdx.x == 0) a.partials[size_t(k) * gridDim.x + blockIdx.x] = s;
   }
@@ -167,38 +192,73 @@ __global__ void __launch_bounds__(kThr) onebit_central_kernel(OnebitArgs a) {
   chunk_range(a.n, g, me, mlo, mn);
   if (threadIdx.x == 0) wait_geq(&myhdr->arrive1, a.epoch * unsigned(g), a.timeout_ns, a.status);
   __syncthreads();
-  float s_in[kMaxRanks];
-  const uint32_t* src[kMaxRanks];
+  const uint32_t* src[G];
 #pragma unroll
-  for (int j = 0; j < kMaxRanks; ++j) {
-    if (j < g) {
-      const uint8_t* slot = a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride;
-      s_in[j] = __ldcg(reinterpret_cast<const float*>(slot));
-      src[j] = reinterpret_cast<const uint32_t*>(slot + 16);
-    }
+  for (int j = 0; j < G; ++j)
+    src[j] = reinterpret_cast<const uint32_t*>(a.win[me] + a.off_recv1 + size_t(j) * a.slot_stride + 16);
+  if (threadIdx.x < g)
+    s_in[threadIdx.x] = __ldcg(reinterpret_cast<const float*>(a.win[me] + a.off_recv1 + size_t(threadIdx.x) * a.slot_stride));
+  __syncthreads();
+  // D(P_j) is +-s_j, so (float)(sum_j ascending in fp64) depends only on the
+  // g sign bits: one table of 2^g values, each folded exactly as
+  // collectives.cpp:125-142 folds an element (kernels.cpp:14-16).
+  for (int idx = threadIdx.x; idx < (1 << g); idx += kThr) {
+    double acc = 0.0;
+    for (int j = 0; j < g; ++j) acc = __dadd_rn(acc, double(((idx >> j) & 1) ? s_in[j] : -s_in[j]));
+    fold_tab[idx] = __double2float_rn(acc);
   }
+  __syncthreads();
   uint32_t* out2 = reinterpret_cast<uint32_t*>(a.win[me] + a.off_out2 + 16);
-  {
+  if constexpr (!EC && G <= 4) {
+    // Without epsilon the second payload is a boolean function of the g sign
+    // words: every one of the 2^g sign patterns (minterms) is a word mask;
+    // its popcount counts the elements whose y2 is fold_tab[pattern], so
+    // sum |y2| = sum_pattern count * |fold_tab| (exact products in fp64).
+    uint32_t cnt[1 << G];
+#pragma unroll
+    for (int p = 0; p < (1 << G); ++p) cnt[p] = 0;
+    for (size_t t = warp; t * kTile < mn; t += nwarps) {
+      const size_t e0 = t * kTile + 32 * size_t(lane);  // this lane's word = elements [e0, e0 + 32)
+      const uint32_t valid = e0 + 32 <= mn ? 0xffffffffu : (e0 >= mn ? 0u : (1u << (mn - e0)) - 1u);
+      uint32_t w[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) w[j] = __ldcg(src[j] + t * 32 + lane);
+      uint32_t word = 0;
+#pragma unroll
+      for (int p = 0; p < (1 << G); ++p) {
+        uint32_t m = valid;
+#pragma unroll
+        for (int j = 0; j < G; ++j) m &= ((p >> j) & 1) ? w[j] : ~w[j];
+        cnt[p] += __popc(m);
+        if (!(__float_as_uint(fold_tab[p]) >> 31)) word |= m;  // sign_pack of y2
+      }
+      out2[t * 32 + lane] = word;
+    }
+    double acc2 = 0.0;
+#pragma unroll
+    for (int p = 0; p < (1 << G); ++p) {
+      acc2 = __dadd_rn(acc2, double(cnt[p]) * fabs(double(fold_tab[p])));
+      bad |= cnt[p] && !finite_f(fold_tab[p]);
+    }
+    const double s = block_sum(acc2, red);
+    if (threadIdx.x == 0) a.partials[size_t(g) * gridDim.x + blockIdx.x] = s;
+  } else {
     double acc2 = 0.0;
     for (size_t t = warp; t * kTile < mn; t += nwarps) {
       const size_t base = t * kTile;
-      uint32_t w[kMaxRanks];
+      const bool full = base + kTile <= mn;
+      uint32_t col[G];  // lane l: bit r = rank j's sign of element 32r + l
 #pragma unroll
-      for (int j = 0; j < kMaxRanks; ++j) w[j] = j < g ? __ldcg(src[j] + t * 32 + lane) : 0u;
+      for (int j = 0; j < G; ++j) col[j] = transpose32(__ldcg(src[j] + t * 32 + lane), lane);
       uint32_t word = 0;
-#pragma unroll 4
+#pragma unroll
       for (int r = 0; r < 32; ++r) {
         const size_t e = base + 32 * r + lane;
-        const bool in = e < mn;
-        double acc = 0.0;
+        const bool in = full || e < mn;
+        uint32_t idx = 0;
 #pragma unroll
-        for (int j = 0; j < kMaxRanks; ++j) {
-          if (j < g) {
-            const uint32_t bit = (__shfl_sync(0xffffffffu, w[j], r) >> lane) & 1u;
-            acc = __dadd_rn(acc, double(bit ? s_in[j] : -s_in[j]));  // kernels.cpp:14-16
-          }
-        }
-        float y2 = __double2float_rn(acc);  // collectives.cpp:140-142
+        for (int j = 0; j < G; ++j) idx |= ((col[j] >> r) & 1u) << j;
+        float y2 = fold_tab[idx];
         if (EC && in) {
           y2 = __fsub_rn(y2, a.eps[e]);  // compensate_encode with epsilon
           a.eps[e] = y2;                 // stash y2 until scale2 is known
@@ -207,10 +267,10 @@ __global__ void __launch_bounds__(kThr) onebit_central_kernel(OnebitArgs a) {
         const uint32_t b = __ballot_sync(0xffffffffu, in && !(__float_as_uint(y2) >> 31));
         if (lane == r) word = b;
         acc2 = __dadd_rn(acc2, fabs(double(y2)));
-        bad |= !finite_f(y2);
       }
       out2[t * 32 + lane] = word;
     }
+    bad |= !isfinite(acc2);
     const double s = block_sum(acc2, red);
     if (threadIdx.x == 0) a.partials[size_t(g) * gridDim.x + blockIdx.x] = s;
   }
@@ -246,12 +306,12 @@ __global__ void __launch_bounds__(kThr) onebit_central_kernel(OnebitArgs a) {
     float* xk = a.x + lo;
     for (size_t t = warp; t * kTile < nk; t += nwarps) {
       const size_t base = t * kTile;
-      const uint32_t w = __ldcg(bits + t * 32 + lane);
+      const bool full = base + kTile <= nk;
+      const uint32_t col = transpose32(__ldcg(bits + t * 32 + lane), lane);
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
         const size_t e = base + 32 * r + lane;
-        const uint32_t bit = (__shfl_sync(0xffffffffu, w, r) >> lane) & 1u;
-        if (e < nk) __stcs(xk + e, bit ? s : -s);  // kernels.cpp:65-69
+        if (full || e < nk) __stcs(xk + e, ((col >> r) & 1u) ? s : -s);  // kernels.cpp:65-69
       }
     }
   }
@@ -259,9 +319,25 @@ __global__ void __launch_bounds__(kThr) onebit_central_kernel(OnebitArgs a) {
 
 }  // namespace
 
+template <int G>
+const void* onebit_fn(bool ec) {
+  return ec ? reinterpret_cast<const void*>(onebit_central_kernel<G, true>)
+            : reinterpret_cast<const void*>(onebit_central_kernel<G, false>);
+}
+
 int launch_onebit_central(const OnebitArgs& a, bool ec, cudaStream_t s) {
-  const void* fn = ec ? reinterpret_cast<const void*>(onebit_central_kernel<true>)
-                      : reinterpret_cast<const void*>(onebit_central_kernel<false>);
+  const void* fn = nullptr;
+  switch (a.g) {
+    case 1: fn = onebit_fn<1>(ec); break;
+    case 2: fn = onebit_fn<2>(ec); break;
+    case 3: fn = onebit_fn<3>(ec); break;
+    case 4: fn = onebit_fn<4>(ec); break;
+    case 5: fn = onebit_fn<5>(ec); break;
+    case 6: fn = onebit_fn<6>(ec); break;
+    case 7: fn = onebit_fn<7>(ec); break;
+    case 8: fn = onebit_fn<8>(ec); break;
+    default: set_error("onebit c_lp_s: %d ranks (1..%d supported)", a.g, kMaxRanks); return B2_ERR_INVALID;
+  }
   const int grid = persistent_grid(fn, kThr);
   OnebitArgs args = a;
   void* params[] = {&args};
