@@ -61,6 +61,7 @@ PRIMS = {  # name -> (default elements, reference time_primitive id, metric labe
     "codec": (4_000_000, 0, "MinMaxUInt8 compress+decompress"),
     "onebit": (4_000_000, 5, "Onebit compress+decompress"),
     "c_lp_s_onebit": (100_000_000, 6, "C_LP_S onebit allreduce"),
+    "d_lp_s_onebit": (25_000_000, 7, "D_LP_S onebit ring averaging"),
 }
 
 
@@ -84,6 +85,8 @@ def algorithmic_bytes(prim: str, n: int, g: int):
         return 4 * n + n + n * nb + 4 * n, n * (nb - 1)
     if prim == "c_lp_s_onebit":  # x 4N; bits N/8 out, N/8 folded, N/8g second bits, N/8 gathered; x' 4N
         return 8 * n + 3 * n // 8 + n // (8 * g), n * (g - 1) // (4 * g)
+    if prim == "d_lp_s_onebit":  # x 4N; my bits N/8; |N| neighbours' bits; x' 4N
+        return 8 * n + (nb + 1) * n // 8, (nb - 1) * n // 8
     if prim == "onebit":  # read x, write bits, read bits, write x
         return 8 * n + 2 * ((n + 7) // 8), 0
     return 10 * n, 0  # codec: read x, write codes, read codes, write x
@@ -191,7 +194,7 @@ def run_b200(args, rank: int, world: int):
     n = args.n
     prim = args.prim
     ep = b2.B200Endpoint(rank, world, dev)
-    codec = b2.Codec(b2.CodecKind.onebit if prim == "c_lp_s_onebit" else b2.CodecKind.uniform8)
+    codec = b2.Codec(b2.CodecKind.onebit if prim.endswith("_onebit") else b2.CodecKind.uniform8)
     stream = torch.cuda.current_stream()
     x = torch.empty(n, dtype=torch.float32, device="cuda")
     b2._lib.check(b2.lib.b2_fill_synthetic(x.data_ptr(), n, 2026 + rank, 0, stream.cuda_stream))
@@ -218,7 +221,7 @@ def run_b200(args, rank: int, world: int):
             b2.c_fp_s(ep, 0.0, buf, blocking=False)
         elif prim == "d_fp_s":
             b2.d_fp_s(ep, 0.0, buf, ring, 0, b2.ReduceMode.average, blocking=False)
-        elif prim == "d_lp_s":
+        elif prim in ("d_lp_s", "d_lp_s_onebit"):
             b2.d_lp_s(ep, 0.0, buf, ring, 0, codec, b2.ReduceMode.average, blocking=False)
         elif prim == "onebit":
             s_ = torch.cuda.current_stream().cuda_stream
@@ -346,7 +349,8 @@ def run_b200(args, rank: int, world: int):
     roof["algorithmic_bytes"] = {"hbm": hbm_b, "nvlink_ingress": nvl_b}
     roof["t_roof_us"] = round(max(t_roof_hbm, t_roof_nvl) * 1e6, 1)
     roof["kernel"] = {"c_lp_s": "central_kernel<uint8> (one fused launch per step)",
-                      "c_lp_s_onebit": "onebit_central_kernel<false> (one cooperative launch per step)",
+                      "c_lp_s_onebit": "onebit_central_kernel<g, false> (one cooperative launch per step)",
+                      "d_lp_s_onebit": "onebit_decent_kernel<|N|> (one cooperative launch per step)",
                       "c_fp_s": "central_kernel<identity> (one fused launch per step)",
                       "d_fp_s": "decent_kernel<identity> (one fused launch per step)",
                       "d_lp_s": "decent_kernel<uint8> (one fused launch per step)",

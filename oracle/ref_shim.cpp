@@ -264,7 +264,8 @@ void ref_synth(float* x, std::size_t n, std::uint64_t seed) { synth(x, n, seed);
 // allocations and first touch.  Inputs are regenerated (untimed) before each
 // repetition.  prim: 0 codec(encode+decode, g must be 1), 1 c_fp_s,
 // 2 c_lp_s (uint8, no EC), 3 d_fp_s ring, 4 d_lp_s ring (uint8),
-// 5 onebit codec (encode+decode, g must be 1), 6 c_lp_s (onebit, no EC).
+// 5 onebit codec (encode+decode, g must be 1), 6 c_lp_s (onebit, no EC),
+// 7 d_lp_s ring (onebit).
 int ref_time_primitive(int prim, int g, std::size_t len, int reps,
                        double* seconds) {
   return guarded([&] {
@@ -291,6 +292,7 @@ int ref_time_primitive(int prim, int g, std::size_t len, int reps,
             case 3: d_fp_s(ep, 0.0, x, ring, 0, ReduceMode::average); break;
             case 4: d_lp_s(ep, 0.0, x, ring, 0, u8, ReduceMode::average); break;
             case 6: c_lp_s(ep, 0.0, x, ob, nullptr); break;
+            case 7: d_lp_s(ep, 0.0, x, ring, 0, ob, ReduceMode::average); break;
             default: throw Error("unknown primitive");
           }
         });

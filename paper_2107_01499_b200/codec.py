@@ -63,9 +63,7 @@ class Codec:
     def payload_size(self, n: int) -> int:
         return int(lib.b2_payload_size(int(self.kind), n))
 
-    def _check_supported(self, rng, collective: bool = True, onebit_ok: bool = False) -> None:
-        if self.kind == CodecKind.onebit and collective and not onebit_ok:
-            raise _lib.B2Error(_lib.B2_ERR_UNSUPPORTED, "the onebit codec is implemented for c_lp_s only")
+    def _check_supported(self, rng) -> None:
         if self.kind == CodecKind.uniform8 and self.rounding == Rounding.stochastic:
             if rng is None:  # codec.cpp:70 wording
                 raise Error("uniform8 stochastic rounding needs a generator")
@@ -104,7 +102,7 @@ class Codec:
     def encode(self, x, rng=None):
         """Payload bytes.  Device input -> device uint8 tensor; host input ->
         numpy uint8 array (the reference's Payload)."""
-        self._check_supported(rng, collective=False)
+        self._check_supported(rng)
         xd, host = _as_device(x)
         xd = xd.reshape(-1)
         n = xd.numel()
@@ -176,7 +174,7 @@ class ErrorState:
 def compensate_encode(codec: Codec, x, delta, rng=None, decoded: list | None = None):
     """codec.hpp:49-54 / codec.cpp:125-137: encodes Q(x - delta) and replaces
     delta by the exact residual (x - delta) - D(Q(x - delta))."""
-    codec._check_supported(rng, collective=False)
+    codec._check_supported(rng)
     xd, host = _as_device(x)
     n = xd.numel()
     host_delta = not (isinstance(delta, torch.Tensor) and delta.is_cuda)

@@ -332,7 +332,7 @@ def c_lp_s(ep: B200Endpoint, now: float, x, codec: Codec, es: ErrorState | None,
     """Compressed ScatterReduce with two compression phases
     (collectives.hpp:54-61).  es != None applies error compensation.
     Codec{onebit} is the 1-bit Adam aggregation (algorithms.cpp:141-148)."""
-    codec._check_supported(rng, onebit_ok=True)
+    codec._check_supported(rng)
     b = _Bucket(ep, x)
     g, me = ep.world_size(), ep.rank()
     own = owned_partition_len(b.n, g, me)
@@ -383,7 +383,7 @@ def d_fp_s(ep: B200Endpoint, now: float, x, topo: Topology, round_: int, mode: R
 def d_lp_s(ep: B200Endpoint, now: float, x, topo: Topology, round_: int, codec: Codec, mode: ReduceMode,
            rng=None, bucket: int = 0, blocking: bool = True) -> float:
     """As d_fp_s, every contribution (self included) through Q
-    (collectives.hpp:68-72)."""
+    (collectives.hpp:68-72).  Any codec, onebit included."""
     codec._check_supported(rng)
     arr, m = _neighbors(ep, topo, round_)
     b = _Bucket(ep, x)

@@ -88,6 +88,27 @@ struct OnebitArgs {
   unsigned long long timeout_ns;
 };
 
+// D_LP_S with the onebit codec (onebit_coll.cu).  Pull design: every rank
+// encodes its bucket into its own window (dbuf[parity]) and publishes
+// dready[parity] = epoch; neighbours read it over NVLink and count their
+// reads in dreads[parity], which the owner waits on before it overwrites
+// that parity two calls later.
+struct OnebitDecentArgs {
+  float* x;
+  size_t n;
+  int me, nnb;
+  int nbrs[kMaxRanks];          // sorted, self-inclusive
+  int parity;
+  unsigned long long epoch;
+  unsigned long long expected_reads;  // dreads[parity] must reach this before we overwrite
+  double inv;                   // 1/|N| (average) or 1.0 (sum), collectives.cpp:282-284
+  uint8_t* win[kMaxRanks];
+  size_t off_dbuf;              // offset of dbuf[parity]
+  double* partials;             // local workspace [grid]
+  int* status;
+  unsigned long long timeout_ns;
+};
+
 // Decentralized neighbourhood reduce (D_FP_S, D_LP_S).
 struct DecentArgs {
   float* x;

@@ -30,6 +30,7 @@ int launch_central(const CentralArgs& a, int codec, bool ec, cudaStream_t s);
 int launch_decent(const DecentArgs& a, int codec, cudaStream_t s);
 int max_persistent_grid();
 int launch_onebit_central(const OnebitArgs& a, bool ec, cudaStream_t s);
+int launch_onebit_decent(const OnebitDecentArgs& a, cudaStream_t s);
 size_t onebit_slot_bytes(size_t maxchunk);
 }  // namespace b2
 
@@ -37,7 +38,7 @@ using namespace b2;
 
 namespace {
 
-enum Family { kCentral = 0, kDecentral = 1, kOnebit = 2 };
+enum Family { kCentral = 0, kDecentral = 1, kOnebit = 2, kOnebitD = 3 };
 
 struct Window {
   size_t bytes = 0;
@@ -135,6 +136,13 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
     off += size_t(g) * w->slot_stride;
     w->off_out2 = off;
     off += w->slot_stride;
+  } else if (family == kOnebitD) {
+    // my bucket's onebit payload, double-buffered by call parity
+    const size_t b = onebit_slot_bytes(n);
+    w->off_dbuf[0] = off;
+    off += b;
+    w->off_dbuf[1] = off;
+    off += b;
   } else {
     // arrival counters: for every source rank one per region of the bucket
     // (+ one for the unaligned tail), cumulative over the calls in which that
@@ -155,7 +163,7 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
     return rc;
   };
   if (cudaMalloc(&w->local, w->bytes) != cudaSuccess ||
-      cudaMemset(w->local, 0, family == kDecentral ? w->off_dbuf[0] : w->off_recv1) != cudaSuccess ||
+      cudaMemset(w->local, 0, (family == kDecentral || family == kOnebitD) ? w->off_dbuf[0] : w->off_recv1) != cudaSuccess ||
       cudaMalloc(&w->partials, sizeof(float2) * (kMaxRanks + 1) * max_persistent_grid()) !=
           cudaSuccess ||
       cudaMalloc(&w->cta_done, sizeof(unsigned) * (kMaxRanks + 4)) != cudaSuccess ||
@@ -524,6 +532,31 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard dg(c->device);
   Window* w = nullptr;
+  if (codec == B2_CODEC_ONEBIT) {  // d_lp_s with Codec{onebit}: pull design, onebit_coll.cu
+    rc = get_window(c, bucket, kOnebitD, n, 1, &w);
+    if (rc) return rc;
+    OnebitDecentArgs a{};
+    a.x = x;
+    a.n = n;
+    a.me = c->rank;
+    a.nnb = n_nbrs;
+    for (int i = 0; i < n_nbrs; ++i) a.nbrs[i] = nbrs[i];
+    a.epoch = ++w->epoch;
+    a.parity = static_cast<int>(a.epoch & 1);
+    a.expected_reads = w->exp_reads[a.parity];
+    a.inv = mode == B2_REDUCE_AVERAGE ? 1.0 / static_cast<double>(n_nbrs) : 1.0;
+    for (int j = 0; j < c->world; ++j) a.win[j] = w->peer[j];
+    a.off_dbuf = w->off_dbuf[a.parity];
+    a.partials = reinterpret_cast<double*>(w->partials);
+    a.status = c->status_d;
+    a.timeout_ns = c->timeout_ns;
+    rc = launch_onebit_decent(a, static_cast<cudaStream_t>(stream));
+    if (rc == B2_OK) {
+      w->exp_reads[a.parity] += static_cast<unsigned long long>(n_nbrs - 1);  // symmetric: my readers
+      ++c->launches;
+    }
+    return rc;
+  }
   rc = get_window(c, bucket, kDecentral, n, codec == B2_CODEC_UNIFORM8 ? 1 : 4, &w);
   if (rc) return rc;
   DecentArgs a{};
@@ -569,11 +602,8 @@ int b2_d_fp_s(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbrs, int 
 
 int b2_d_lp_s(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbrs, int codec, int mode,
               uint32_t bucket, void* stream) {
-  if (codec == B2_CODEC_ONEBIT) {
-    set_error("d_lp_s: onebit codec is not implemented on the B200 path");
-    return B2_ERR_UNSUPPORTED;
-  }
-  B2_REQUIRE(codec == B2_CODEC_UNIFORM8 || codec == B2_CODEC_IDENTITY, "unknown codec %d", codec);
+  B2_REQUIRE(codec == B2_CODEC_UNIFORM8 || codec == B2_CODEC_IDENTITY || codec == B2_CODEC_ONEBIT,
+             "unknown codec %d", codec);
   return decentral(c, x, n, nbrs, n_nbrs, codec, 1, mode, bucket, stream);
 }
 

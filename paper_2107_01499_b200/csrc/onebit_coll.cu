@@ -317,6 +317,109 @@ __global__ void __launch_bounds__(kThr) onebit_central_kernel(OnebitArgs a) {
   }
 }
 
+
+// ---------------------------------------------------------------- D_LP_S
+// d_lp_s with Codec{onebit} (collectives.cpp:260-288): one encode of the
+// whole bucket (one scale), x' = (float)((sum_{j in N, ascending} (double)
+// D(P_j)) * inv).  D(P_j) = +-s_j, so x' is a function of the |N| sign bits:
+// a 2^|N| table folded exactly as the reference folds one element.
+template <int NB>
+__global__ void __launch_bounds__(kThr) onebit_decent_kernel(OnebitDecentArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[kWarps];
+  __shared__ float tab[1 << NB];
+  __shared__ float s_nb[NB];
+  const int lane = threadIdx.x & 31;
+  const size_t warp = (size_t(blockIdx.x) * kThr + threadIdx.x) >> 5;
+  const size_t nwarps = (size_t(gridDim.x) * kThr) >> 5;
+  const size_t n = a.n;
+  const int p = a.parity;
+  WinHdr* myhdr = reinterpret_cast<WinHdr*>(a.win[a.me]);
+  uint8_t* mine = a.win[a.me] + a.off_dbuf;
+
+  // my dbuf[p] is free once the neighbours of two calls ago have read it
+  if (threadIdx.x == 0) wait_geq(&myhdr->dreads[p], a.expected_reads, a.timeout_ns, a.status);
+  __syncthreads();
+
+  // encode: sign words into my window, fp64 sum |x| (kernels.cpp:26-32, 58-63)
+  uint32_t* bits = reinterpret_cast<uint32_t*>(mine + 16);
+  double acc = 0.0;
+  for (size_t t = warp; t * kTile < n; t += nwarps) {
+    const size_t base = t * kTile;
+    const bool full = base + kTile <= n;
+    float y[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const size_t e = base + 32 * r + lane;
+      y[r] = (full || e < n) ? __ldcg(a.x + e) : 0.0f;
+    }
+    uint32_t word = 0;
+    double acc_odd = 0.0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const bool in = full || base + 32 * r + lane < n;
+      const uint32_t b = __ballot_sync(0xffffffffu, in && !(__float_as_uint(y[r]) >> 31));
+      if (lane == r) word = b;
+      if (r & 1)
+        acc_odd = __dadd_rn(acc_odd, fabs(double(y[r])));
+      else
+        acc = __dadd_rn(acc, fabs(double(y[r])));
+    }
+    acc = __dadd_rn(acc, acc_odd);
+    bits[t * 32 + lane] = word;
+  }
+  const bool bad = !isfinite(acc);  // finite |x| cannot overflow an fp64 sum
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) a.partials[blockIdx.x] = s;
+  if (__syncthreads_or(bad) && threadIdx.x == 0) latch(a.status, kStatusNonFinite);  // codec.cpp:24-27
+  if (threadIdx.x == 0) fence_acq_rel_sys();  // my sign words precede CTA 0's publication
+  grid.sync();
+  const float scale = scale_of(a.partials, n, red);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __stcg(reinterpret_cast<float*>(mine), scale);
+    fence_acq_rel_sys();
+    st_release_sys(&myhdr->dready[p], a.epoch);
+  }
+
+  // gather the neighbours' payloads (self included), fold by table
+  if (threadIdx.x < NB) {
+    const uint8_t* w = a.win[a.nbrs[threadIdx.x]] + a.off_dbuf;
+    wait_geq(&reinterpret_cast<const WinHdr*>(a.win[a.nbrs[threadIdx.x]])->dready[p], a.epoch, a.timeout_ns,
+             a.status);
+    s_nb[threadIdx.x] = __ldcg(reinterpret_cast<const float*>(w));
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < (1 << NB); idx += kThr) {
+    double f = 0.0;
+    for (int i = 0; i < NB; ++i) f = __dadd_rn(f, double(((idx >> i) & 1) ? s_nb[i] : -s_nb[i]));
+    tab[idx] = __double2float_rn(__dmul_rn(f, a.inv));  // collectives.cpp:282-286
+  }
+  __syncthreads();
+  const uint32_t* src[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) src[i] = reinterpret_cast<const uint32_t*>(a.win[a.nbrs[i]] + a.off_dbuf + 16);
+  for (size_t t = warp; t * kTile < n; t += nwarps) {
+    const size_t base = t * kTile;
+    const bool full = base + kTile <= n;
+    uint32_t col[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) col[i] = transpose32(__ldcg(src[i] + t * 32 + lane), lane);
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const size_t e = base + 32 * r + lane;
+      uint32_t idx = 0;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) idx |= ((col[i] >> r) & 1u) << i;
+      if (full || e < n) __stcs(a.x + e, tab[idx]);
+    }
+  }
+  // my reads of the neighbours' windows are done: one credit to each of them
+  __syncthreads();
+  if (threadIdx.x == 0) fence_acq_rel_sys();
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x < NB && a.nbrs[threadIdx.x] != a.me)
+    red_release_sys_add(&reinterpret_cast<WinHdr*>(a.win[a.nbrs[threadIdx.x]])->dreads[p], 1ull);
+}
 }  // namespace
 
 template <int G>
@@ -340,6 +443,26 @@ int launch_onebit_central(const OnebitArgs& a, bool ec, cudaStream_t s) {
   }
   const int grid = persistent_grid(fn, kThr);
   OnebitArgs args = a;
+  void* params[] = {&args};
+  B2_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThr), params, 0, s));
+  return B2_OK;
+}
+
+int launch_onebit_decent(const OnebitDecentArgs& a, cudaStream_t s) {
+  const void* fn = nullptr;
+  switch (a.nnb) {
+    case 1: fn = reinterpret_cast<const void*>(onebit_decent_kernel<1>); break;
+    case 2: fn = reinterpret_cast<const void*>(onebit_decent_kernel<2>); break;
+    case 3: fn = reinterpret_cast<const void*>(onebit_decent_kernel<3>); break;
+    case 4: fn = reinterpret_cast<const void*>(onebit_decent_kernel<4>); break;
+    case 5: fn = reinterpret_cast<const void*>(onebit_decent_kernel<5>); break;
+    case 6: fn = reinterpret_cast<const void*>(onebit_decent_kernel<6>); break;
+    case 7: fn = reinterpret_cast<const void*>(onebit_decent_kernel<7>); break;
+    case 8: fn = reinterpret_cast<const void*>(onebit_decent_kernel<8>); break;
+    default: set_error("onebit d_lp_s: %d neighbours (1..%d supported)", a.nnb, kMaxRanks); return B2_ERR_INVALID;
+  }
+  const int grid = persistent_grid(fn, kThr);
+  OnebitDecentArgs args = a;
   void* params[] = {&args};
   B2_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThr), params, 0, s));
   return B2_OK;

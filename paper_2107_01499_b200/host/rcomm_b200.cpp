@@ -96,9 +96,7 @@ std::vector<float> to_host(std::span<const float> x) {
   return h;
 }
 
-void check_codec(const Codec& c, std::mt19937* rng, bool onebit_ok = true) {
-  if (c.kind == CodecKind::onebit && !onebit_ok)
-    throw Error(B2_ERR_UNSUPPORTED, "onebit codec is implemented for c_lp_s only on the B200 path");
+void check_codec(const Codec& c, std::mt19937* rng) {
   if (c.kind == CodecKind::uniform8 && c.rounding == Rounding::stochastic) {
     if (!rng) throw Error(B2_ERR_INVALID, "uniform8 stochastic rounding needs a generator");  // codec.cpp:70
     throw Error(B2_ERR_UNSUPPORTED, "uniform8 stochastic rounding is not implemented on the B200 path");
@@ -395,7 +393,7 @@ double d_fp_s(B200Endpoint& ep, double now, std::span<float> x, const Topology& 
 
 double d_lp_s(B200Endpoint& ep, double now, std::span<float> x, const Topology& topo, std::uint64_t round,
               const Codec& codec, ReduceMode mode, std::mt19937* rng, std::uint32_t bucket) {
-  check_codec(codec, rng, /*onebit_ok=*/false);
+  check_codec(codec, rng);
   const auto nb = nbrs_of(ep, topo, round);
   DeviceScope ds(ep.device());
   auto s = static_cast<cudaStream_t>(ep.stream());

@@ -184,6 +184,31 @@ def run(args):
             orc.c_lp_s(w, codec=2)
         ck.close(f"c_lp_s onebit back-to-back buf{r}", ts[r].cpu().numpy(), w[rank])
 
+    # ---- D_LP_S onebit over ring / full / random, both modes, repeated rounds
+    for n in [1, 5, 37, 1000, 4097, 65536 + 7, 1_000_003] + ([] if args.quick else [4_000_000]):
+        bucket += 1
+        xs = [orc.synth(n, 8800 + r) for r in range(g)]
+        for kind in (b2.TopologyKind.ring, b2.TopologyKind.full, b2.TopologyKind.random):
+            topo = b2.Topology(kind, g, 77)
+            for rnd in range(3):
+                nb = topo.neighbors(rank, rnd)
+                for mode in (b2.ReduceMode.average, b2.ReduceMode.sum):
+                    t = torch.as_tensor(xs[rank]).cuda()
+                    b2.d_lp_s(ep, 0.0, t, topo, rnd, OB, mode, bucket=bucket)
+                    ck.close(f"d_lp_s onebit {kind.name} r{rnd} {mode.name} n={n}", t.cpu().numpy(),
+                             orc.d_lp_s_rank([xs[j] for j in nb], 2, int(mode)))
+    # back-to-back non-blocking onebit D_LP_S with a changing (random) topology, state carried
+    bucket += 1
+    n = 300_007
+    topo = b2.Topology(b2.TopologyKind.random, g, 5)
+    cur = [orc.synth(n, 610 + r) for r in range(g)]
+    t = torch.as_tensor(cur[rank]).cuda()
+    for rnd in range(12):
+        b2.d_lp_s(ep, 0.0, t, topo, rnd, OB, b2.ReduceMode.average, bucket=bucket, blocking=False)
+        cur = [orc.d_lp_s_rank([cur[j] for j in topo.neighbors(r, rnd)], 2, 1) for r in range(g)]
+    ep.sync()
+    ck.close("d_lp_s onebit back-to-back random topology", t.cpu().numpy(), cur[rank])
+
     # ---- interleaved buckets, non-blocking issue, one sync (overlap of buckets)
     bucket += 1
     n = 300_001

@@ -85,14 +85,9 @@ def test_nonfinite_raises():
         U8.decode(torch.tensor([1, 2, 3], dtype=torch.uint8).cuda(), 10)
 
 
-def test_stochastic_and_onebit_collective_are_rejected():
+def test_stochastic_rounding_is_rejected():
     with pytest.raises(b2.Error):
         b2.Codec(b2.CodecKind.uniform8, b2.Rounding.stochastic).encode(dev([1.0, 2.0]))
-    ep = b2.B200Endpoint(0, 1, 0)
-    with pytest.raises(b2.Error):  # D_LP_S with onebit: not on the B200 path
-        b2.d_lp_s(ep, 0.0, dev([1.0, 2.0]), b2.Topology(b2.TopologyKind.ring, 1, 0), 0,
-                  b2.Codec(b2.CodecKind.onebit), b2.ReduceMode.average)
-    ep.close()
 
 
 # ------------------------------------------------------------------ onebit

@@ -224,3 +224,13 @@ def test_c_lp_s_onebit_nonfinite_raises(ep):
     t = torch.tensor([1.0, float("inf"), 2.0], dtype=torch.float32).cuda()
     with pytest.raises(b2.Error):
         b2.c_lp_s(ep, 0.0, t, OB, None, bucket=43)
+
+
+@pytest.mark.parametrize("n", [1, 37, 1025, 1_000_003])
+def test_d_lp_s_onebit_g1(ep, oracle, n):
+    x = oracle.synth(n, 5050 + n)
+    topo = b2.Topology(b2.TopologyKind.ring, 1)
+    for mode in (b2.ReduceMode.average, b2.ReduceMode.sum):
+        t = torch.as_tensor(x).cuda()
+        b2.d_lp_s(ep, 0.0, t, topo, 0, OB, mode, bucket=44)
+        assert np.array_equal(bits(t.cpu().numpy()), bits(oracle.d_lp_s_rank([x], 2, int(mode))))

@@ -131,3 +131,17 @@ def test_onebit_ec_rounds_match_reference(oracle, ref):
         for p, q in zip(a + da + ea, b + db + eb):
             tol = 4 * np.spacing(np.float32(np.abs(q).max() if q.size else 1.0))
             assert np.abs(p - q).max(initial=0) <= tol
+
+
+@pytest.mark.parametrize("g", [2, 4, 8])
+def test_onebit_d_lp_s_matches_reference(oracle, ref, g):
+    # d_lp_s with Codec{onebit} (collectives.cpp:260-288); grid inputs: exact sums, bitwise
+    n = 50_001
+    xs = [ref.synth(n, 1313 + r) for r in range(g)]
+    for kind, seed in ((0, 0), (1, 5), (2, 0)):
+        for mode in (0, 1):
+            b = [x.copy() for x in xs]
+            ref.d_lp_s(b, topo_kind=kind, seed=seed, round_=1, codec=2, mode=mode)
+            for r in range(g):
+                nb = ref.neighbors(kind, g, seed, r, 1)
+                assert np.array_equal(bits(oracle.d_lp_s_rank([xs[j] for j in nb], 2, mode)), bits(b[r]))
