@@ -51,7 +51,7 @@ typedef enum {
   B2_ERR_CUDA = 2,        /* CUDA runtime failure                            */
   B2_ERR_NONFINITE = 3,   /* encode saw NaN/Inf  (codec.cpp:26)              */
   B2_ERR_TIMEOUT = 4,     /* a peer never arrived (rendezvous timeout)       */
-  B2_ERR_UNSUPPORTED = 5, /* e.g. stochastic rounding, onebit codec          */
+  B2_ERR_UNSUPPORTED = 5, /* e.g. stochastic rounding                          */
   B2_ERR_BOOTSTRAP = 6    /* the allgather callback failed                   */
 } b2_status;
 
@@ -103,8 +103,8 @@ int b2_u8_pack_wire(const uint8_t* codes, const float* hdr, size_t n, uint8_t* w
  * reference's order: scale is identical whenever that sum is exact and within
  * one float rounding otherwise.  A non-finite input gives a NaN scale (the
  * reference throws).  x, out, wire 16-byte aligned; wire holds 4 + ceil(n/8)
- * bytes rounded up to 4.  (Replaces Codec{onebit}.encode / decode; C_LP_S with
- * onebit still returns B2_ERR_UNSUPPORTED.) */
+ * bytes rounded up to 4.  (Replaces Codec{onebit}.encode / decode; the
+ * primitives below take B2_CODEC_ONEBIT too.) */
 int b2_onebit_encode(const float* x, size_t n, uint8_t* wire, void* stream);
 int b2_onebit_decode(const uint8_t* wire, size_t n, float* out, void* stream);
 int b2_u8_unpack_wire(const uint8_t* wire, size_t n, uint8_t* codes, float* hdr, void* stream);
@@ -153,7 +153,8 @@ int b2_comm_read_trace(b2_comm_t comm, uint64_t* out, int max_ctas, int* n_slots
  *   every rank ends with (float) sum_j (double) x_j, ranks folded ascending;
  *   world == 1 leaves x untouched.
  * c_lp_s  (collectives.hpp:59-61; scatter_reduce_lp collectives.cpp:91-163):
- *   codec B2_CODEC_UNIFORM8 (ByteGrad) or B2_CODEC_IDENTITY.  delta/eps both
+ *   codec B2_CODEC_UNIFORM8 (ByteGrad), B2_CODEC_ONEBIT (the 1-bit Adam
+ *   aggregation, algorithms.cpp:141-148) or B2_CODEC_IDENTITY.  delta/eps both
  *   NULL = stateless; else ErrorState (codec.hpp:40-47): delta has n floats,
  *   eps has owned_partition_len(n, world, rank) floats, both updated.
  *   stochastic rounding is not supported (B2_ERR_UNSUPPORTED).
@@ -161,7 +162,7 @@ int b2_comm_read_trace(b2_comm_t comm, uint64_t* out, int max_ctas, int* n_slots
  * d_lp_s  (collectives.hpp:69-72; collectives.cpp:260-288):
  *   nbrs = Topology::neighbors(rank, round) (sorted, self-inclusive, HOST
  *   array); the neighbour relation must be symmetric, as every rcomm
- *   Topology is.  mode = B2_REDUCE_SUM / B2_REDUCE_AVERAGE. */
+ *   Topology is.  mode = B2_REDUCE_SUM / B2_REDUCE_AVERAGE.  Any codec. */
 int b2_c_fp_s(b2_comm_t comm, float* x, size_t n, uint32_t bucket, void* stream);
 int b2_c_lp_s(b2_comm_t comm, float* x, size_t n, int codec, float* delta, size_t delta_len,
               float* eps, size_t eps_len, uint32_t bucket, void* stream);
