@@ -476,6 +476,8 @@ static int onebit_central(b2_comm_t c, float* x, size_t n, float* delta, size_t 
   if (delta) {  // collectives.cpp:102-107
     B2_REQUIRE(delta_len == n, "c_lp_s: delta length does not match bucket length");
     B2_REQUIRE(eps_len == own, "c_lp_s: epsilon length does not match owned partition");
+    B2_REQUIRE((reinterpret_cast<uintptr_t>(delta) & 15) == 0 && (reinterpret_cast<uintptr_t>(eps) & 15) == 0,
+               "delta and epsilon must be 16-byte aligned");
   }
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard dg(c->device);

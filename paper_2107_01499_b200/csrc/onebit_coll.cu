@@ -16,11 +16,10 @@
 //            my out2, grid barrier, scale2, publish; eps = y2 - D(P2).
 //   phase 3  every owner's out2 decoded into x (collectives.cpp:154-161).
 //
-// Layout: a warp tile is 1024 consecutive chunk elements; lane l of row r
-// holds element 32r + l, so one __ballot_sync per row yields the row's
-// 32-bit LE sign word exactly as sign_pack lays it out (bit k%8 of byte
-// k/8), and decode is one shuffle per row.  Loads/stores are 128 B per warp
-// instruction; the words of a tile are one 128 B line.
+// Layout: a warp tile is 1024 consecutive chunk elements moved as 16-byte
+// quads (see encode_tile); one __ballot_sync per element column gives a
+// 32-bit sign word, decode transposes the tile's 32 words once.  The words
+// of a tile are one 128 B line.
 //
 // Exactness: signs, the ascending fp64 fold and every fp32 expression are
 // the reference's.  The fp64 |y| sums are summed in a fixed tree order, not
@@ -94,6 +93,90 @@ __device__ __forceinline__ float sign_value(float y, float s) {  // D(Q(y)) for 
 }
 
 // G = the number of ranks (compile time: the fold's bit gathering unrolls).
+
+// Internal sign-word layout of a 1024-element tile: lane l holds elements
+// 128q + 4l + c (q = 0..7, c = 0..3) -- one 16-byte load per q -- and word
+// 4q + c collects, in bit l, the sign of element 128q + 4l + c.  The words
+// live only in the collectives' windows (b2_onebit_encode alone emits
+// sign_pack's wire order), so the layout follows the 16-byte accesses.
+__device__ __forceinline__ float comp(const float4& v, int c) {
+  return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ void set_comp(float4& v, int c, float f) {
+  if (c == 0) v.x = f; else if (c == 1) v.y = f; else if (c == 2) v.z = f; else v.w = f;
+}
+// elements [e, e+4) of p (zero past n); vec: p is 16-byte aligned
+template <bool STREAM>
+__device__ __forceinline__ float4 ld_quad(const float* p, size_t e, size_t n, bool vec) {
+  if (vec && e + 4 <= n) {
+    const float4* q = reinterpret_cast<const float4*>(p + e);
+    return STREAM ? __ldcs(q) : __ldcg(q);
+  }
+  float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  if (e < n) v.x = p[e];
+  if (e + 1 < n) v.y = p[e + 1];
+  if (e + 2 < n) v.z = p[e + 2];
+  if (e + 3 < n) v.w = p[e + 3];
+  return v;
+}
+__device__ __forceinline__ void st_quad(float* p, size_t e, size_t n, bool vec, float4 v) {
+  if (vec && e + 4 <= n) {
+    __stcs(reinterpret_cast<float4*>(p + e), v);
+    return;
+  }
+  if (e < n) p[e] = v.x;
+  if (e + 1 < n) p[e + 1] = v.y;
+  if (e + 2 < n) p[e + 2] = v.z;
+  if (e + 3 < n) p[e + 3] = v.w;
+}
+__device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Sign word of this lane (word index = lane) for tile [base, base+1024) of
+// y = x - d (d null: y = x), accumulating sum |y| in fp64 (kernels.cpp:26-32).
+template <bool EC>
+__device__ __forceinline__ uint32_t encode_tile(const float* x, const float* d, size_t base, size_t n, bool vec,
+                                                int lane, double& acc) {
+  float4 v[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const size_t e = base + 128 * q + 4 * lane;
+    v[q] = ld_quad<true>(x, e, n, vec);
+    if (EC) {  // codec.cpp:131
+      const float4 dq = ld_quad<true>(d, e, n, vec);
+      v[q] = make_float4(__fsub_rn(v[q].x, dq.x), __fsub_rn(v[q].y, dq.y), __fsub_rn(v[q].z, dq.z),
+                         __fsub_rn(v[q].w, dq.w));
+    }
+  }
+  const bool full = base + kTile <= n;
+  uint32_t word = 0;
+  double acc_odd = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float y = comp(v[q], c);  // +0 past n: no |y|
+      const bool in = full || base + 128 * q + 4 * lane + c < n;
+      const uint32_t b = __ballot_sync(0xffffffffu, in && !(__float_as_uint(y) >> 31));
+      if (lane == 4 * q + c) word = b;
+      if (c & 1)
+        acc_odd = __dadd_rn(acc_odd, fabs(double(y)));
+      else
+        acc = __dadd_rn(acc, fabs(double(y)));
+    }
+  }
+  acc = __dadd_rn(acc, acc_odd);
+  return word;
+}
+
+// Valid-bit mask of word `lane` of a tile with rem elements left.
+__device__ __forceinline__ uint32_t valid_mask(size_t rem, int lane) {
+  if (rem >= kTile) return 0xffffffffu;
+  const size_t off = 128 * size_t(lane >> 2) + (lane & 3);
+  if (rem <= off) return 0u;
+  const size_t cnt = (rem - off + 3) / 4;
+  return cnt >= 32 ? 0xffffffffu : (1u << cnt) - 1u;
+}
+
 template <int G, bool EC>
 __global__ void __launch_bounds__(kThr) onebit_central_kernel(OnebitArgs a) {
   cg::grid_group grid = cg::this_grid();
@@ -119,36 +202,10 @@ __global__ void __launch_bounds__(kThr) onebit_central_kernel(OnebitArgs a) {
     uint32_t* dst = reinterpret_cast<uint32_t*>(a.win[k] + a.off_recv1 + size_t(me) * a.slot_stride + 16);
     const float* xk = a.x + lo;
     const float* dk = EC ? a.delta + lo : nullptr;
+    const bool vec = aligned16(xk) && (!EC || aligned16(dk));
     double acc = 0.0;
-    for (size_t t = warp; t * kTile < nk; t += nwarps) {
-      const size_t base = t * kTile;
-      const bool full = base + kTile <= nk;
-      float y[32];
-#pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const size_t e = base + 32 * r + lane;
-        float v = 0.0f;
-        if (full || e < nk) {
-          v = __ldcs(xk + e);
-          if (EC) v = __fsub_rn(v, __ldcs(dk + e));  // codec.cpp:131
-        }
-        y[r] = v;  // out-of-range lanes hold +0: no bit, no |y|
-      }
-      uint32_t word = 0;
-      double acc_odd = 0.0;
-#pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const bool in = full || base + 32 * r + lane < nk;
-        const uint32_t b = __ballot_sync(0xffffffffu, in && !(__float_as_uint(y[r]) >> 31));
-        if (lane == r) word = b;
-        if (r & 1)
-          acc_odd = __dadd_rn(acc_odd, fabs(double(y[r])));
-        else
-          acc = __dadd_rn(acc, fabs(double(y[r])));
-      }
-      acc = __dadd_rn(acc, acc_odd);  // a non-finite y makes the chunk's sum non-finite
-      dst[t * 32 + lane] = word;
-    }
+    for (size_t t = warp; t * kTile < nk; t += nwarps)
+      dst[t * 32 + lane] = encode_tile<EC>(xk, dk, t * kTile, nk, vec, lane, acc);
     bad |= !isfinite(acc);  // finite |y| cannot overflow an fp64 sum
     const double s = block_sum(acc, red);
     if (threadIdx.x == 0) a.partials[size_t(k) * gridDim.x + blockIdx.x] = s;
@@ -218,8 +275,7 @@ __global__ void __launch_bounds__(kThr) onebit_central_kernel(OnebitArgs a) {
 #pragma unroll
     for (int p = 0; p < (1 << G); ++p) cnt[p] = 0;
     for (size_t t = warp; t * kTile < mn; t += nwarps) {
-      const size_t e0 = t * kTile + 32 * size_t(lane);  // this lane's word = elements [e0, e0 + 32)
-      const uint32_t valid = e0 + 32 <= mn ? 0xffffffffu : (e0 >= mn ? 0u : (1u << (mn - e0)) - 1u);
+      const uint32_t valid = valid_mask(mn - t * kTile, lane);
       uint32_t w[G];
 #pragma unroll
       for (int j = 0; j < G; ++j) w[j] = __ldcg(src[j] + t * 32 + lane);
@@ -247,26 +303,33 @@ __global__ void __launch_bounds__(kThr) onebit_central_kernel(OnebitArgs a) {
     for (size_t t = warp; t * kTile < mn; t += nwarps) {
       const size_t base = t * kTile;
       const bool full = base + kTile <= mn;
-      uint32_t col[G];  // lane l: bit r = rank j's sign of element 32r + l
+      uint32_t col[G];  // lane l: bit 4q+c = rank j's sign of element 128q + 4l + c
 #pragma unroll
       for (int j = 0; j < G; ++j) col[j] = transpose32(__ldcg(src[j] + t * 32 + lane), lane);
       uint32_t word = 0;
 #pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const size_t e = base + 32 * r + lane;
-        const bool in = full || e < mn;
-        uint32_t idx = 0;
+      for (int q = 0; q < 8; ++q) {
+        const size_t e = base + 128 * q + 4 * lane;
+        float4 ev = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (EC) ev = ld_quad<false>(a.eps, e, mn, true);
 #pragma unroll
-        for (int j = 0; j < G; ++j) idx |= ((col[j] >> r) & 1u) << j;
-        float y2 = fold_tab[idx];
-        if (EC && in) {
-          y2 = __fsub_rn(y2, a.eps[e]);  // compensate_encode with epsilon
-          a.eps[e] = y2;                 // stash y2 until scale2 is known
+        for (int c = 0; c < 4; ++c) {
+          const int k = 4 * q + c;
+          const bool in = full || e + c < mn;
+          uint32_t idx = 0;
+#pragma unroll
+          for (int j = 0; j < G; ++j) idx |= ((col[j] >> k) & 1u) << j;
+          float y2 = fold_tab[idx];
+          if (EC) {
+            y2 = __fsub_rn(y2, comp(ev, c));  // compensate_encode with epsilon
+            set_comp(ev, c, y2);              // stash y2 until scale2 is known
+          }
+          if (!in) y2 = 0.0f;
+          const uint32_t b = __ballot_sync(0xffffffffu, in && !(__float_as_uint(y2) >> 31));
+          if (lane == k) word = b;
+          acc2 = __dadd_rn(acc2, fabs(double(y2)));
         }
-        if (!in) y2 = 0.0f;
-        const uint32_t b = __ballot_sync(0xffffffffu, in && !(__float_as_uint(y2) >> 31));
-        if (lane == r) word = b;
-        acc2 = __dadd_rn(acc2, fabs(double(y2)));
+        if (EC) st_quad(a.eps, e, mn, true, ev);
       }
       out2[t * 32 + lane] = word;
     }
@@ -304,14 +367,16 @@ __global__ void __launch_bounds__(kThr) onebit_central_kernel(OnebitArgs a) {
     const float s = __ldcg(reinterpret_cast<const float*>(a.win[k] + a.off_out2));
     const uint32_t* bits = reinterpret_cast<const uint32_t*>(a.win[k] + a.off_out2 + 16);
     float* xk = a.x + lo;
+    const bool vec = aligned16(xk);
     for (size_t t = warp; t * kTile < nk; t += nwarps) {
       const size_t base = t * kTile;
-      const bool full = base + kTile <= nk;
       const uint32_t col = transpose32(__ldcg(bits + t * 32 + lane), lane);
 #pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const size_t e = base + 32 * r + lane;
-        if (full || e < nk) __stcs(xk + e, ((col >> r) & 1u) ? s : -s);  // kernels.cpp:65-69
+      for (int q = 0; q < 8; ++q) {
+        float4 o;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) set_comp(o, c, ((col >> (4 * q + c)) & 1u) ? s : -s);  // kernels.cpp:65-69
+        st_quad(xk, base + 128 * q + 4 * lane, nk, vec, o);
       }
     }
   }
@@ -344,30 +409,8 @@ __global__ void __launch_bounds__(kThr) onebit_decent_kernel(OnebitDecentArgs a)
   // encode: sign words into my window, fp64 sum |x| (kernels.cpp:26-32, 58-63)
   uint32_t* bits = reinterpret_cast<uint32_t*>(mine + 16);
   double acc = 0.0;
-  for (size_t t = warp; t * kTile < n; t += nwarps) {
-    const size_t base = t * kTile;
-    const bool full = base + kTile <= n;
-    float y[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const size_t e = base + 32 * r + lane;
-      y[r] = (full || e < n) ? __ldcg(a.x + e) : 0.0f;
-    }
-    uint32_t word = 0;
-    double acc_odd = 0.0;
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const bool in = full || base + 32 * r + lane < n;
-      const uint32_t b = __ballot_sync(0xffffffffu, in && !(__float_as_uint(y[r]) >> 31));
-      if (lane == r) word = b;
-      if (r & 1)
-        acc_odd = __dadd_rn(acc_odd, fabs(double(y[r])));
-      else
-        acc = __dadd_rn(acc, fabs(double(y[r])));
-    }
-    acc = __dadd_rn(acc, acc_odd);
-    bits[t * 32 + lane] = word;
-  }
+  for (size_t t = warp; t * kTile < n; t += nwarps)
+    bits[t * 32 + lane] = encode_tile<false>(a.x, nullptr, t * kTile, n, true, lane, acc);
   const bool bad = !isfinite(acc);  // finite |x| cannot overflow an fp64 sum
   const double s = block_sum(acc, red);
   if (threadIdx.x == 0) a.partials[blockIdx.x] = s;
@@ -400,17 +443,20 @@ __global__ void __launch_bounds__(kThr) onebit_decent_kernel(OnebitDecentArgs a)
   for (int i = 0; i < NB; ++i) src[i] = reinterpret_cast<const uint32_t*>(a.win[a.nbrs[i]] + a.off_dbuf + 16);
   for (size_t t = warp; t * kTile < n; t += nwarps) {
     const size_t base = t * kTile;
-    const bool full = base + kTile <= n;
     uint32_t col[NB];
 #pragma unroll
     for (int i = 0; i < NB; ++i) col[i] = transpose32(__ldcg(src[i] + t * 32 + lane), lane);
 #pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const size_t e = base + 32 * r + lane;
-      uint32_t idx = 0;
+    for (int q = 0; q < 8; ++q) {
+      float4 o;
 #pragma unroll
-      for (int i = 0; i < NB; ++i) idx |= ((col[i] >> r) & 1u) << i;
-      if (full || e < n) __stcs(a.x + e, tab[idx]);
+      for (int c = 0; c < 4; ++c) {
+        uint32_t idx = 0;
+#pragma unroll
+        for (int i = 0; i < NB; ++i) idx |= ((col[i] >> (4 * q + c)) & 1u) << i;
+        set_comp(o, c, tab[idx]);
+      }
+      st_quad(a.x, base + 128 * q + 4 * lane, n, true, o);
     }
   }
   // my reads of the neighbours' windows are done: one credit to each of them

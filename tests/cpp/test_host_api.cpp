@@ -107,6 +107,50 @@ static void test_codec_kats() {
   report(bitwise(delta, dref) && bitwise(dec, dd), "compensate_encode bit-exact vs oracle");
 }
 
+static void test_onebit() {
+  Codec ob{CodecKind::onebit};
+  auto p = ob.encode(std::vector<float>{1, -1, 1, 1, -1, 1, 1, 1, -1});  // test_codec.cpp:103-123
+  float scale;
+  std::memcpy(&scale, p.data(), 4);
+  report(p.size() == 6 && scale == 1.0f && p[4] == 0xED && p[5] == 0, "onebit wire KAT");
+  bool ok = true;
+  for (std::size_t n : {1ul, 9ul, 1000ul, 65537ul}) {
+    auto x = synth(n, 300 + n);
+    auto w = ob.encode(x);
+    std::vector<std::uint8_t> ref(4 + (n + 7) / 8);
+    orc_onebit_encode_wire(x.data(), n, ref.data());
+    ok &= w == ref;
+    auto d = ob.decode(w, n);
+    std::vector<float> rd(n);
+    orc_onebit_decode_wire(ref.data(), n, rd.data());
+    ok &= bitwise(d, rd);
+  }
+  report(ok, "onebit random vectors bit-exact vs oracle");
+  B200Endpoint ep(0, 1, 0);
+  std::vector<float> x = {0.3f, -0.1f};  // test_collectives.cpp:209-225
+  ErrorState es(2, 2, 0);
+  c_lp_s(ep, 0.0, x, ob, &es);
+  std::vector<float> d(2), e(2);
+  cudaMemcpy(d.data(), es.delta(), 8, cudaMemcpyDefault);
+  cudaMemcpy(e.data(), es.epsilon(), 8, cudaMemcpyDefault);
+  report(std::fabs(x[0] - 0.2f) < 1e-6f && std::fabs(x[1] + 0.2f) < 1e-6f && std::fabs(d[0] - 0.1f) < 1e-6f &&
+             std::fabs(d[1] - 0.1f) < 1e-6f && e[0] == 0.0f && e[1] == 0.0f,
+         "c_lp_s onebit+EC single-worker KAT");
+  for (std::size_t n : {37ul, 1000003ul}) {
+    auto y = synth(n, 4242), want = y;
+    float* xs[] = {want.data()};
+    orc_c_lp_s(1, n, xs, ORC_CODEC_ONEBIT, nullptr, nullptr);
+    c_lp_s(ep, 0.0, y, ob, nullptr);
+    report(bitwise(y, want), "c_lp_s onebit g=1 n=" + std::to_string(n));
+    auto z = synth(n, 4343);
+    const float* nb[] = {z.data()};
+    std::vector<float> wz(n);
+    orc_d_lp_s_rank(n, nb, 1, ORC_CODEC_ONEBIT, ORC_REDUCE_AVERAGE, wz.data());
+    d_lp_s(ep, 0.0, z, Topology{TopologyKind::ring, 1, 0}, 0, ob, ReduceMode::average);
+    report(bitwise(z, wz), "d_lp_s onebit g=1 n=" + std::to_string(n));
+  }
+}
+
 static void test_tensor() {  // test_tensor.cpp:10-60
   FlatTensor t1("t1", {2}, {1.0f, 2.0f}), t2("t2", {1}, {3.0f});
   auto arena = BucketArena::flatten({&t1, &t2});
@@ -320,6 +364,7 @@ int main() {
   }
   try {
     test_codec_kats();
+    test_onebit();
     test_tensor();
     test_single_rank();
     for (int g = 2; g <= std::min(ndev, 4); g *= 2) test_multi(g);
