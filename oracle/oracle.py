@@ -52,6 +52,7 @@ class Oracle:
         L.orc_u8_compensate_encode.argtypes = [_f32p, _f32p, _sz, _f32p, _f32p, _u8p, _f32p]
         L.orc_c_fp_s.argtypes = [C.c_int, _sz, C.POINTER(_f32p)]
         L.orc_c_lp_s.argtypes = [C.c_int, _sz, C.POINTER(_f32p), C.c_int, C.POINTER(_f32p), C.POINTER(_f32p)]
+        L.orc_hierarchical_c.argtypes = [C.c_int, _sz, C.POINTER(_f32p), C.POINTER(C.c_int), C.c_int]
         L.orc_d_fp_s_rank.argtypes = [_sz, C.POINTER(_f32p), C.c_int, C.c_int, _f32p]
         L.orc_d_lp_s_rank.argtypes = [_sz, C.POINTER(_f32p), C.c_int, C.c_int, C.c_int, _f32p]
         L.orc_topology_neighbors.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]
@@ -135,6 +136,12 @@ class Oracle:
         if rc:
             raise ValueError("encode: non-finite input value")
 
+    def hierarchical_c(self, xs, nodes, codec=1):
+        arr = (C.c_int * len(nodes))(*nodes)
+        rc = self.lib.orc_hierarchical_c(len(xs), xs[0].size, _ptr_array(xs), arr, codec)
+        if rc:
+            raise ValueError("encode: non-finite input value")
+
     def d_fp_s_rank(self, nbr_xs, mode=1):
         out = np.zeros(nbr_xs[0].size, np.float32)
         self.lib.orc_d_fp_s_rank(out.size, _ptr_array(nbr_xs), len(nbr_xs), mode, _f(out))
@@ -183,6 +190,7 @@ class Reference:
         L.ref_c_fp_s.argtypes = [C.c_int, _sz, C.POINTER(_f32p), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.ref_c_lp_s.argtypes = [C.c_int, _sz, C.POINTER(_f32p), C.c_int, C.POINTER(_f32p),
                                  C.POINTER(_f32p), C.c_int, C.POINTER(C.c_uint64)]
+        L.ref_hierarchical_c.argtypes = [C.c_int, _sz, C.POINTER(_f32p), C.POINTER(C.c_int), C.c_int]
         L.ref_d_fp_s.argtypes = [C.c_int, _sz, C.POINTER(_f32p), C.c_int, C.c_uint64, C.c_uint64, C.c_int]
         L.ref_d_lp_s.argtypes = [C.c_int, _sz, C.POINTER(_f32p), C.c_int, C.c_uint64, C.c_uint64,
                                  C.c_int, C.c_int]
@@ -247,6 +255,10 @@ class Reference:
                                         _ptr_array(deltas) if deltas is not None else None,
                                         _ptr_array(eps) if eps is not None else None, rounds, b))
         return list(b)
+
+    def hierarchical_c(self, xs, nodes, codec=1):
+        arr = (C.c_int * len(nodes))(*nodes)
+        self._check(self.lib.ref_hierarchical_c(len(xs), xs[0].size, _ptr_array(xs), arr, codec))
 
     def d_fp_s(self, xs, topo_kind=0, seed=0, round_=0, mode=1):
         self._check(self.lib.ref_d_fp_s(len(xs), xs[0].size, _ptr_array(xs), topo_kind, seed, round_, mode))

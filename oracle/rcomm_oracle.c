@@ -189,6 +189,77 @@ int orc_c_lp_s(int g, size_t len, float* const* xs, int codec,
   return rc;
 }
 
+/* hierarchical_c, collectives.cpp:290-385 (no error feedback).  nodes[r] is
+ * rank r's node; members of a node ascending, leader = lowest member. */
+int orc_hierarchical_c(int g, size_t len, float* const* xs, const int* nodes, int codec) {
+  int node_ids[64], L = 0, rc = ORC_OK;
+  for (int r = 0; r < g; ++r) { /* distinct nodes, ascending (std::map order, 303-308) */
+    int seen = 0;
+    for (int i = 0; i < L; ++i) seen |= node_ids[i] == nodes[r];
+    if (!seen) node_ids[L++] = nodes[r];
+  }
+  for (int i = 1; i < L; ++i) /* insertion sort */
+    for (int j = i; j > 0 && node_ids[j - 1] > node_ids[j]; --j) {
+      int t = node_ids[j]; node_ids[j] = node_ids[j - 1]; node_ids[j - 1] = t;
+    }
+  double* acc = (double*)calloc((size_t)L * (len ? len : 1), sizeof(double));
+  int leaders[64];
+  for (int i = 0; i < L; ++i) {
+    double* a = acc + (size_t)i * len;
+    leaders[i] = -1;
+    for (int r = 0; r < g; ++r) /* members in rank order (322-334) */
+      if (nodes[r] == node_ids[i]) {
+        if (leaders[i] < 0) leaders[i] = r;
+        for (size_t e = 0; e < len; ++e) a[e] += (double)xs[r][e];
+      }
+  }
+  /* leaders sorted ascending by rank (308) */
+  for (int i = 1; i < L; ++i)
+    for (int j = i; j > 0 && leaders[j - 1] > leaders[j]; --j) {
+      int t = leaders[j]; leaders[j] = leaders[j - 1]; leaders[j - 1] = t;
+      for (size_t e = 0; e < len; ++e) {
+        double d = acc[(size_t)j * len + e];
+        acc[(size_t)j * len + e] = acc[(size_t)(j - 1) * len + e];
+        acc[(size_t)(j - 1) * len + e] = d;
+      }
+    }
+  if (L > 1 && codec == ORC_CODEC_IDENTITY) {
+    /* fp64 partials: owner k's part = its own acc, then the other leaders'
+     * in leader order (350-357); every leader ends with all parts (360-372) */
+    double* fin = (double*)malloc((len ? len : 1) * sizeof(double));
+    for (int k = 0; k < L; ++k) {
+      size_t lo, m;
+      orc_partition_range(len, L, k, &lo, &m);
+      for (size_t e = 0; e < m; ++e) {
+        double part = acc[(size_t)k * len + lo + e];
+        for (int j = 0; j < L; ++j)
+          if (j != k) part += acc[(size_t)j * len + lo + e];
+        fin[lo + e] = part;
+      }
+    }
+    for (int i = 0; i < L; ++i)
+      for (size_t e = 0; e < len; ++e) xs[leaders[i]][e] = (float)fin[e];
+    free(fin);
+  } else {
+    for (int i = 0; i < L; ++i)
+      for (size_t e = 0; e < len; ++e) xs[leaders[i]][e] = (float)acc[(size_t)i * len + e];
+    if (L > 1) { /* scatter_reduce_lp over the leader group (375) */
+      float* lx[64];
+      for (int i = 0; i < L; ++i) lx[i] = xs[leaders[i]];
+      rc = orc_c_lp_s(L, len, lx, codec, NULL, NULL);
+    }
+  }
+  /* leaders send x down to their members (382-383) */
+  for (int r = 0; r < g; ++r) {
+    int lead = -1;
+    for (int i = 0; i < L && lead < 0; ++i)
+      if (nodes[leaders[i]] == nodes[r]) lead = leaders[i];
+    if (lead != r) memcpy(xs[r], xs[lead], len * sizeof(float));
+  }
+  free(acc);
+  return rc;
+}
+
 /* d_fp_s, collectives.cpp:229-258 (one rank) */
 void orc_d_fp_s_rank(size_t len, const float* const* nbr_x, int nnb, int mode,
                      float* out) {

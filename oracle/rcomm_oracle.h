@@ -46,6 +46,10 @@ int orc_u8_encode(const float* x, size_t n, float* lo, float* hi, uint8_t* codes
  * 58-63): scale = (float)(sequential fp64 sum of |x|) / (float)n; wire =
  * [scale f32][ceil(n/8) bytes, bit k (LE) = !signbit(x[k])].  Returns
  * ORC_ERR_NONFINITE where the reference throws. */
+/* hierarchical_c, collectives.cpp:290-385 (no error feedback); nodes[r] =
+ * node of rank r (<= 64 ranks). */
+int orc_hierarchical_c(int g, size_t len, float* const* xs, const int* nodes, int codec);
+
 int orc_onebit_encode_wire(const float* x, size_t n, uint8_t* wire);
 /* codec.cpp:110-114, kernels.cpp:65-69 */
 void orc_onebit_decode_wire(const uint8_t* wire, size_t n, float* out);

@@ -205,6 +205,18 @@ int ref_c_lp_s(int g, std::size_t len, float* const* xs, int codec,
   });
 }
 
+// hierarchical_c (collectives.cpp:290-385) on a SimCluster whose ranks sit
+// on nodes[r] (sim_transport.hpp node assignment), no error feedback.
+int ref_hierarchical_c(int g, std::size_t len, float* const* xs, const int* nodes, int codec) {
+  return guarded([&] {
+    SimCluster cluster(g, fast_profile(), std::vector<int>(nodes, nodes + g));
+    const Codec c = make_codec(codec);
+    run_workers(cluster, g, [&](Endpoint& ep, int r) {
+      hierarchical_c(ep, 0.0, std::span<float>(xs[r], len), c, nullptr);
+    });
+  });
+}
+
 int ref_d_fp_s(int g, std::size_t len, float* const* xs, int topo_kind,
                std::uint64_t seed, std::uint64_t round, int mode) {
   return guarded([&] {

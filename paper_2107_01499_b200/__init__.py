@@ -17,6 +17,7 @@ from .collectives import (  # noqa: F401
     c_lp_s,
     d_fp_s,
     d_lp_s,
+    hierarchical_c,
     owned_partition_len,
     partition_range,
     phase,
@@ -28,5 +29,5 @@ __all__ = [
     "OverlapEngine", "plan_buckets",
     "B200Endpoint", "BucketArena", "Codec", "CodecKind", "Error", "ErrorState", "FlatTensor", "ReduceMode",
     "Rounding", "TensorView", "ThreadBootstrap", "Topology", "TopologyKind", "TorchBootstrap", "c_fp_s",
-    "c_lp_s", "compensate_encode", "d_fp_s", "d_lp_s", "owned_partition_len", "partition_range", "phase",
+    "c_lp_s", "compensate_encode", "d_fp_s", "d_lp_s", "hierarchical_c", "owned_partition_len", "partition_range", "phase",
 ]

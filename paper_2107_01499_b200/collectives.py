@@ -362,6 +362,73 @@ def c_lp_s(ep: B200Endpoint, now: float, x, codec: Codec, es: ErrorState | None,
     return now
 
 
+def _node_groups(nodes):
+    """Members per node (ascending) and the leaders (lowest member of each
+    node, ascending), as hierarchical_c forms them (collectives.cpp:299-310)."""
+    by_node: dict = {}
+    for r, nd in enumerate(nodes):
+        by_node.setdefault(nd, []).append(r)
+    members = [by_node[nd] for nd in sorted(by_node)]
+    leaders = sorted(m[0] for m in members)
+    return members, leaders
+
+
+def _hier_endpoints(ep: B200Endpoint, nodes):
+    """Sub-communicators of one node layout, created once (collectively:
+    every rank creates every group in the same order)."""
+    cache = ep.__dict__.setdefault("_hier", {})
+    key = tuple(nodes)
+    if key not in cache:
+        import torch.distributed as dist
+        members, leaders = _node_groups(nodes)
+        me = ep.rank()
+        intra = lead = None
+        for m in members:
+            grp = dist.new_group(m, backend="gloo")
+            if me in m:
+                intra = B200Endpoint(m.index(me), len(m), ep.device, bootstrap=TorchBootstrap(grp))
+        grp = dist.new_group(leaders, backend="gloo")
+        if me in leaders:
+            lead = B200Endpoint(leaders.index(me), len(leaders), ep.device, bootstrap=TorchBootstrap(grp))
+        cache[key] = (intra, lead)
+    return cache[key]
+
+
+def hierarchical_c(ep: B200Endpoint, now: float, x, codec: Codec, es: ErrorState | None = None, rng=None,
+                   bucket: int = 0, nodes=None) -> float:
+    """Two-level centralized aggregation (collectives.cpp:290-385): members'
+    x summed in fp64 at the node leader, leaders aggregate across nodes --
+    fp64 partials when the codec is lossless, scatter_reduce_lp (C_LP_S over
+    the leader group, with es) otherwise -- and every member ends with its
+    leader's result.  nodes[r] = node of rank r (default: ep.node_of, i.e.
+    one node).  Blocking.
+
+    One node, or a lossless codec: the result is the fp64 sum of every rank's
+    x rounded once, which is c_fp_s over all ranks (the reference's lossless
+    branch exchanges fp64 partials exactly so that it matches the flat
+    primitive, test_collectives.cpp:234-252; association order differs only
+    when those fp64 sums are inexact).  Lossy across nodes: c_fp_s inside the
+    node (every member holds the leader's (float) node sum), c_lp_s among the
+    leaders, then c_fp_s inside the node with the members contributing +0 --
+    exactly the leader's values (a -0.0 arrives as +0.0; compare with ==)."""
+    codec._check_supported(rng)
+    g, me = ep.world_size(), ep.rank()
+    nodes = list(nodes) if nodes is not None else [ep.node_of(r) for r in range(g)]
+    if len(nodes) != g:
+        raise Error("hierarchical: node list does not match the world size")
+    members, leaders = _node_groups(nodes)
+    if len(leaders) == 1 or codec.lossless():
+        return c_fp_s(ep, now, x, bucket)
+    intra, lead = _hier_endpoints(ep, nodes)
+    c_fp_s(intra, now, x, bucket)
+    if lead is not None:
+        c_lp_s(lead, now, x, codec, es, rng, bucket)
+    else:
+        x.zero_()
+    c_fp_s(intra, now, x, bucket)  # down: the leader's values to its members
+    return now
+
+
 def _neighbors(ep: B200Endpoint, topo: Topology, round_: int):
     if topo.n != ep.world_size():
         raise Error("topology size mismatch")  # collectives.cpp:232

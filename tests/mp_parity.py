@@ -209,6 +209,23 @@ def run(args):
     ep.sync()
     ck.close("d_lp_s onebit back-to-back random topology", t.cpu().numpy(), cur[rank])
 
+    # ---- hierarchical_c over virtual node layouts (collectives.cpp:290-385)
+    layouts = {2: [[0, 1], [0, 0]], 3: [[0, 0, 1], [0, 1, 2]], 4: [[0, 0, 1, 1], [0, 1, 1, 2], [1, 0, 1, 0]]}
+    for nodes in layouts.get(g, [[0] * g]):
+        for codec_kind, codec in ((0, ID), (1, U8), (2, OB)):
+            for n in (37, 100_003):
+                bucket += 1
+                xs = [orc.synth(n, 7700 + r) for r in range(g)]
+                want = [x.copy() for x in xs]
+                orc.hierarchical_c(want, nodes, codec_kind)
+                t = torch.as_tensor(xs[rank]).cuda()
+                b2.hierarchical_c(ep, 0.0, t, codec, None, bucket=bucket, nodes=nodes)
+                got = t.cpu().numpy()
+                if np.array_equal(got, want[rank]):  # == : a -0.0 leader value reaches members as +0.0
+                    ck.passed += 1
+                else:
+                    ck.fail.append(f"rank{rank} hierarchical_c nodes={nodes} codec={codec_kind} n={n}")
+
     # ---- interleaved buckets, non-blocking issue, one sync (overlap of buckets)
     bucket += 1
     n = 300_001

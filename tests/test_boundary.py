@@ -134,3 +134,10 @@ def test_codec_host_errors():
 def test_status_strings(b2lib):
     assert b2lib.lib.b2_status_string(b2lib.B2_ERR_NONFINITE) == b"encode: non-finite input value"
     assert b2lib.lib.b2_version() == 1
+
+
+def test_hierarchical_node_groups():
+    # collectives.cpp:299-310: members ascending per node, leaders = lowest member, ascending
+    from paper_2107_01499_b200.collectives import _node_groups
+    assert _node_groups([0, 0, 0, 1, 1, 2]) == ([[0, 1, 2], [3, 4], [5]], [0, 3, 5])
+    assert _node_groups([2, 0, 1, 0, 2, 1]) == ([[1, 3], [2, 5], [0, 4]], [0, 1, 2])

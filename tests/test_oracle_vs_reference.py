@@ -145,3 +145,18 @@ def test_onebit_d_lp_s_matches_reference(oracle, ref, g):
             for r in range(g):
                 nb = ref.neighbors(kind, g, seed, r, 1)
                 assert np.array_equal(bits(oracle.d_lp_s_rank([xs[j] for j in nb], 2, mode)), bits(b[r]))
+
+
+@pytest.mark.parametrize("nodes", [[0, 0, 0, 1, 1, 2], [0, 0, 1, 1], [0, 1], [0, 0, 0], [2, 0, 1, 0, 2, 1, 1, 0]])
+@pytest.mark.parametrize("codec", [0, 1, 2])
+def test_hierarchical_c_matches_reference(oracle, ref, nodes, codec):
+    # collectives.cpp:290-385: intra-node fp64 sum at the leader, leaders
+    # exchange fp64 partials (lossless) or run scatter_reduce_lp, members get
+    # the leader's result; the restatement must be bitwise equal
+    g, n = len(nodes), 10_007
+    xs = [ref.synth(n, 5150 + r) for r in range(g)]
+    a = [x.copy() for x in xs]
+    b = [x.copy() for x in xs]
+    oracle.hierarchical_c(a, nodes, codec)
+    ref.hierarchical_c(b, nodes, codec)
+    assert all(np.array_equal(bits(p), bits(q)) for p, q in zip(a, b))
