@@ -89,6 +89,13 @@ int b2_topology_neighbors(int kind, int n, uint64_t seed, int rank, uint64_t rou
  * into the reference's Error.  n == 0 writes hdr = (0, 0). */
 int b2_u8_encode(const float* x, size_t n, uint8_t* codes, float* hdr, void* stream);
 int b2_u8_decode(const uint8_t* codes, const float* hdr, size_t n, float* out, void* stream);
+/* Codec{uniform8, Rounding::stochastic}.encode (codec.cpp:67-78): as
+ * b2_u8_encode, levels rounded up with probability q - floor(q); the uniform
+ * draws come from a counter hash of (seed, element), not mt19937, so only
+ * unbiasedness is shared with the reference (test_codec.cpp:175-192).  The
+ * collectives still reject stochastic rounding (B2_ERR_UNSUPPORTED). */
+int b2_u8_encode_stochastic(const float* x, size_t n, uint8_t* codes, float* hdr, uint64_t seed,
+                            void* stream);
 /* compensate_encode (codec.hpp:49-54, codec.cpp:125-137) with uniform8:
  * y = x - delta; codes,hdr = Q(y); delta = y - D(Q(y)); decoded (nullable) = D(Q(y)) */
 int b2_u8_compensate_encode(const float* x, float* delta, size_t n, uint8_t* codes,

@@ -30,6 +30,7 @@ _SIGS = {
     "b2_payload_size": (C.c_size_t, [C.c_int, C.c_size_t]),
     "b2_topology_neighbors": (C.c_int, [C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_uint64, C.POINTER(C.c_int)]),
     "b2_u8_encode": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "b2_u8_encode_stochastic": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "b2_u8_decode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]),
     "b2_u8_compensate_encode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
                                           C.c_void_p, C.c_void_p]),

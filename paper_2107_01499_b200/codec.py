@@ -63,17 +63,29 @@ class Codec:
     def payload_size(self, n: int) -> int:
         return int(lib.b2_payload_size(int(self.kind), n))
 
-    def _check_supported(self, rng) -> None:
+    def _check_supported(self, rng, collective: bool = True) -> None:
         if self.kind == CodecKind.uniform8 and self.rounding == Rounding.stochastic:
             if rng is None:  # codec.cpp:70 wording
                 raise Error("uniform8 stochastic rounding needs a generator")
-            raise _lib.B2Error(_lib.B2_ERR_UNSUPPORTED,
-                               "uniform8 stochastic rounding is not implemented on the B200 path")
+            if collective:
+                raise _lib.B2Error(_lib.B2_ERR_UNSUPPORTED,
+                                   "uniform8 stochastic rounding is implemented for the codec, not the collectives")
+
+    @staticmethod
+    def _seed(rng) -> int:
+        """64 bits drawn from the caller's generator (random.Random-like or a
+        numpy Generator), advancing it like the reference's per-element draws
+        advance its mt19937 (codec.cpp:71-74)."""
+        if hasattr(rng, "getrandbits"):
+            return int(rng.getrandbits(64))
+        if hasattr(rng, "integers"):
+            return int(rng.integers(0, 2**64, dtype=np.uint64))
+        raise Error("stochastic rounding: rng must provide getrandbits() or integers()")
 
     # -- SoA device form (what the collectives use internally) -------------
-    def encode_soa(self, x: torch.Tensor):
+    def encode_soa(self, x: torch.Tensor, seed: int | None = None):
         """uniform8: -> (codes uint8[n], hdr float32[4]) on x's device; raises
-        Error on non-finite input (codec.cpp:24-27)."""
+        Error on non-finite input (codec.cpp:24-27).  seed: stochastic rounding."""
         assert x.is_cuda and x.dtype == torch.float32
         x = x.contiguous()
         if not _aligned(x):
@@ -81,7 +93,11 @@ class Codec:
         n = x.numel()
         codes = torch.empty(max(n, 4) + 16, dtype=torch.uint8, device=x.device)
         hdr = torch.empty(4, dtype=torch.float32, device=x.device)
-        check(lib.b2_u8_encode(x.data_ptr(), n, codes.data_ptr(), hdr.data_ptr(), _stream(x.device)))
+        if seed is None:
+            check(lib.b2_u8_encode(x.data_ptr(), n, codes.data_ptr(), hdr.data_ptr(), _stream(x.device)))
+        else:
+            check(lib.b2_u8_encode_stochastic(x.data_ptr(), n, codes.data_ptr(), hdr.data_ptr(), seed,
+                                              _stream(x.device)))
         lohi = hdr[:2].cpu()
         if not bool(torch.isfinite(lohi).all()):
             raise Error("encode: non-finite input value")
@@ -102,7 +118,7 @@ class Codec:
     def encode(self, x, rng=None):
         """Payload bytes.  Device input -> device uint8 tensor; host input ->
         numpy uint8 array (the reference's Payload)."""
-        self._check_supported(rng)
+        self._check_supported(rng, collective=False)
         xd, host = _as_device(x)
         xd = xd.reshape(-1)
         n = xd.numel()
@@ -120,7 +136,8 @@ class Codec:
                 raise Error("encode: non-finite input value")
             wire = xd.contiguous().view(torch.uint8).clone()
         else:
-            codes, hdr = self.encode_soa(xd)
+            stochastic = self.rounding == Rounding.stochastic
+            codes, hdr = self.encode_soa(xd, self._seed(rng) if stochastic else None)
             wire = torch.empty(8 + n, dtype=torch.uint8, device=xd.device)
             check(lib.b2_u8_pack_wire(codes.data_ptr() if n else 0, hdr.data_ptr(), n, wire.data_ptr(),
                                       _stream(xd.device)))

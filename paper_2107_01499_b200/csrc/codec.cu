@@ -235,6 +235,32 @@ __global__ void __launch_bounds__(kThreads) synth_kernel(float* x, size_t n, uin
   }
 }
 
+
+// Codec::encode uniform8 with Rounding::stochastic (codec.cpp:67-78):
+// level = floor(q) + (u < q - floor(q)), q = (x - min) * inv_step, clamped
+// to [0, 255].  u is uniform in [0, 1) with 24 random bits (the resolution of
+// std::uniform_real_distribution<float>) from a counter hash of (seed,
+// element) instead of the host's mt19937 stream, so the levels are unbiased
+// like the reference's (test_codec.cpp:175-192) but not the same draws.
+// Runs after the nearest-rounding encode, whose header it reuses; a
+// degenerate range keeps the all-zero codes (codec.cpp:62-64).
+__global__ void u8_stochastic_kernel(const float* __restrict__ x, size_t n, uint8_t* __restrict__ codes,
+                                     const float* __restrict__ hdr, uint64_t seed) {
+  const float lo = hdr[0], hi = hdr[1];
+  const float range = __fsub_rn(hi, lo);
+  if (range == 0.0f) return;
+  const float inv = __fdiv_rn(255.0f, range);
+  const uint64_t key = splitmix64(seed);
+  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += size_t(gridDim.x) * blockDim.x) {
+    const float q = __fmul_rn(__fsub_rn(x[e], lo), inv);
+    const float fl = floorf(q);
+    const float u = float(uint32_t(splitmix64(key + e) >> 40)) * 0x1p-24f;
+    float level = __fadd_rn(fl, u < __fsub_rn(q, fl) ? 1.0f : 0.0f);
+    level = level < 0.0f ? 0.0f : (level > 255.0f ? 255.0f : level);
+    codes[e] = uint8_t(level);
+  }
+}
+
 int grid_for(const void* f) { return persistent_grid(f, kThreads); }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -416,6 +442,15 @@ int b2_u8_encode(const float* x, size_t n, uint8_t* codes, float* hdr, void* str
   B2_REQUIRE(n == 0 || aligned16(x), "b2_u8_encode: x must be 16-byte aligned");
   B2_REQUIRE(n == 0 || aligned16(codes), "b2_u8_encode: codes must be 16-byte aligned");
   return launch_encode(x, nullptr, n, codes, hdr, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int b2_u8_encode_stochastic(const float* x, size_t n, uint8_t* codes, float* hdr, uint64_t seed, void* stream) {
+  int rc = b2_u8_encode(x, n, codes, hdr, stream);
+  if (rc != B2_OK || n == 0) return rc;
+  const int grid = int(std::min<size_t>((n + 255) / 256, size_t(sm_count()) * 8));
+  u8_stochastic_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(x, n, codes, hdr, seed);
+  B2_CUDA_TRY(cudaGetLastError());
+  return B2_OK;
 }
 
 // onebit scratch: per-block fp64 partials + the last-block counter, per device

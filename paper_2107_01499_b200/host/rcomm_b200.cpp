@@ -96,10 +96,11 @@ std::vector<float> to_host(std::span<const float> x) {
   return h;
 }
 
-void check_codec(const Codec& c, std::mt19937* rng) {
+void check_codec(const Codec& c, std::mt19937* rng, bool collective = true) {
   if (c.kind == CodecKind::uniform8 && c.rounding == Rounding::stochastic) {
     if (!rng) throw Error(B2_ERR_INVALID, "uniform8 stochastic rounding needs a generator");  // codec.cpp:70
-    throw Error(B2_ERR_UNSUPPORTED, "uniform8 stochastic rounding is not implemented on the B200 path");
+    if (collective)
+      throw Error(B2_ERR_UNSUPPORTED, "uniform8 stochastic rounding is implemented for the codec, not the collectives");
   }
 }
 
@@ -107,7 +108,7 @@ void check_codec(const Codec& c, std::mt19937* rng) {
 
 // ------------------------------------------------------------------ codec
 Payload Codec::encode(std::span<const float> x, std::mt19937* rng) const {
-  check_codec(*this, rng);
+  check_codec(*this, rng, /*collective=*/false);
   const std::size_t n = x.size();
   if (kind == CodecKind::identity) {  // codec.cpp:41,47-50
     std::vector<float> h = to_host(x);
@@ -131,7 +132,12 @@ Payload Codec::encode(std::span<const float> x, std::mt19937* rng) const {
   }
   DevBuf xs((n ? n : 1) * 4), codes(n + 64), hdr(B2_U8_HDR_BYTES), wire(8 + n);
   if (n) cuda_check(cudaMemcpy(xs.p, x.data(), 4 * n, cudaMemcpyDefault), "stage in");
-  check(b2_u8_encode(xs.as<float>(), n, codes.as<std::uint8_t>(), hdr.as<float>(), nullptr));
+  if (rounding == Rounding::stochastic) {  // seed drawn from (and advancing) the caller's mt19937
+    const std::uint64_t seed = (std::uint64_t((*rng)()) << 32) | std::uint64_t((*rng)());
+    check(b2_u8_encode_stochastic(xs.as<float>(), n, codes.as<std::uint8_t>(), hdr.as<float>(), seed, nullptr));
+  } else {
+    check(b2_u8_encode(xs.as<float>(), n, codes.as<std::uint8_t>(), hdr.as<float>(), nullptr));
+  }
   check(b2_u8_pack_wire(codes.as<std::uint8_t>(), hdr.as<float>(), n, wire.as<std::uint8_t>(), nullptr));
   Payload p(8 + n);
   cuda_check(cudaMemcpy(p.data(), wire.p, 8 + n, cudaMemcpyDeviceToHost), "copy payload");

@@ -127,6 +127,10 @@ def test_codec_host_errors():
     import paper_2107_01499_b200 as b2
     with pytest.raises(b2.Error, match="needs a generator"):
         b2.Codec(b2.CodecKind.uniform8, b2.Rounding.stochastic)._check_supported(None)
+    import random
+    with pytest.raises(b2.Error):  # the collectives keep rejecting stochastic rounding
+        b2.Codec(b2.CodecKind.uniform8, b2.Rounding.stochastic)._check_supported(random.Random(1))
+    b2.Codec(b2.CodecKind.uniform8, b2.Rounding.stochastic)._check_supported(random.Random(1), collective=False)
     b2.Codec(b2.CodecKind.onebit)._check_supported(None)  # every primitive takes the onebit codec
     assert b2.phase.make_tag(3, b2.phase.bcast) == 51
 

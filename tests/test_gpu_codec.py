@@ -234,3 +234,29 @@ def test_golden_fixtures():
         assert got[4:8].view(np.float32)[0] == wire[4:8].view(np.float32)[0]
         dec = U8.decode(torch.as_tensor(wire).cuda(), x.size).cpu().numpy()
         assert same(dec, z[f"dec{i}"])
+
+
+# ------------------------------------------------- stochastic rounding
+def test_stochastic_rounding_unbiased():
+    # test_codec.cpp:175-192, vectorised: one bucket with the reference's three
+    # values, the third repeated, every element an independent draw
+    import random
+    st = b2.Codec(b2.CodecKind.uniform8, b2.Rounding.stochastic)
+    draws = 200_000
+    x = np.full(draws + 2, 0.3777, np.float32)
+    x[0], x[1] = 0.0, 1.0
+    rng = random.Random(11)
+    w1 = st.encode(dev(x), rng)
+    y = st.decode(w1, x.size).cpu().numpy().astype(np.float64)
+    assert y[0] == 0.0 and y[1] == 1.0
+    e = y[2:] - 0.3777
+    assert abs(e.mean()) <= 3.0 * np.sqrt(e.var() / draws)
+    codes = w1.cpu().numpy()[8:]
+    q = (np.float32(0.3777) - np.float32(0.0)) * np.float32(255.0)
+    assert set(np.unique(codes[2:]).tolist()) <= {int(np.floor(q)), int(np.floor(q)) + 1}
+    w2 = st.encode(dev(x), rng)  # the generator advanced: different draws
+    assert not torch.equal(w1, w2)
+    w3 = st.encode(dev(x), random.Random(11))  # same stream: same draws
+    assert torch.equal(w1, w3)
+    with pytest.raises(b2.Error):
+        st.encode(dev([1.0, 2.0]), None)  # codec.cpp:68
