@@ -154,6 +154,18 @@ def test_random_vs_oracle(oracle, n):
     assert np.array_equal(bits(got), bits(oracle.decode(lo, hi, want)))
 
 
+def test_decode_random_codes(oracle):
+    # random codes (every level, not just those a gaussian reaches) at a
+    # small and a > 32Mi size, ragged tails: bit-exact vs the oracle
+    rng = np.random.default_rng(5)
+    for n in (16 * 12345 + 15, (32 << 20) + 17):
+        codes = rng.integers(0, 256, n, dtype=np.uint8)
+        lo, hi = np.float32(-1.7), np.float32(2.3)
+        got = U8.decode_soa(torch.as_tensor(codes).cuda(), dev([lo, hi, 0, 0]),
+                            torch.empty(n, device="cuda")).cpu().numpy()
+        assert np.array_equal(bits(got), bits(oracle.decode(lo, hi, codes)))
+
+
 @pytest.mark.parametrize("offset", [1, 2, 3, 5])
 def test_unaligned_views(oracle, offset):
     # misaligned device views take the staging path and stay bit-exact
