@@ -303,17 +303,36 @@ def run_b200(args, rank: int, world: int):
     ep.sync()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e_steps = max(2, min(args.steps, args.e2e_steps))
+    e_steps = max(2, args.steps if args.e2e_steps is None else min(args.steps, args.e2e_steps))
     e0.record(stream)
     e2e_run(e_steps, e0)
     e1.record(stream)
     e1.synchronize()
     ep.sync()
     ems = e0.elapsed_time(e1) / e_steps
+    # the e2e leg's bound: the same two copies (H2D of the input, D2H of a
+    # result) on their streams at once, no collective -- the full-duplex PCIe
+    # ceiling of one step (tests/cpp/pcie_probe.py measures it standalone)
+    barrier()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(stream)
+    h2d_s.wait_event(c0)
+    d2h_s.wait_event(c0)
+    with torch.cuda.stream(h2d_s):
+        xd[0].copy_(host, non_blocking=True)
+    with torch.cuda.stream(d2h_s):
+        host_out[1].copy_(xd[1], non_blocking=True)
+    for s_ in (h2d_s, d2h_s):
+        ev = torch.cuda.Event()
+        ev.record(s_)
+        stream.wait_event(ev)
+    c1.record(stream)
+    c1.synchronize()
+    pcie_ms = c0.elapsed_time(c1)
     if world > 1:
-        t = torch.tensor([ems], device="cuda")
+        t = torch.tensor([ems, pcie_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ems = float(t.item())
+        ems, pcie_ms = float(t[0].item()), float(t[1].item())
 
     trace = None
     if args.trace and prim not in ("codec", "onebit"):
@@ -371,7 +390,9 @@ def run_b200(args, rank: int, world: int):
                    "per_gpu_gbs": round(per_gpu, 2), "l2": f"inputs {4 * n / 1e6:.0f} MB/GPU per step, {nbuf} buffer(s) cycled; > 126 MB L2, no flush"},
         "roofline": roof,
         "e2e": {"value": round(g * 4 * n / (ems / 1e3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
-                "d2h_bytes_per_step": 4 * n, "ms_per_step": round(ems, 3)},
+                "d2h_bytes_per_step": 4 * n, "ms_per_step": round(ems, 3), "steps": e_steps,
+                "bound": "pcie (concurrent pinned H2D + D2H of one step's bytes, measured in this run)",
+                "ceiling": round(g * 4 * n / (pcie_ms / 1e3) / 1e9, 2), "frac": round(pcie_ms / ems, 3)},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
@@ -399,7 +420,8 @@ def main():
     ap.add_argument("--prim", default="c_lp_s", choices=sorted(PRIMS))
     ap.add_argument("--n", "--elements", dest="n", type=int, default=None,
                     help="elements per GPU (default: the BASELINE config size); use --elements under torchrun")
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="steps in the e2e leg (default: --steps; the pipeline fill is amortised over them)")
     ap.add_argument("--cpu-sample", type=int, default=25_000_000)
     ap.add_argument("--ref-sample", type=int, default=25_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
