@@ -267,19 +267,20 @@ def run_b200(args, rank: int, world: int):
 
     # ---------------- end to end through the public API with host buffers
     # Every step copies its input gradients from pinned host memory and reads
-    # its result back; steps are software-pipelined over two device buffers
+    # its result back; steps are software-pipelined over NB device buffers
     # and three streams (H2D of step i+1 and D2H of step i-1 overlap the
     # collective of step i: PCIe is full duplex), as a training loop would.
     host = torch.empty(n, dtype=torch.float32).pin_memory()   # the step's input gradients
     host.copy_(xs[-1].cpu())
-    host_out = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(2)]  # results
-    xd = [torch.empty_like(x) for _ in range(2)]
+    NB = 2  # 3 buffers measured no better (41.4-45.2 vs 45.8 GB/s at g=1)
+    host_out = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(NB)]  # results
+    xd = [torch.empty_like(x) for _ in range(NB)]
     h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
 
     def e2e_run(steps, start_ev):
-        freed = [start_ev, start_ev]  # buffer b may be overwritten after this event
+        freed = [start_ev] * NB  # buffer b may be overwritten after this event
         for i in range(steps):
-            bi = i % 2
+            bi = i % NB
             with torch.cuda.stream(h2d_s):
                 h2d_s.wait_event(freed[bi])
                 xd[bi].copy_(host, non_blocking=True)
@@ -314,21 +315,24 @@ def run_b200(args, rank: int, world: int):
     # result) on their streams at once, no collective -- the full-duplex PCIe
     # ceiling of one step (tests/cpp/pcie_probe.py measures it standalone)
     barrier()
-    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    c0.record(stream)
-    h2d_s.wait_event(c0)
-    d2h_s.wait_event(c0)
-    with torch.cuda.stream(h2d_s):
-        xd[0].copy_(host, non_blocking=True)
-    with torch.cuda.stream(d2h_s):
-        host_out[1].copy_(xd[1], non_blocking=True)
-    for s_ in (h2d_s, d2h_s):
-        ev = torch.cuda.Event()
-        ev.record(s_)
-        stream.wait_event(ev)
-    c1.record(stream)
-    c1.synchronize()
-    pcie_ms = c0.elapsed_time(c1)
+    pcie_ms = float("inf")
+    for _ in range(3):  # best of 3: one 8 ms sample varies by +-10% with host load
+        barrier()  # all ranks copy at once: they share the host's memory and root ports
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        h2d_s.wait_event(c0)
+        d2h_s.wait_event(c0)
+        with torch.cuda.stream(h2d_s):
+            xd[0].copy_(host, non_blocking=True)
+        with torch.cuda.stream(d2h_s):
+            host_out[1].copy_(xd[1], non_blocking=True)
+        for s_ in (h2d_s, d2h_s):
+            ev = torch.cuda.Event()
+            ev.record(s_)
+            stream.wait_event(ev)
+        c1.record(stream)
+        c1.synchronize()
+        pcie_ms = min(pcie_ms, c0.elapsed_time(c1))
     if world > 1:
         t = torch.tensor([ems, pcie_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
