@@ -147,6 +147,25 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def host_info() -> dict:
+    """nproc, CPU model and RAM of the box the CPU legs run on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    mem_gb = None
+    try:
+        mem_gb = round(os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2**30, 1)
+    except (ValueError, OSError):
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "ram_gib": mem_gb}
+
+
 def cpu_reference_gbs(prim_id: int, g: int, n_sample: int, reps: int):
     """The unmodified reference (oracle/_ref) primitive through its SimCluster harness."""
     from oracle import Reference  # test/baseline infrastructure only
@@ -159,7 +178,7 @@ def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
     g = world
-    n_sample = min(args.n, args.ref_sample)
+    n_sample = min(args.n, args.ref_sample or args.n)
     prim_id, label = PRIMS[args.prim][1], PRIMS[args.prim][2]
     if args.prim in ("codec", "onebit"):
         g = 1
@@ -167,17 +186,23 @@ def run_reference(args, rank: int, world: int):
     timed = secs[args.warmup:] or secs
     t = statistics.median(timed)
     value = g * 4 * n_sample / t / 1e9
+    full = n_sample == args.n
+    workload = (f"C_LP_S ByteGrad MinMaxUInt8 allreduce of {args.n} fp32 gradients per GPU (VGG16-sized), g={world}"
+                if args.prim == "c_lp_s" else f"{label} of {args.n} fp32 elements per GPU, g={world}")
     line = {
         "metric": f"effective gradient GB/s for {label}", "value": round(value, 4), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+u8", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": f"{label}, {n_sample} fp32 elements per worker (bounded sample of the "
-                               f"{args.n}-element bucket), {g} worker threads on SimCluster",
-                   "elements": n_sample, "workers": g},
+        "config": {"workload": workload if full else f"{label}, {n_sample} fp32 elements per worker (bounded "
+                               f"sample of the {args.n}-element bucket), {g} worker threads on SimCluster",
+                   "primitive": args.prim, "elements_per_gpu": n_sample, "parallelism": f"dp{world}",
+                   "workers": g, "same_config_as_b200_arm": full},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": g, "kind": "reference",
-                         "sample": f"{n_sample} elements x {g} workers, median of {len(timed)} calls, "
-                                   f"kernels backend {backend}"},
+                         "sample": f"{n_sample} elements x {g} workers (one thread per simulated GPU, the "
+                                   f"reference's threading), median of {len(timed)} calls after {args.warmup} "
+                                   f"warm-up, wall from spawn to join",
+                         "backend": backend, **host_info()},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -401,13 +426,14 @@ def run_b200(args, rank: int, world: int):
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline and prim != "c_fp_s":
-        n_sample = min(n, args.cpu_sample)
-        secs, backend = cpu_reference_gbs(PRIMS[prim][1], 1, n_sample, 3)
-        tc = statistics.median(secs)
+        n_sample = min(n, args.cpu_sample or n)
+        secs, backend = cpu_reference_gbs(PRIMS[prim][1], 1, n_sample, 4)
+        tc = statistics.median(secs[1:])  # 1 warm-up, median of 3
         line["cpu_baseline"] = {"value": round(4 * n_sample / tc / 1e9, 4), "unit": "GB/s", "cores": 1,
                                 "kind": "reference",
-                                "sample": f"{label} g=1 over {n_sample} elements, median of 3 calls "
-                                          f"(reference SimCluster harness, {backend} kernels)"}
+                                "sample": f"{label} g=1 over {n_sample} elements (the full bucket), 1 warm-up "
+                                          f"then median of 3 calls (reference SimCluster harness)",
+                                "backend": backend, **host_info()}
     if rank == 0:
         print(json.dumps(line), flush=True)
         if trace is not None:
@@ -426,8 +452,8 @@ def main():
                     help="elements per GPU (default: the BASELINE config size); use --elements under torchrun")
     ap.add_argument("--e2e-steps", type=int, default=None,
                     help="steps in the e2e leg (default: --steps; the pipeline fill is amortised over them)")
-    ap.add_argument("--cpu-sample", type=int, default=25_000_000)
-    ap.add_argument("--ref-sample", type=int, default=25_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=None, help="elements (default: the full bucket)")
+    ap.add_argument("--ref-sample", type=int, default=None, help="elements per worker (default: the full bucket)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace", action="store_true", help="print per-phase device timestamps (stderr)")
     ap.add_argument("--traffic", type=float, default=None,

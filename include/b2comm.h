@@ -25,7 +25,9 @@
  * Completion is stream-ordered; calls on one bucket must be stream-ordered on
  * each rank (the reference's "one collective per tag at a time",
  * SPEC.md:300).  Peer buffers are library-owned windows exchanged once per
- * (bucket, primitive family, size) through the caller-supplied allgather.
+ * (bucket, primitive family, size) through the caller-supplied allgather;
+ * if any rank fails to allocate one, every rank returns the error (no rank is
+ * left blocking in the exchange).
  */
 #ifndef B2COMM_H
 #define B2COMM_H
@@ -142,8 +144,25 @@ int b2_comm_world(b2_comm_t comm);
 int b2_comm_sync(b2_comm_t comm, void* stream);
 /* Return (and clear) the latched status without synchronizing. */
 int b2_comm_poll(b2_comm_t comm);
-/* Rendezvous timeout for device-side waits, in milliseconds (default 20000). */
+/* Rendezvous timeout for device-side waits, in milliseconds (default 600000).
+ * A wait that times out latches B2_ERR_TIMEOUT and POISONS the window on every
+ * rank (a word in each rank's window header) before this rank publishes
+ * anything else; a late rank that consumes anything published after that
+ * sees the poison at its kernel end and fails too.  From then on the
+ * communicator is poisoned: b2_comm_sync/poll keep returning B2_ERR_TIMEOUT
+ * and every primitive is refused with B2_ERR_TIMEOUT until the communicator
+ * is destroyed and re-created (there is no way to re-agree the epochs). */
 int b2_comm_set_timeout_ms(b2_comm_t comm, uint64_t ms);
+/* 1 when the communicator is poisoned by a rendezvous timeout (see above). */
+int b2_comm_poisoned(b2_comm_t comm);
+/* Collective (every rank, same bucket id): free every window of `bucket`
+ * (all primitive families and sizes).  Drains this GPU, then synchronises the
+ * ranks through the bootstrap allgather before unmapping, so no peer kernel
+ * can still be reading.  Windows are otherwise kept for the communicator's
+ * lifetime (one per (bucket, family, size)). */
+int b2_comm_release_bucket(b2_comm_t comm, uint32_t bucket);
+/* Device bytes held in peer windows by this communicator. */
+size_t b2_comm_window_bytes(b2_comm_t comm);
 /* Number of kernel launches this communicator has issued (evidence counter). */
 uint64_t b2_comm_launches(b2_comm_t comm);
 /* Phase tracing (the multi-GPU stand-in for ncu, which cannot replay kernels

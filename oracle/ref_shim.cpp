@@ -287,8 +287,12 @@ int ref_time_primitive(int prim, int g, std::size_t len, int reps,
     const Codec ob = make_codec(2);
     const Topology ring = make_topo(0, g, 0);
     for (int t = 0; t < reps; ++t) {
-      for (int r = 0; r < g; ++r)
-        synth(xs[static_cast<std::size_t>(r)].data(), len, 2026u + r);
+      {  // untimed: one generator thread per worker (full-size buckets, g up to 8)
+        std::vector<std::thread> gen;
+        for (int r = 0; r < g; ++r)
+          gen.emplace_back([&, r] { synth(xs[static_cast<std::size_t>(r)].data(), len, 2026u + r); });
+        for (auto& th : gen) th.join();
+      }
       const auto t0 = std::chrono::steady_clock::now();
       if (prim == 0 || prim == 5) {  // standalone codec: uniform8 (0) or onebit (5)
         const Codec c = make_codec(prim == 0 ? 1 : 2);

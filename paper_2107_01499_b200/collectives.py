@@ -125,7 +125,7 @@ class B200Endpoint:
     """One worker's handle on the B200 communicator (libb2comm b2_comm_t)."""
 
     def __init__(self, rank: int | None = None, world_size: int | None = None, device: int | None = None,
-                 bootstrap=None, timeout_ms: int = 20000):
+                 bootstrap=None, timeout_ms: int | None = None):
         import torch.distributed as dist
         if rank is None or world_size is None:
             if dist.is_available() and dist.is_initialized():
@@ -146,7 +146,8 @@ class B200Endpoint:
         with torch.cuda.device(self.device):
             check(lib.b2_comm_create(self._world, self._rank, self.device, self._cb, None, C.byref(h)))
         self._h = h
-        check(lib.b2_comm_set_timeout_ms(h, timeout_ms))
+        if timeout_ms is not None:  # default: the library's (b2comm.h, 10 min)
+            check(lib.b2_comm_set_timeout_ms(h, int(timeout_ms)))
 
     def _allgather(self, user, send, nbytes, recv) -> int:
         try:
@@ -187,6 +188,18 @@ class B200Endpoint:
 
     def launches(self) -> int:
         return int(lib.b2_comm_launches(self._h))
+
+    def poisoned(self) -> bool:
+        """True once a rendezvous timed out: every further primitive raises
+        until the endpoint is closed and re-created (b2comm.h)."""
+        return bool(lib.b2_comm_poisoned(self._h))
+
+    def release_bucket(self, bucket: int) -> None:
+        """Collective: free every peer window of `bucket` (b2_comm_release_bucket)."""
+        check(lib.b2_comm_release_bucket(self._h, int(bucket)))
+
+    def window_bytes(self) -> int:
+        return int(lib.b2_comm_window_bytes(self._h))
 
     # -- phase tracing (ncu cannot replay kernels that rendezvous across GPUs)
     TRACE_POINTS = ("start", "p1_first_minmax", "p1_first_push", "p1_done", "p2_ready", "p2_minmax",

@@ -191,27 +191,60 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // Status bits latched into the communicator's mapped status word.
 enum : int { kStatusNonFinite = 1, kStatusTimeout = 2 };
 
-__device__ __forceinline__ void latch(int* status, int bit) {
-  atomicOr_system(status, bit);
+// Failure context of one window (device memory, built by the communicator):
+// the mapped host status word and every rank's poison word (WinHdr::poison).
+// A rendezvous timeout POISONS the window on every rank before this rank
+// publishes anything else: a late peer that passes its (cumulative) waits and
+// consumes data published after the timeout sees the poison at its kernel end
+// (fail_epilogue) and latches B2_ERR_TIMEOUT instead of returning success; the
+// host then refuses every further launch on the communicator (comm.cu).
+struct Fail {
+  int* host;                             // mapped host status word
+  unsigned long long* mine;              // my window's poison word
+  unsigned long long* peer[kMaxRanks];   // every rank's poison word (peer-mapped; [me] == mine)
+  int n;
+};
+
+__device__ __forceinline__ void latch(Fail* f, int bit) {
+  atomicOr_system(f->host, bit);
+  if (bit & kStatusTimeout) {
+    for (int j = 0; j < f->n; ++j)
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(f->peer[j]), "l"(1ull) : "memory");
+    __threadfence_system();  // the poison is visible before anything this rank publishes later
+  }
+}
+__device__ __forceinline__ bool poisoned(const Fail* f) {
+  return *reinterpret_cast<volatile unsigned long long*>(f->mine) != 0ull;
 }
 
 // Spin until *flag >= target (acquire, system scope) or the timeout expires.
-// Returns false on timeout (status latched) so the caller can fall through
-// instead of hanging the GPU.
+// Returns false on timeout (status latched, every rank's window poisoned) so
+// the caller can fall through instead of hanging the GPU; a window that is
+// already poisoned (by this rank or a peer) fails every wait at once.
 __device__ __forceinline__ bool wait_geq(const unsigned long long* flag, unsigned long long target,
-                                         unsigned long long timeout_ns, int* status) {
+                                         unsigned long long timeout_ns, Fail* f) {
   if (ld_acquire_sys(flag) >= target) return true;
   const unsigned long long t0 = globaltimer();
   unsigned ns = 32;
   while (ld_acquire_sys(flag) < target) {
     __nanosleep(ns);
     if (ns < 1024) ns <<= 1;
+    if (poisoned(f)) {
+      atomicOr_system(f->host, kStatusTimeout);
+      return false;
+    }
     if (globaltimer() - t0 > timeout_ns) {
-      latch(status, kStatusTimeout);
+      latch(f, kStatusTimeout);
       return false;
     }
   }
   return true;
+}
+
+// Kernel epilogue (one thread per CTA, after the CTA's last wait): a poison
+// set by a peer that timed out in this call turns the call into an error.
+__device__ __forceinline__ void fail_epilogue(Fail* f) {
+  if (poisoned(f)) atomicOr_system(f->host, kStatusTimeout);
 }
 
 // --------------------------------------------------- work decomposition

@@ -17,7 +17,7 @@ struct WinHdr {
   unsigned long long dready[2]; // decentral: epoch of my published buffer, per parity
   unsigned long long dreads[2]; // decentral: #neighbour reads of my buffer completed (cumulative)
   unsigned long long arrive_e;  // central uint8: #ranks whose unaligned head/tail codes for me landed
-  unsigned long long pad0;
+  unsigned long long poison;    // nonzero: a rank timed out on this window (b2_device.cuh Fail); never cleared
   float2 hdr1[kMaxRanks];       // central uint8: (min,max) of my chunk as encoded by rank j
   float2 hdr2;                  // central uint8: (min,max) of my phase-2 payload
   float2 dhdr[2];               // decentral uint8: (min,max) of my bucket, per parity
@@ -62,7 +62,7 @@ struct CentralArgs {
   unsigned* gridbar;            // local workspace [2]: consumer grid barrier
   unsigned long long* sched;    // local workspace [kSchedPasses]: dynamic tile counters, or null
   unsigned* sched_end;          // local workspace: CTAs finished (counter reset)
-  int* status;                  // mapped host status word
+  Fail* status;                 // failure context of this window (b2_device.cuh)
   unsigned long long timeout_ns;
   unsigned long long* trace;    // [grid * kTraceSlots] globaltimer stamps, or null
 };
@@ -84,7 +84,7 @@ struct OnebitArgs {
   uint8_t* win[kMaxRanks];
   size_t off_recv1, slot_stride, off_out2;
   double* partials;             // local workspace [(g + 1) * grid] fp64 |y| partial sums
-  int* status;
+  Fail* status;
   unsigned long long timeout_ns;
 };
 
@@ -105,7 +105,7 @@ struct OnebitDecentArgs {
   uint8_t* win[kMaxRanks];
   size_t off_dbuf;              // offset of dbuf[parity]
   double* partials;             // local workspace [grid]
-  int* status;
+  Fail* status;
   unsigned long long timeout_ns;
 };
 
@@ -130,7 +130,7 @@ struct DecentArgs {
   unsigned* gridbar;
   unsigned long long* sched;
   unsigned* sched_end;
-  int* status;
+  Fail* status;
   unsigned long long timeout_ns;
   unsigned long long* trace;
 };

@@ -14,7 +14,9 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstring>
+#include <string>
 #include <map>
 #include <mutex>
 #include <numeric>
@@ -52,9 +54,11 @@ struct Window {
   float2* partials = nullptr;
   unsigned* cta_done = nullptr;
   unsigned long long* sched = nullptr;  // [kSchedPasses] tile counters + end counter
+  Fail* fail = nullptr;                 // device: status word + every rank's poison word
 };
 
 struct Blob {  // what each rank publishes about one window
+  int ok;   // 0: this rank's allocation failed -- every rank fails the window together
   int pid;
   int device;
   int grid;  // persistent grid size: per-CTA arrival counts must agree across ranks
@@ -74,7 +78,8 @@ struct b2_comm {
   std::map<std::tuple<uint32_t, int, size_t, int>, Window*> wins;
   int* status_h = nullptr;  // mapped pinned host word
   int* status_d = nullptr;
-  unsigned long long timeout_ns = 20000ull * 1000000ull;
+  unsigned long long timeout_ns = 600000ull * 1000000ull;  // 10 min; tests and benches set their own
+  bool poisoned = false;  // a rendezvous timed out: every further launch is refused
   unsigned long long launches = 0;
   unsigned long long* trace = nullptr;  // device [max grid * kTraceSlots], when enabled
   int trace_grid = 0;
@@ -103,6 +108,7 @@ void free_window(b2_comm* c, Window* w) {
   if (w->partials) cudaFree(w->partials);
   if (w->cta_done) cudaFree(w->cta_done);
   if (w->sched) cudaFree(w->sched);
+  if (w->fail) cudaFree(w->fail);
   delete w;
   (void)c;
 }
@@ -162,39 +168,44 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
     free_window(c, w);
     return rc;
   };
-  if (cudaMalloc(&w->local, w->bytes) != cudaSuccess ||
-      cudaMemset(w->local, 0, (family == kDecentral || family == kOnebitD) ? w->off_dbuf[0] : w->off_recv1) != cudaSuccess ||
-      cudaMalloc(&w->partials, sizeof(float2) * (kMaxRanks + 1) * max_persistent_grid()) !=
-          cudaSuccess ||
-      cudaMalloc(&w->cta_done, sizeof(unsigned) * (kMaxRanks + 4)) != cudaSuccess ||
-      cudaMemset(w->cta_done, 0, sizeof(unsigned) * (kMaxRanks + 4)) != cudaSuccess ||
-      cudaMalloc(&w->sched, sizeof(unsigned long long) * (kSchedPasses + 1)) != cudaSuccess ||
-      cudaMemset(w->sched, 0, sizeof(unsigned long long) * (kSchedPasses + 1)) != cudaSuccess) {
-    set_error("window allocation of %zu bytes failed: %s", w->bytes,
-              cudaGetErrorString(cudaGetLastError()));
-    return fail(B2_ERR_CUDA);
-  }
-  if (cudaDeviceSynchronize() != cudaSuccess) {
-    set_error("window init failed: %s", cudaGetErrorString(cudaGetLastError()));
-    return fail(B2_ERR_CUDA);
-  }
+  const bool ok =
+      cudaMalloc(&w->local, w->bytes) == cudaSuccess &&
+      cudaMemset(w->local, 0, (family == kDecentral || family == kOnebitD) ? w->off_dbuf[0] : w->off_recv1) ==
+          cudaSuccess &&
+      cudaMalloc(&w->partials, sizeof(float2) * (kMaxRanks + 1) * max_persistent_grid()) == cudaSuccess &&
+      cudaMalloc(&w->cta_done, sizeof(unsigned) * (kMaxRanks + 4)) == cudaSuccess &&
+      cudaMemset(w->cta_done, 0, sizeof(unsigned) * (kMaxRanks + 4)) == cudaSuccess &&
+      cudaMalloc(&w->sched, sizeof(unsigned long long) * (kSchedPasses + 1)) == cudaSuccess &&
+      cudaMemset(w->sched, 0, sizeof(unsigned long long) * (kSchedPasses + 1)) == cudaSuccess &&
+      cudaMalloc(&w->fail, sizeof(Fail)) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess;
+  std::string why;
+  if (!ok) why = cudaGetErrorString(cudaGetLastError());
   w->peer[c->rank] = w->local;
   if (g > 1) {
+    // every rank takes part in the exchange even when its allocation failed,
+    // so that all ranks fail together instead of the others blocking here
     Blob mine{};
+    mine.ok = ok ? 1 : 0;
     mine.pid = static_cast<int>(getpid());
     mine.device = c->device;
     mine.grid = sm_count();
     mine.ptr = reinterpret_cast<unsigned long long>(w->local);
     mine.bytes = w->bytes;
-    if (cudaIpcGetMemHandle(&mine.handle, w->local) != cudaSuccess) {
-      set_error("cudaIpcGetMemHandle failed: %s", cudaGetErrorString(cudaGetLastError()));
-      return fail(B2_ERR_CUDA);
+    if (ok && cudaIpcGetMemHandle(&mine.handle, w->local) != cudaSuccess) {
+      mine.ok = 0;
+      why = cudaGetErrorString(cudaGetLastError());
     }
     std::vector<Blob> all(g);
     if (!c->allgather || c->allgather(c->user, &mine, sizeof(Blob), all.data()) != 0) {
       set_error("bootstrap allgather failed for bucket %u", bucket);
       return fail(B2_ERR_BOOTSTRAP);
     }
+    for (int j = 0; j < g; ++j)
+      if (!all[j].ok) {
+        set_error("window allocation of %zu bytes failed on rank %d%s%s", w->bytes, j, j == c->rank ? ": " : "",
+                  j == c->rank ? why.c_str() : "");
+        return fail(B2_ERR_CUDA);
+      }
     for (int j = 0; j < g; ++j) {
       if (all[j].bytes != w->bytes) {
         set_error("rank %d window size %llu != %zu: mismatched collective arguments", j,
@@ -228,9 +239,34 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
         w->ipc_opened[j] = true;
       }
     }
+  } else if (!ok) {
+    set_error("window allocation of %zu bytes failed: %s", w->bytes, why.c_str());
+    return fail(B2_ERR_CUDA);
+  }
+  Fail f{};
+  f.host = c->status_d;
+  f.n = g;
+  for (int j = 0; j < g; ++j)
+    f.peer[j] = reinterpret_cast<unsigned long long*>(w->peer[j] + offsetof(WinHdr, poison));
+  f.mine = f.peer[c->rank];
+  if (cudaMemcpy(w->fail, &f, sizeof(Fail), cudaMemcpyHostToDevice) != cudaSuccess) {
+    set_error("window init failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return fail(B2_ERR_CUDA);
   }
   c->wins[key] = w;
   *out = w;
+  return B2_OK;
+}
+
+// A communicator whose device latched a rendezvous timeout is poisoned: the
+// windows' epochs no longer agree across ranks, so every further launch is
+// refused until the communicator is destroyed and re-created.
+int refuse_if_poisoned(b2_comm* c) {
+  if (!c->poisoned && (__atomic_load_n(c->status_h, __ATOMIC_ACQUIRE) & kStatusTimeout)) c->poisoned = true;
+  if (c->poisoned) {
+    set_error("communicator poisoned by an earlier rendezvous timeout: destroy and re-create it");
+    return B2_ERR_TIMEOUT;
+  }
   return B2_OK;
 }
 
@@ -382,6 +418,48 @@ int b2_comm_read_trace(b2_comm_t c, uint64_t* out, int max_ctas, int* n_slots) {
   return B2_OK;
 }
 
+int b2_comm_poisoned(b2_comm_t c) {
+  if (!c) return 0;
+  if (__atomic_load_n(c->status_h, __ATOMIC_ACQUIRE) & kStatusTimeout) c->poisoned = true;
+  return c->poisoned ? 1 : 0;
+}
+
+// Collective (every rank, same bucket): free the bucket's windows once no
+// rank's kernels can still touch them -- each rank drains its device, then a
+// barrier through the bootstrap allgather, then IPC mappings are closed and
+// the memory freed.
+int b2_comm_release_bucket(b2_comm_t c, uint32_t bucket) {
+  B2_REQUIRE(c, "null communicator");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  B2_CUDA_TRY(cudaDeviceSynchronize());
+  if (c->world > 1) {
+    std::vector<int> all(c->world);
+    int mine = 1;
+    if (!c->allgather || c->allgather(c->user, &mine, sizeof(int), all.data()) != 0) {
+      set_error("bootstrap allgather failed while releasing bucket %u", bucket);
+      return B2_ERR_BOOTSTRAP;
+    }
+  }
+  for (auto it = c->wins.begin(); it != c->wins.end();) {
+    if (std::get<0>(it->first) == bucket) {
+      free_window(c, it->second);
+      it = c->wins.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  return B2_OK;
+}
+
+size_t b2_comm_window_bytes(b2_comm_t c) {
+  if (!c) return 0;
+  std::lock_guard<std::mutex> lk(c->mu);
+  size_t b = 0;
+  for (auto& kv : c->wins) b += kv.second->bytes;
+  return b;
+}
+
 int b2_comm_rank(b2_comm_t c) { return c ? c->rank : -1; }
 int b2_comm_world(b2_comm_t c) { return c ? c->world : -1; }
 uint64_t b2_comm_launches(b2_comm_t c) { return c ? c->launches : 0; }
@@ -395,8 +473,9 @@ int b2_comm_set_timeout_ms(b2_comm_t c, uint64_t ms) {
 int b2_comm_poll(b2_comm_t c) {
   B2_REQUIRE(c, "null communicator");
   const int s = __atomic_exchange_n(c->status_h, 0, __ATOMIC_SEQ_CST);
-  if (s & kStatusTimeout) {
-    set_error("rendezvous timeout: a peer did not arrive");
+  if ((s & kStatusTimeout) || c->poisoned) {  // sticky: see refuse_if_poisoned
+    c->poisoned = true;
+    set_error("rendezvous timeout: a peer did not arrive (the communicator is poisoned)");
     return B2_ERR_TIMEOUT;
   }
   if (s & kStatusNonFinite) {
@@ -435,6 +514,7 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   }
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard dg(c->device);
+  if ((rc = refuse_if_poisoned(c))) return rc;
   Window* w = nullptr;
   rc = get_window(c, bucket, kCentral, n, codec == B2_CODEC_UNIFORM8 ? 1 : 4, &w);
   if (rc) return rc;
@@ -457,7 +537,7 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   a.gridbar = w->cta_done + kMaxRanks + 2;
   a.sched = static_sched() ? nullptr : w->sched;
   a.sched_end = reinterpret_cast<unsigned*>(w->sched + kSchedPasses);
-  a.status = c->status_d;
+  a.status = w->fail;
   a.timeout_ns = c->timeout_ns;
   a.trace = c->trace;
   rc = launch_central(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity, delta != nullptr,
@@ -481,6 +561,7 @@ static int onebit_central(b2_comm_t c, float* x, size_t n, float* delta, size_t 
   }
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard dg(c->device);
+  if ((rc = refuse_if_poisoned(c))) return rc;
   Window* w = nullptr;
   rc = get_window(c, bucket, kOnebit, n, 1, &w);
   if (rc) return rc;
@@ -497,7 +578,7 @@ static int onebit_central(b2_comm_t c, float* x, size_t n, float* delta, size_t 
   a.slot_stride = w->slot_stride;
   a.off_out2 = w->off_out2;
   a.partials = reinterpret_cast<double*>(w->partials);
-  a.status = c->status_d;
+  a.status = w->fail;
   a.timeout_ns = c->timeout_ns;
   rc = launch_onebit_central(a, delta != nullptr, static_cast<cudaStream_t>(stream));
   if (rc == B2_OK) ++c->launches;
@@ -533,6 +614,7 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
   B2_REQUIRE(has_self, "neighbour list must include the calling rank");
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard dg(c->device);
+  if ((rc = refuse_if_poisoned(c))) return rc;
   Window* w = nullptr;
   if (codec == B2_CODEC_ONEBIT) {  // d_lp_s with Codec{onebit}: pull design, onebit_coll.cu
     rc = get_window(c, bucket, kOnebitD, n, 1, &w);
@@ -550,7 +632,7 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
     for (int j = 0; j < c->world; ++j) a.win[j] = w->peer[j];
     a.off_dbuf = w->off_dbuf[a.parity];
     a.partials = reinterpret_cast<double*>(w->partials);
-    a.status = c->status_d;
+    a.status = w->fail;
     a.timeout_ns = c->timeout_ns;
     rc = launch_onebit_decent(a, static_cast<cudaStream_t>(stream));
     if (rc == B2_OK) {
@@ -583,7 +665,7 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
   a.gridbar = w->cta_done + kMaxRanks + 2;
   a.sched = static_sched() ? nullptr : w->sched;
   a.sched_end = reinterpret_cast<unsigned*>(w->sched + kSchedPasses);
-  a.status = c->status_d;
+  a.status = w->fail;
   a.timeout_ns = c->timeout_ns;
   a.trace = c->trace;
   rc = launch_decent(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity,

@@ -380,6 +380,8 @@ __global__ void __launch_bounds__(kThr) onebit_central_kernel(OnebitArgs a) {
       }
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) fail_epilogue(a.status);
 }
 
 
@@ -465,6 +467,7 @@ __global__ void __launch_bounds__(kThr) onebit_decent_kernel(OnebitDecentArgs a)
   grid.sync();
   if (blockIdx.x == 0 && threadIdx.x < NB && a.nbrs[threadIdx.x] != a.me)
     red_release_sys_add(&reinterpret_cast<WinHdr*>(a.win[a.nbrs[threadIdx.x]])->dreads[p], 1ull);
+  if (threadIdx.x == 0) fail_epilogue(a.status);
 }
 }  // namespace
 

@@ -255,10 +255,10 @@ struct Ring {
   int npass = 0;                        // passes streamed so far (identical in every role)
   unsigned long long wt[4] = {0, 0, 0, 0};  // traced waits (ns): slot/gate, empty/retire, full
   bool timed = false;                   // accumulate wt[] (tracing only)
-  int* status;
+  Fail* status;
   unsigned long long timeout_ns;
 
-  __device__ void init(uint8_t* smem, int* st, unsigned long long to, unsigned long long* sched_ctrs = nullptr) {
+  __device__ void init(uint8_t* smem, Fail* st, unsigned long long to, unsigned long long* sched_ctrs = nullptr) {
     sched = sched_ctrs;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     // pipe barriers: [full, empty] x (kStages + kSplitStagesA + (kStages - kSplitStagesA)) = 4 kStages
@@ -651,6 +651,7 @@ struct Ring {
   // counters for the next launch on this workspace.
   __device__ void finish(unsigned* end_ctr) {
     __syncthreads();
+    if (threadIdx.x == 0) fail_epilogue(status);
     if (sched && threadIdx.x == 0) {
       __threadfence();
       if (atomicAdd(end_ctr, 1u) == gridDim.x - 1) {

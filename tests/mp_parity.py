@@ -72,14 +72,128 @@ class Checker:
             self.fail.append(f"rank{self.rank} {name}: max err {err} > {tol}")
 
 
+def replicas_identical(ck, name, t, g, rank):
+    """Every rank must hold the identical bucket after a C_* primitive."""
+    digest = hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest()
+    allv = [None] * g
+    dist.all_gather_object(allv, digest)
+    if len(set(allv)) != 1:
+        ck.fail.append(f"rank{rank} {name}: replicas differ {allv}")
+    else:
+        ck.passed += 1
+
+
+def run_large(ep, ck, orc, rank, g):
+    """BASELINE.json's configs at their full sizes, every rank checked against
+    the oracle.  C_*: the owner checks its own partition against the
+    partition-local restatement and all ranks compare digests
+    of their whole outputs (so every replica of every partition is checked);
+    where the whole problem fits (25M) the full oracle runs instead.  D_*:
+    the per-rank restatement over the rank's neighbours' inputs.  Inputs are
+    splitmix64 synthetic gradients generated identically on the device and
+    on the host (orc_synth == b2_fill_synthetic)."""
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def fill(n, seed):
+        t = torch.empty(n, device="cuda")
+        b2._lib.check(b2.lib.b2_fill_synthetic(t.data_ptr(), n, seed, 0, stream))
+        return t
+
+    bucket = 5000
+    # -- config 2: C_FP_S, 25M fp32, full oracle (fp64 ascending rank fold)
+    n = 25_000_000
+    xs = [orc.synth(n, 2026 + r) for r in range(g)]
+    want = [x.copy() for x in xs]
+    orc.c_fp_s(want)
+    for it in range(2):
+        t = torch.as_tensor(xs[rank]).cuda()
+        b2.c_fp_s(ep, 0.0, t, bucket=bucket)
+        ck.eq(f"large c_fp_s n={n} it={it}", t.cpu().numpy(), want[rank])
+    del want
+    # -- config 4: D_FP_S ring averaging, 25M, two chained rounds
+    topo = b2.Topology(b2.TopologyKind.ring, g, 0)
+    nb = topo.neighbors(rank, 0)
+    t = torch.as_tensor(xs[rank]).cuda()
+    cur = xs
+    for rnd in range(2):
+        b2.d_fp_s(ep, 0.0, t, topo, rnd, b2.ReduceMode.average, bucket=bucket + 1)
+        cur = [orc.d_fp_s_rank([cur[j] for j in topo.neighbors(r, rnd)], 1) for r in range(g)]
+        ck.eq(f"large d_fp_s ring n={n} round={rnd}", t.cpu().numpy(), cur[rank])
+    del cur, xs
+
+    # -- config 3: C_LP_S 100M uint8 (stateless, two calls), onebit, uint8 + error feedback
+    n = 100_000_000
+    lo, sz = b2.partition_range(n, g, rank)
+    for it in range(2):
+        seed0 = 2026 + 100 * it
+        t = fill(n, seed0 + rank)
+        b2.c_lp_s(ep, 0.0, t, U8, None, bucket=bucket + 2)
+        acc = np.zeros(sz, np.float64)
+        for r in range(g):  # partition-local restatement: D(Q2((float) sum_j D(Q1(x_j|k))))
+            l1, h1, c1 = orc.encode(orc.synth(sz, seed0 + r, lo))
+            acc += orc.decode(l1, h1, c1).astype(np.float64)
+        l2, h2, c2 = orc.encode(acc.astype(np.float32))
+        ck.eq(f"large c_lp_s u8 n={n} it={it} own partition", t[lo:lo + sz].cpu().numpy(), orc.decode(l2, h2, c2))
+        replicas_identical(ck, f"large c_lp_s u8 n={n} it={it}", t, g, rank)
+    t = fill(n, 2026 + rank)
+    b2.c_lp_s(ep, 0.0, t, OB, None, bucket=bucket + 3)
+    acc = np.zeros(sz, np.float64)
+    for r in range(g):
+        p = orc.synth(sz, 2026 + r, lo)
+        acc += orc.onebit_decode_wire(orc.onebit_encode_wire(p), sz).astype(np.float64)
+    s = acc.astype(np.float32)
+    ck.close(f"large c_lp_s onebit n={n} own partition", t[lo:lo + sz].cpu().numpy(),
+             orc.onebit_decode_wire(orc.onebit_encode_wire(s), sz))
+    replicas_identical(ck, f"large c_lp_s onebit n={n}", t, g, rank)
+    del acc, s
+    # uint8 + ErrorState over 3 rounds (acceptance c4 semantics, collectives.cpp:109-151):
+    # my whole delta, my epsilon and my own partition of x' are checked
+    es = b2.ErrorState(n, sz)
+    parts = [(b2.partition_range(n, g, k)) for k in range(g)]
+    my_delta = np.zeros(n, np.float32)               # delta of this rank, whole bucket
+    d_mine = [np.zeros(sz, np.float32) for _ in range(g)]  # delta_j over MY partition, every j
+    eps = np.zeros(sz, np.float32)
+    for rnd in range(3):
+        seed0 = 4040 + 100 * rnd
+        t = fill(n, seed0 + rank)
+        b2.c_lp_s(ep, 0.0, t, U8, es, bucket=bucket + 4)
+        for k, (lk, nk) in enumerate(parts):  # my delta: chunk by chunk, codec.cpp:125-137
+            orc.compensate_encode(orc.synth(nk, seed0 + rank, lk), my_delta[lk:lk + nk])
+        acc = np.zeros(sz, np.float64)
+        for r in range(g):
+            _, _, _, dec = orc.compensate_encode(orc.synth(sz, seed0 + r, lo), d_mine[r])
+            acc += dec[:sz].astype(np.float64)
+        _, _, _, d2 = orc.compensate_encode(acc.astype(np.float32), eps)
+        ck.eq(f"large c_lp_s u8+EC n={n} round={rnd} own partition", t[lo:lo + sz].cpu().numpy(), d2[:sz])
+        ck.eq(f"large c_lp_s u8+EC n={n} round={rnd} delta", es.delta.cpu().numpy(), my_delta)
+        ck.eq(f"large c_lp_s u8+EC n={n} round={rnd} epsilon", es.epsilon.cpu().numpy(), eps)
+        replicas_identical(ck, f"large c_lp_s u8+EC n={n} round={rnd}", t, g, rank)
+    del es, my_delta, d_mine, eps, acc, t
+    torch.cuda.empty_cache()
+
+    # -- config 5: D_LP_S ring averaging, bucket sweep 1M .. 340M (per-rank restatement)
+    for i, n in enumerate((1_000_000, 25_000_000, 100_000_000, 340_000_000)):
+        t = fill(n, 6060 + rank)
+        b2.d_lp_s(ep, 0.0, t, topo, 0, U8, b2.ReduceMode.average, bucket=bucket + 10 + i)
+        want = orc.d_lp_s_rank([orc.synth(n, 6060 + j) for j in nb], 1, 1)
+        ck.eq(f"large d_lp_s ring n={n}", t.cpu().numpy(), want)
+        del t, want
+        ep.release_bucket(bucket + 10 + i)
+        torch.cuda.empty_cache()
+
+
 def run(args):
     rank, world = dist.get_rank(), dist.get_world_size()
     dev = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(dev)
     orc = Oracle()
-    ep = b2.B200Endpoint(rank, world, dev)
+    ep = b2.B200Endpoint(rank, world, dev, timeout_ms=120_000)
     ck = Checker(rank)
     g = world
+
+    if args.large:
+        run_large(ep, ck, orc, rank, g)
+        return ck, ep.launches()
 
     sizes = [1, 3, 5, 37, 1000, 4097, 65536 + 7, 1_000_003]
     if not args.quick:
@@ -322,54 +436,15 @@ def run(args):
             orc.c_lp_s(xs_b, codec=1)
             ck.eq(f"engine it={it} bucket {b.id} layers {b.layers}", eng.arenas[b.id].cpu().numpy(), xs_b[rank])
 
-    # ---- large: owner-partition restatement + identical-replica digest
-    if args.large:
-        for n in (100_000_000,):
-            bucket += 10
-            t = torch.empty(n, device="cuda")
-            b2.lib.b2_fill_synthetic(t.data_ptr(), n, 2026 + rank, 0, torch.cuda.current_stream().cuda_stream)
-            b2.c_lp_s(ep, 0.0, t, U8, None, bucket=bucket)
-            lo, sz = b2.partition_range(n, g, rank)
-            parts = [orc.synth(sz, 2026 + r, lo) for r in range(g)]
-            # partition-local restatement: D(Q2((float) sum_j D(Q1(x_j|k))))
-            acc = np.zeros(sz, np.float64)
-            for p in parts:
-                l1, h1, c1 = orc.encode(p)
-                acc += orc.decode(l1, h1, c1).astype(np.float64)
-            s = acc.astype(np.float32)
-            l2, h2, c2 = orc.encode(s)
-            ck.eq(f"c_lp_s n={n} own partition", t[lo:lo + sz].cpu().numpy(), orc.decode(l2, h2, c2))
-            digest = hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest()
-            allv = [None] * g
-            dist.all_gather_object(allv, digest)
-            if len(set(allv)) != 1:
-                ck.fail.append(f"rank{rank} c_lp_s n={n}: replicas differ {allv}")
-            else:
-                ck.passed += 1
-            # the same bucket through C_LP_S onebit: own partition vs the restatement, replicas identical
-            b2.lib.b2_fill_synthetic(t.data_ptr(), n, 2026 + rank, 0, torch.cuda.current_stream().cuda_stream)
-            b2.c_lp_s(ep, 0.0, t, OB, None, bucket=bucket + 1)
-            acc = np.zeros(sz, np.float64)
-            for p in parts:
-                acc += orc.onebit_decode_wire(orc.onebit_encode_wire(p), sz).astype(np.float64)
-            s = acc.astype(np.float32)
-            ck.close(f"c_lp_s onebit n={n} own partition", t[lo:lo + sz].cpu().numpy(),
-                     orc.onebit_decode_wire(orc.onebit_encode_wire(s), sz))
-            digest = hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest()
-            allv = [None] * g
-            dist.all_gather_object(allv, digest)
-            if len(set(allv)) != 1:
-                ck.fail.append(f"rank{rank} c_lp_s onebit n={n}: replicas differ {allv}")
-            else:
-                ck.passed += 1
-
     return ck, ep.launches()
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
-    ap.add_argument("--large", action="store_true")
+    ap.add_argument("--large", action="store_true",
+                    help="only BASELINE.json's configs at full size (25M C_FP_S / D_FP_S, 100M C_LP_S "
+                         "uint8 / onebit / EC, D_LP_S 1M-340M)")
     args = ap.parse_args()
     dist.init_process_group("gloo")
     t0 = time.time()

@@ -41,6 +41,32 @@ def test_c_lp_s_g1(ep, oracle, n):
     assert np.array_equal(bits(t.cpu().numpy()), bits(want))
 
 
+def test_c_lp_s_g1_headline_100m(ep, oracle):
+    """The headline bucket (BASELINE.json config 3, 100M fp32) at g = 1, bit-exact,
+    stateless and with error feedback (two rounds, state carried)."""
+    n = 100_000_000
+    stream = torch.cuda.current_stream().cuda_stream
+    t = torch.empty(n, device="cuda")
+    b2._lib.check(b2.lib.b2_fill_synthetic(t.data_ptr(), n, 2026, 0, stream))
+    want = oracle.synth(n, 2026)
+    oracle.c_lp_s([want], codec=1)
+    b2.c_lp_s(ep, 0.0, t, U8, None, bucket=100)
+    assert np.array_equal(bits(t.cpu().numpy()), bits(want))
+    es = b2.ErrorState(n, n)
+    d_or, e_or = [np.zeros(n, np.float32)], [np.zeros(n, np.float32)]
+    for r in range(2):
+        b2._lib.check(b2.lib.b2_fill_synthetic(t.data_ptr(), n, 3030 + r, 0, stream))
+        want = oracle.synth(n, 3030 + r)
+        oracle.c_lp_s([want], codec=1, deltas=d_or, eps=e_or)
+        b2.c_lp_s(ep, 0.0, t, U8, es, bucket=101)
+        assert np.array_equal(bits(t.cpu().numpy()), bits(want)), r
+        assert np.array_equal(bits(es.delta.cpu().numpy()), bits(d_or[0])), r
+        assert np.array_equal(bits(es.epsilon.cpu().numpy()), bits(e_or[0])), r
+    del t, es
+    ep.release_bucket(100)
+    ep.release_bucket(101)
+
+
 def test_c_lp_s_g1_identity_and_ec(ep, oracle):
     n = 1001
     x = oracle.synth(n, 7)
