@@ -291,54 +291,47 @@ def run_b200(args, rank: int, world: int):
     barrier()
 
     # ---------------- end to end through the public API with host buffers
-    # Every step copies its input gradients from pinned host memory and reads
-    # its result back; steps are software-pipelined over NB device buffers
-    # and three streams (H2D of step i+1 and D2H of step i-1 overlap the
-    # collective of step i: PCIe is full duplex), as a training loop would.
-    host = torch.empty(n, dtype=torch.float32).pin_memory()   # the step's input gradients
-    host.copy_(xs[-1].cpu())
-    NB = 2  # 3 buffers measured no better (41.4-45.2 vs 45.8 GB/s at g=1)
-    host_out = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(NB)]  # results
-    xd = [torch.empty_like(x) for _ in range(NB)]
-    h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+    # Every step hands the API a PINNED host bucket (the caller's gradients);
+    # the library's host path (collectives._HostStaging) uploads it on its own
+    # copy stream, runs the collective and downloads the result back into the
+    # same host buffer on a second copy stream.  With blocking=False the
+    # upload of step i+1 and the download of step i overlap the collective
+    # (PCIe is full duplex), as a training loop issuing buckets would.  Two
+    # host buckets alternate; each step's input is the result the buffer
+    # received two steps before.
+    NB = 2
+    host = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(NB)]
+    for h in host:
+        h.copy_(xs[-1].cpu())
 
-    def e2e_run(steps, start_ev):
-        freed = [start_ev] * NB  # buffer b may be overwritten after this event
-        for i in range(steps):
-            bi = i % NB
-            with torch.cuda.stream(h2d_s):
-                h2d_s.wait_event(freed[bi])
-                xd[bi].copy_(host, non_blocking=True)
-                e_in = torch.cuda.Event()
-                e_in.record(h2d_s)
-            stream.wait_event(e_in)
-            step(xd[bi])
-            e_c = torch.cuda.Event()
-            e_c.record(stream)
-            with torch.cuda.stream(d2h_s):
-                d2h_s.wait_event(e_c)
-                host_out[bi].copy_(xd[bi], non_blocking=True)
-                freed[bi] = torch.cuda.Event()
-                freed[bi].record(d2h_s)
-        for ev in freed:
-            stream.wait_event(ev)
+    def e2e_step(i):
+        hb = host[i % NB]
+        if prim in ("codec", "onebit"):  # the standalone codec has no host-bucket API: stage by hand
+            xd = ep.__dict__.setdefault("_e2e_dev", torch.empty_like(x))
+            xd.copy_(hb, non_blocking=True)
+            step(xd)
+            hb.copy_(xd, non_blocking=True)
+        else:
+            step(hb)
 
-    w0 = torch.cuda.Event()
-    w0.record(stream)
-    e2e_run(max(2, args.warmup // 2), w0)
+    for i in range(max(2, args.warmup // 2)):
+        e2e_step(i)
     ep.sync()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_steps = max(2, args.steps if args.e2e_steps is None else min(args.steps, args.e2e_steps))
     e0.record(stream)
-    e2e_run(e_steps, e0)
+    for i in range(e_steps):
+        e2e_step(i)
+    ep.join(stream)  # the last downloads are part of the timed region
     e1.record(stream)
     e1.synchronize()
     ep.sync()
     ems = e0.elapsed_time(e1) / e_steps
-    # the e2e leg's bound: the same two copies (H2D of the input, D2H of a
-    # result) on their streams at once, no collective -- the full-duplex PCIe
-    # ceiling of one step (tests/cpp/pcie_probe.py measures it standalone)
+    # the e2e leg's bound: one step's H2D and D2H on two streams at once, no
+    # collective -- the full-duplex PCIe ceiling (tests/cpp/pcie_probe.py)
+    h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+    xd = [torch.empty_like(x) for _ in range(2)]
     barrier()
     pcie_ms = float("inf")
     for _ in range(3):  # best of 3: one 8 ms sample varies by +-10% with host load
@@ -348,9 +341,9 @@ def run_b200(args, rank: int, world: int):
         h2d_s.wait_event(c0)
         d2h_s.wait_event(c0)
         with torch.cuda.stream(h2d_s):
-            xd[0].copy_(host, non_blocking=True)
+            xd[0].copy_(host[0], non_blocking=True)
         with torch.cuda.stream(d2h_s):
-            host_out[1].copy_(xd[1], non_blocking=True)
+            host[1].copy_(xd[1], non_blocking=True)
         for s_ in (h2d_s, d2h_s):
             ev = torch.cuda.Event()
             ev.record(s_)
@@ -358,6 +351,7 @@ def run_b200(args, rank: int, world: int):
         c1.record(stream)
         c1.synchronize()
         pcie_ms = min(pcie_ms, c0.elapsed_time(c1))
+    del xd
     if world > 1:
         t = torch.tensor([ems, pcie_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -421,6 +415,9 @@ def run_b200(args, rank: int, world: int):
         "e2e": {"value": round(g * 4 * n / (ems / 1e3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
                 "d2h_bytes_per_step": 4 * n, "ms_per_step": round(ems, 3), "steps": e_steps,
                 "bound": "pcie (concurrent pinned H2D + D2H of one step's bytes, measured in this run)",
+                "path": ("b2.c_lp_s / c_fp_s / d_*(ep, 0.0, pinned_host_bucket, ..., blocking=False): the library's "
+                         "own host staging (cached device ring, copy streams), ep.sync() after the last step"
+                         if prim not in ("codec", "onebit") else "hand-staged: the standalone codec has no host API"),
                 "ceiling": round(g * 4 * n / (pcie_ms / 1e3) / 1e9, 2), "frac": round(pcie_ms / ems, 3)},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),

@@ -81,7 +81,9 @@ def build_host(force: bool = False) -> str | None:
     """C++ host layer mirroring rcomm's API over the C ABI."""
     if not os.path.isdir(HOST):
         return None
-    srcs = [p for p in _deps(HOST, (".cpp",))]
+    # rcomm_link.cpp is the link-time drop-in built against the REFERENCE's
+    # headers (build_dropin), not part of this library
+    srcs = [p for p in _deps(HOST, (".cpp",)) if not p.endswith("rcomm_link.cpp")]
     if not srcs:
         return None
     deps = srcs + _deps(os.path.join(INCLUDE, "rcomm_b200"), (".hpp",)) + [LIB]
@@ -122,6 +124,68 @@ def build_host_test(force: bool = False) -> str | None:
         raise RuntimeError("g++ failed on the host-layer test")
     os.replace(HOST_TEST_BIN + ".tmp", HOST_TEST_BIN)
     return HOST_TEST_BIN
+
+
+REF_PROJ = "/root/reference/proj"
+DROPIN_SRC = os.path.join(REPO, "tests", "cpp", "algo_dropin.cpp")
+DROPIN_REF_BIN = os.path.join(REPO, "tests", "cpp", "algo_dropin_ref")
+DROPIN_B200_BIN = os.path.join(REPO, "tests", "cpp", "algo_dropin_b200")
+
+
+def build_dropin(force: bool = False) -> tuple | None:
+    """The reference's own algorithms.cpp (UNMODIFIED, compiled in place from
+    /root/reference) linked twice: with its collectives.cpp on SimCluster
+    (algo_dropin_ref) and with host/rcomm_link.cpp -- the B200 primitives
+    behind the reference's API -- instead (algo_dropin_b200).  Needs the
+    reference tree, so it is built here; the binaries travel to the GPU box
+    with the snapshot.  Reference sources are never copied into the repo."""
+    src = os.path.join(REF_PROJ, "src")
+    if not (os.path.isdir(src) and os.path.exists(DROPIN_SRC) and os.path.exists(LIB)):
+        return None
+    link_cpp = os.path.join(HOST, "rcomm_link.cpp")
+    common = ["algorithms.cpp", "kernels.cpp", "kernels_avx2.cpp", "tensor.cpp", "codec.cpp"]
+    ref_only = ["collectives.cpp", "sim_transport.cpp"]
+    deps = [DROPIN_SRC, link_cpp, LIB, os.path.join(INCLUDE, "rcomm_b200", "rcomm_link.hpp")] + \
+        [os.path.join(src, f) for f in common + ref_only]
+    if not force and not _stale(DROPIN_REF_BIN, deps) and not _stale(DROPIN_B200_BIN, deps):
+        return DROPIN_REF_BIN, DROPIN_B200_BIN
+    objdir = os.path.join(REPO, "tests", "cpp", "dropin_obj")
+    os.makedirs(objdir, exist_ok=True)
+    flags = ["g++", "-std=c++20", "-O2", "-g", "-I", os.path.join(REF_PROJ, "include")]  # CMakeLists.txt:3,9
+
+    def obj(path, extra=()):
+        o = os.path.join(objdir, os.path.basename(path).replace(".cpp", ".o"))
+        if force or _stale(o, [path]):
+            r = subprocess.run([*flags, *extra, "-c", path, "-o", o], capture_output=True, text=True)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"g++ failed on {path}")
+        return o
+
+    objs = [obj(os.path.join(src, f), ["-mavx2"] if f == "kernels_avx2.cpp" else []) for f in common]
+    cuda = ["-I", INCLUDE, "-I", "/usr/local/cuda/include"]
+    link_o = os.path.join(objdir, "rcomm_link.o")
+    drv_b200 = os.path.join(objdir, "algo_dropin_b200.o")
+    drv_ref = os.path.join(objdir, "algo_dropin_ref.o")
+    for cmd in ([*flags, *cuda, "-c", link_cpp, "-o", link_o],
+                [*flags, *cuda, "-c", DROPIN_SRC, "-o", drv_b200],
+                [*flags, "-DDROPIN_REF", "-c", DROPIN_SRC, "-o", drv_ref]):
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("g++ failed on the drop-in test")
+    ref_objs = [obj(os.path.join(src, f)) for f in ref_only]
+    for out, extra in ((DROPIN_REF_BIN, [drv_ref, *ref_objs]),
+                       (DROPIN_B200_BIN, [drv_b200, link_o, "-L", PKG_DIR, "-lb2comm",
+                                          "-L/usr/local/cuda/lib64", "-lcudart",
+                                          f"-Wl,-rpath,{PKG_DIR}:/usr/local/cuda/lib64",
+                                          "-Wl,-rpath,$ORIGIN/../../paper_2107_01499_b200"])):
+        r = subprocess.run(["g++", "-o", out + ".tmp", *objs, *extra, "-lpthread"], capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"link failed for {out}")
+        os.replace(out + ".tmp", out)
+    return DROPIN_REF_BIN, DROPIN_B200_BIN
 
 
 def build(force: bool = False, verbose: bool = False) -> None:

@@ -248,9 +248,28 @@ class B200Endpoint:
     def stream(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream
 
+    def _staging(self) -> "_HostStaging":
+        st = self.__dict__.get("_stage")
+        if st is None:
+            st = self._stage = _HostStaging(self.device)
+        return st
+
+    def join(self, stream=None) -> None:
+        """Make `stream` (default: current) wait for this endpoint's pending
+        host uploads / downloads (non-blocking host buckets)."""
+        st = self.__dict__.get("_stage")
+        if st is not None:
+            st.join(stream or torch.cuda.current_stream(self.device))
+
     def sync(self) -> None:
-        """Wait for this rank's queued primitives; raise on latched errors."""
+        """Wait for this rank's queued primitives (and host copies); raise on
+        latched errors."""
+        st = self.__dict__.get("_stage")
+        if st is not None and st.pending:
+            st.join(torch.cuda.current_stream(self.device))
         check(lib.b2_comm_sync(self._h, self.stream()))
+        if st is not None:
+            st.host_ev.clear()  # every download has landed
 
     def close(self) -> None:
         if getattr(self, "_h", None):
@@ -269,9 +288,63 @@ class B200Endpoint:
 
 
 # ------------------------------------------------------------ bucket staging
+class _HostStaging:
+    """Per-endpoint staging of HOST buckets (the drop-in path for callers
+    holding gradients in host memory, like the reference's std::vector
+    buckets): device buffers are cached per bucket length (a ring of two, so
+    the upload of one call overlaps the download of the previous one), pinned
+    bounce buffers are cached for pageable inputs, and uploads / downloads run
+    on their own streams -- PCIe is full duplex.  Nothing is allocated or
+    pinned per call once a length has been seen."""
+
+    RING = 2
+
+    def __init__(self, device: int):
+        self.device = device
+        self.h2d = torch.cuda.Stream(device=device)
+        self.d2h = torch.cuda.Stream(device=device)
+        self._dev: dict = {}      # n -> [[tensor, free event | None], ...]
+        self._next: dict = {}     # n -> next ring slot
+        self._bounce: dict = {}   # n -> pinned host tensor
+        self.host_ev: dict = {}   # host address -> event of the last download into it
+        self.pending = False      # downloads issued since the last join
+
+    def slot(self, n: int):
+        ring = self._dev.get(n)
+        if ring is None:
+            ring = self._dev[n] = [[torch.empty(max(n, 4), dtype=torch.float32,
+                                                device=torch.device("cuda", self.device))[:n], None]
+                                   for _ in range(self.RING)]
+            self._next[n] = 0
+        i = self._next[n]
+        self._next[n] = (i + 1) % self.RING
+        return ring[i]
+
+    def bounce(self, n: int) -> torch.Tensor:
+        b = self._bounce.get(n)
+        if b is None:
+            b = self._bounce[n] = torch.empty(max(n, 4), dtype=torch.float32).pin_memory()[:n]
+        return b
+
+    def join(self, stream) -> None:
+        """`stream` waits for every upload and download issued so far."""
+        stream.wait_stream(self.h2d)
+        stream.wait_stream(self.d2h)
+        self.pending = False
+
+
 class _Bucket:
-    """Resolve x to an aligned contiguous device float32 tensor; write back
-    on exit when a staging copy was needed (host input or misalignment)."""
+    """Resolve x to an aligned contiguous device float32 tensor.
+
+    Device tensors are used in place.  Host buckets go through the
+    endpoint's _HostStaging: a pinned torch tensor is uploaded straight from
+    its memory and the result downloaded straight back into it (with
+    blocking=False both copies are asynchronous and the result is valid after
+    ep.sync()); pageable inputs (numpy, unpinned tensors) go through a cached
+    pinned bounce buffer and are always blocking.  The latched device status
+    is checked BEFORE a blocking call writes anything back, so a failing call
+    (non-finite input, timeout) leaves a host x untouched, as the reference
+    throws from encode before x changes (codec.cpp:24-27)."""
 
     def __init__(self, ep: B200Endpoint, x):
         if (type(x) is torch.Tensor and x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
@@ -285,11 +358,36 @@ class _Bucket:
         if isinstance(x, (FlatTensor, BucketArena)):
             x = x.data()
         self.host = not (isinstance(x, torch.Tensor) and x.is_cuda)
+        self.ep = ep
         if self.host:
-            arr = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, np.float32))
-            self.host_t = arr
-            pinned = arr.to(torch.float32).reshape(-1).pin_memory()
-            self.dev = pinned.to(torch.device("cuda", ep.device), non_blocking=True)
+            if isinstance(x, torch.Tensor):
+                if x.dtype != torch.float32:
+                    raise Error("bucket must be float32")
+                self.host_t = x
+                flat = x.reshape(-1) if x.is_contiguous() else None
+            else:
+                self.host_t = x
+                arr = np.asarray(x)
+                if arr.dtype != np.float32:
+                    raise Error("bucket must be float32")
+                flat = torch.from_numpy(arr).reshape(-1) if arr.flags.c_contiguous else None
+            self.n = int(np.prod(np.shape(x))) if not isinstance(x, torch.Tensor) else x.numel()
+            st = ep._staging()
+            self.pinned = flat is not None and isinstance(x, torch.Tensor) and flat.is_pinned()
+            self.src = flat if self.pinned else st.bounce(self.n)
+            if not self.pinned:
+                self.src.copy_(torch.as_tensor(np.ascontiguousarray(x, np.float32)).reshape(-1)
+                               if flat is None else flat)
+            self.slot = st.slot(self.n)
+            self.dev = self.slot[0]
+            with torch.cuda.stream(st.h2d):
+                if self.slot[1] is not None:
+                    st.h2d.wait_event(self.slot[1])  # the slot's previous download is done
+                prev = st.host_ev.get(self.src.data_ptr())
+                if prev is not None:
+                    st.h2d.wait_event(prev)  # a pending download into this host bucket lands first
+                self.dev.copy_(self.src, non_blocking=True)
+            torch.cuda.current_stream(ep.device).wait_stream(st.h2d)
             self.view = None
         else:
             if x.dtype != torch.float32:
@@ -300,19 +398,33 @@ class _Bucket:
                 self.dev = x.reshape(-1).clone()
             else:
                 self.dev = flat
-        self.n = self.dev.numel()
+            self.n = self.dev.numel()
 
-    def finish(self) -> None:
-        if self.dev is self.view:
+    def finish(self, blocking: bool) -> None:
+        """After the launch on the endpoint's stream."""
+        if not self.host:
+            if self.dev is not self.view and self.dev.data_ptr() != self.view.data_ptr():
+                self.view.copy_(self.dev.view_as(self.view))
             return
-        if self.host:
-            res = self.dev.cpu()
-            if isinstance(self.host_t, torch.Tensor):
-                self.host_t.copy_(res.view_as(self.host_t))
-            else:
-                np.copyto(self.host_t, res.numpy().reshape(np.shape(self.host_t)))
-        elif self.dev is not self.view and self.dev.data_ptr() != self.view.data_ptr():
-            self.view.copy_(self.dev.view_as(self.view))
+        ep = self.ep
+        st = ep._staging()
+        if blocking or not self.pinned:
+            ep.sync()  # raises on a latched error: nothing is written back
+            self.src.copy_(self.dev)  # device -> pinned, synchronous
+            if not self.pinned:
+                if isinstance(self.host_t, torch.Tensor):
+                    self.host_t.copy_(self.src.view_as(self.host_t))
+                else:
+                    np.copyto(self.host_t, self.src.numpy().reshape(np.shape(self.host_t)))
+            return
+        with torch.cuda.stream(st.d2h):
+            st.d2h.wait_stream(torch.cuda.current_stream(ep.device))
+            self.src.copy_(self.dev, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(st.d2h)
+            self.slot[1] = ev
+            st.host_ev[self.src.data_ptr()] = ev
+        st.pending = True
 
 
 def _on_device(ep: B200Endpoint):
@@ -321,9 +433,9 @@ def _on_device(ep: B200Endpoint):
 
 
 def _finish(ep: B200Endpoint, b: _Bucket, blocking: bool) -> None:
-    if blocking or b.host:
+    if blocking and not b.host:
         ep.sync()
-    b.finish()
+    b.finish(blocking)
 
 
 def c_fp_s(ep: B200Endpoint, now: float, x, bucket: int = 0, blocking: bool = True) -> float:

@@ -55,8 +55,8 @@ def scenario(rank, world, dev, prim):
     if rank == world - 1:
         time.sleep(LATE_S)  # far beyond the device timeout
     res["late_call"] = attempt(call)
-    res["poisoned"] = ep.poisoned()
     dist.barrier()
+    res["poisoned"] = ep.poisoned()
     res["next_call"] = attempt(call)  # everybody on time again: still refused
     res["sync"] = attempt(ep.sync)
     ep.close()
@@ -83,7 +83,11 @@ def main():
         out[prim] = r
         if r.get("warm") != "ok":
             bad.append(f"rank{rank} {prim}: warm-up call failed {r}")
-        if r.get("late_call") == "ok":
+        late = world - 1
+        # D_LP_S over the ring: a rank that is not a neighbour of the late rank
+        # never waits for it, and its (correct) result may stand
+        depends = prim != "d_lp_s" or late in b2.Topology(b2.TopologyKind.ring, world, 0).neighbors(rank, 0)
+        if depends and r.get("late_call") == "ok":
             bad.append(f"rank{rank} {prim}: the late call returned success")
         if r.get("next_call") != "timeout" or r.get("sync") != "timeout" or not r.get("poisoned", False):
             bad.append(f"rank{rank} {prim}: communicator kept working after the timeout {r}")

@@ -136,6 +136,43 @@ def test_host_buffer_path(ep, oracle):
     y = x.copy()
     b2.c_lp_s(ep, 0.0, y, U8, None, bucket=11)  # numpy in place, staged through the GPU
     assert np.array_equal(bits(y), bits(want))
+    # unpinned torch tensor: the same, through the cached pinned bounce buffer
+    z = torch.as_tensor(x.copy())
+    b2.c_lp_s(ep, 0.0, z, U8, None, bucket=11)
+    assert np.array_equal(bits(z.numpy()), bits(want))
+
+
+def test_host_pinned_pipeline(ep, oracle):
+    """Pinned host buckets with blocking=False: uploads, kernels and downloads
+    of consecutive calls overlap on the endpoint's copy streams; after
+    ep.sync() every buffer holds its own call chain's result."""
+    n = 1_000_003
+    bufs = [torch.as_tensor(oracle.synth(n, 70 + b)).pin_memory() for b in range(3)]
+    want = [oracle.synth(n, 70 + b) for b in range(3)]
+    for i in range(9):
+        b2.c_lp_s(ep, 0.0, bufs[i % 3], U8, None, bucket=12, blocking=False)
+        w = [want[i % 3]]
+        oracle.c_lp_s(w, codec=1)
+    ep.sync()
+    for b in range(3):
+        assert np.array_equal(bits(bufs[b].numpy()), bits(want[b])), b
+
+
+def test_host_nonfinite_leaves_x_untouched(ep):
+    """The reference throws from encode before x changes (codec.cpp:24-27):
+    a blocking host call checks the device status before writing back."""
+    x = np.ones(5000, np.float32)
+    x[17] = np.inf
+    before = x.copy()
+    with pytest.raises(b2.Error):
+        b2.c_lp_s(ep, 0.0, x, U8, None, bucket=13)
+    assert np.array_equal(bits(x), bits(before))
+    p = torch.ones(5000).pin_memory()
+    p[9] = float("nan")
+    before = p.clone()
+    with pytest.raises(b2.Error):
+        b2.c_lp_s(ep, 0.0, p, U8, None, bucket=13)
+    assert np.array_equal(bits(p.numpy()), bits(before.numpy()))
 
 
 def test_flatten_aliasing_and_collective(ep, oracle):
