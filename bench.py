@@ -218,7 +218,7 @@ def run_b200(args, rank: int, world: int):
     g = world
     n = args.n
     prim = args.prim
-    ep = b2.B200Endpoint(rank, world, dev)
+    ep = b2.B200Endpoint(rank, world, dev, timeout_ms=120_000)
     codec = b2.Codec(b2.CodecKind.onebit if prim.endswith("_onebit") else b2.CodecKind.uniform8)
     stream = torch.cuda.current_stream()
     x = torch.empty(n, dtype=torch.float32, device="cuda")
@@ -274,18 +274,22 @@ def run_b200(args, rank: int, world: int):
     launches0 = n_launches()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if args.profile_range:  # ncu --profile-from-start off: only the timed steps
+        torch.cuda.profiler.start()
     with ClockSampler(dev) as clk:
         ev0.record(stream)
         for i in range(args.steps):
             step(xs[i % nbuf])
         ev1.record(stream)
         ev1.synchronize()
+    if args.profile_range:
+        torch.cuda.profiler.stop()
     ep.sync()
     launches = n_launches() - launches0
     ms_local = ev0.elapsed_time(ev1) / args.steps
     ms = ms_local
     if world > 1:
-        t = torch.tensor([ms_local], device="cuda")
+        t = torch.tensor([ms_local], device="cuda" if args.dist == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     barrier()
@@ -353,7 +357,7 @@ def run_b200(args, rank: int, world: int):
         pcie_ms = min(pcie_ms, c0.elapsed_time(c1))
     del xd
     if world > 1:
-        t = torch.tensor([ems, pcie_ms], device="cuda")
+        t = torch.tensor([ems, pcie_ms], device="cuda" if args.dist == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ems, pcie_ms = float(t[0].item()), float(t[1].item())
 
@@ -453,6 +457,10 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=None, help="elements per worker (default: the full bucket)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace", action="store_true", help="print per-phase device timestamps (stderr)")
+    ap.add_argument("--profile-range", action="store_true",
+                    help="cudaProfilerStart/Stop around the timed steps (ncu --profile-from-start off)")
+    ap.add_argument("--dist", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend of the plumbing (barriers, max over ranks)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes/launch from an ncu --set full capture (profiles/)")
     args = ap.parse_args()
@@ -465,7 +473,7 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        if args.impl == "b200":
+        if args.impl == "b200" and args.dist == "nccl":
             torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
             dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank))))
         else:

@@ -102,6 +102,16 @@ int b2_u8_encode_stochastic(const float* x, size_t n, uint8_t* codes, float* hdr
  * y = x - delta; codes,hdr = Q(y); delta = y - D(Q(y)); decoded (nullable) = D(Q(y)) */
 int b2_u8_compensate_encode(const float* x, float* delta, size_t n, uint8_t* codes,
                             float* hdr, float* decoded, void* stream);
+/* compensate_encode with the identity codec: y = x - delta -> y (the payload
+ * floats), delta = y - y; *nonfinite (device int) |= 1 if any y is non-finite
+ * (the reference's encode throws, codec.cpp:24-27).  x, delta, y device. */
+int b2_identity_compensate_encode(const float* x, float* delta, size_t n, float* y, int* nonfinite,
+                                  void* stream);
+/* compensate_encode with the onebit codec: decoded := y = x - delta,
+ * wire = Q(y) (as b2_onebit_encode), decoded := D(Q(y)), delta = y - D(Q(y)).
+ * decoded (n floats, 16-byte aligned) is required: it holds y meanwhile. */
+int b2_onebit_compensate_encode(const float* x, float* delta, size_t n, uint8_t* wire, float* decoded,
+                                void* stream);
 /* Exact reference wire bytes [min f32 LE][max f32 LE][u8 x n] (codec.hpp:21-24)
  * into a device buffer of 8 + n bytes, and back. */
 int b2_u8_pack_wire(const uint8_t* codes, const float* hdr, size_t n, uint8_t* wire, void* stream);

@@ -198,16 +198,29 @@ def compensate_encode(codec: Codec, x, delta, rng=None, decoded: list | None = N
     dd = torch.as_tensor(np.asarray(delta, dtype=np.float32)).to(xd.device) if host_delta else delta
     if dd.numel() != n:
         raise Error("compensate_encode: length mismatch")
-    if codec.kind == CodecKind.identity:
-        y = xd - dd
-        payload = codec.encode(y)
-        dec = y.clone()
-        dd.copy_(y - dec)
+    if codec.kind == CodecKind.identity:  # y = x - delta is the payload; delta = y - y (one kernel)
+        xa = xd.reshape(-1).contiguous()
+        da = dd.reshape(-1) if dd.is_contiguous() else dd.reshape(-1).clone()
+        dec = torch.empty(n, dtype=torch.float32, device=xd.device)
+        flag = torch.zeros(1, dtype=torch.int32, device=xd.device)
+        check(lib.b2_identity_compensate_encode(xa.data_ptr() if n else 0, da.data_ptr() if n else 0, n,
+                                                dec.data_ptr() if n else 0, flag.data_ptr(), _stream(xd.device)))
+        if int(flag.item()):
+            raise Error("encode: non-finite input value")  # codec.cpp:24-27, delta untouched
+        if da.data_ptr() != dd.data_ptr():
+            dd.copy_(da.view_as(dd))
+        payload = dec.view(torch.uint8).clone()
     elif codec.kind == CodecKind.onebit:  # y = x - delta; P = Q(y); delta = y - D(P), all exact fp32
-        y = xd.reshape(-1) - dd.reshape(-1)
-        payload = codec.encode(y)
-        dec = codec.decode(payload, n)
-        dd.copy_((y - dec).view_as(dd))
+        xa = xd.reshape(-1) if _aligned(xd) and xd.is_contiguous() else xd.reshape(-1).clone()
+        da = dd.reshape(-1).clone()  # written only once the encode succeeded
+        dec = torch.empty(max(n, 4), dtype=torch.float32, device=xd.device)[:n]
+        wire = torch.empty(((4 + (n + 7) // 8) + 15) // 16 * 16, dtype=torch.uint8, device=xd.device)
+        check(lib.b2_onebit_compensate_encode(xa.data_ptr() if n else 0, da.data_ptr() if n else 0, n,
+                                              wire.data_ptr(), dec.data_ptr(), _stream(xd.device)))
+        payload = wire[:codec.payload_size(n)]
+        if bool(torch.isnan(payload[:4].view(torch.float32)).all()):  # the kernel's non-finite mark
+            raise Error("encode: non-finite input value")
+        dd.copy_(da.view_as(dd))
     else:
         xa = xd if _aligned(xd) else xd.clone()
         da = dd if _aligned(dd) and dd.is_contiguous() else dd.clone()

@@ -417,8 +417,9 @@ class _Bucket:
                 else:
                     np.copyto(self.host_t, self.src.numpy().reshape(np.shape(self.host_t)))
             return
+        compute = torch.cuda.current_stream(ep.device)  # the collective was launched here
         with torch.cuda.stream(st.d2h):
-            st.d2h.wait_stream(torch.cuda.current_stream(ep.device))
+            st.d2h.wait_stream(compute)
             self.src.copy_(self.dev, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(st.d2h)

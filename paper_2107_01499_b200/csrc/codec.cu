@@ -376,6 +376,39 @@ __global__ void __launch_bounds__(kObThreads) onebit_decode_kernel(const uint8_t
   }
 }
 
+// compensate_encode (codec.cpp:125-137) for the identity and onebit codecs:
+// y = x - delta (fp32), then delta = y - D(Q(y)).  Identity: Q is the copy,
+// so delta = y - y (0, NaN for non-finite y) and `flag` records a non-finite
+// y (the reference's encode throws, codec.cpp:24-27).
+__global__ void identity_compensate_kernel(const float* __restrict__ x, float* __restrict__ delta, size_t n,
+                                           float* __restrict__ y_out, int* flag) {
+  int bad = 0;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const float y = __fsub_rn(x[i], delta[i]);
+    y_out[i] = y;
+    delta[i] = __fsub_rn(y, y);
+    bad |= !finite_f(y);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+// onebit, before the encode: y = x - delta into `y` (the caller's decoded buffer)
+__global__ void sub_kernel(const float* __restrict__ x, const float* __restrict__ delta, size_t n,
+                           float* __restrict__ y) {
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    y[i] = __fsub_rn(x[i], delta[i]);
+}
+// onebit, after the encode: D(Q(y)) = (y not negative ? s : -s) (kernels.cpp:65-69), delta = y - D(Q(y))
+__global__ void onebit_residual_kernel(const uint8_t* __restrict__ wire, float* __restrict__ y_dec,
+                                       float* __restrict__ delta, size_t n) {
+  const float s = *reinterpret_cast<const float*>(wire);
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const float y = y_dec[i];
+    const float d = (__float_as_uint(y) >> 31) ? -s : s;
+    delta[i] = __fsub_rn(y, d);
+    y_dec[i] = d;
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------- shared host utils
@@ -523,6 +556,36 @@ int b2_u8_compensate_encode(const float* x, float* delta, size_t n, uint8_t* cod
   B2_REQUIRE(n == 0 || (aligned16(x) && aligned16(delta) && aligned16(codes) && (!decoded || aligned16(decoded))),
              "b2_u8_compensate_encode: x, delta, codes, decoded must be 16-byte aligned");
   return launch_encode(x, delta, n, codes, hdr, decoded, static_cast<cudaStream_t>(stream));
+}
+
+static int elementwise_grid(size_t n) {
+  return int(std::min<size_t>(std::max<size_t>((n + kThreads - 1) / kThreads, 1), size_t(sm_count()) * 8));
+}
+
+int b2_identity_compensate_encode(const float* x, float* delta, size_t n, float* y, int* nonfinite, void* stream) {
+  B2_REQUIRE(nonfinite, "b2_identity_compensate_encode: nonfinite flag is null");
+  if (n == 0) return B2_OK;
+  B2_REQUIRE(x && delta && y, "b2_identity_compensate_encode: null buffer");
+  identity_compensate_kernel<<<elementwise_grid(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, delta, n, y, nonfinite);
+  B2_CUDA_TRY(cudaGetLastError());
+  return B2_OK;
+}
+
+int b2_onebit_compensate_encode(const float* x, float* delta, size_t n, uint8_t* wire, float* decoded,
+                                void* stream) {
+  B2_REQUIRE(wire && (n == 0 || (x && delta && decoded)), "b2_onebit_compensate_encode: null buffer");
+  B2_REQUIRE(n == 0 || aligned16(decoded), "b2_onebit_compensate_encode: decoded must be 16-byte aligned");
+  auto s = static_cast<cudaStream_t>(stream);
+  if (n) {
+    sub_kernel<<<elementwise_grid(n), kThreads, 0, s>>>(x, delta, n, decoded);
+    B2_CUDA_TRY(cudaGetLastError());
+  }
+  int rc = b2_onebit_encode(decoded, n, wire, stream);
+  if (rc || n == 0) return rc;
+  onebit_residual_kernel<<<elementwise_grid(n), kThreads, 0, s>>>(wire, decoded, delta, n);
+  B2_CUDA_TRY(cudaGetLastError());
+  return B2_OK;
 }
 
 int b2_u8_pack_wire(const uint8_t* codes, const float* hdr, size_t n, uint8_t* wire, void* stream) {

@@ -110,12 +110,18 @@ void check_codec(const Codec& c, std::mt19937* rng, bool collective = true) {
 Payload Codec::encode(std::span<const float> x, std::mt19937* rng) const {
   check_codec(*this, rng, /*collective=*/false);
   const std::size_t n = x.size();
-  if (kind == CodecKind::identity) {  // codec.cpp:41,47-50
-    std::vector<float> h = to_host(x);
-    for (float v : h)
-      if (!std::isfinite(v)) throw Error(B2_ERR_NONFINITE, "encode: non-finite input value");
+  if (kind == CodecKind::identity) {  // codec.cpp:41,47-50: the payload is x, after check_finite
+    if (n == 0) return {};
+    DevBuf xs(4 * n), zero(4 * n), y(4 * n), flag(sizeof(int));
+    cuda_check(cudaMemcpy(xs.p, x.data(), 4 * n, cudaMemcpyDefault), "stage in");
+    cuda_check(cudaMemset(zero.p, 0, 4 * n), "memset");
+    cuda_check(cudaMemset(flag.p, 0, sizeof(int)), "memset");
+    check(b2_identity_compensate_encode(xs.as<float>(), zero.as<float>(), n, y.as<float>(), flag.as<int>(), nullptr));
+    int bad = 0;
+    cuda_check(cudaMemcpy(&bad, flag.p, sizeof(int), cudaMemcpyDeviceToHost), "flag");
+    if (bad) throw Error(B2_ERR_NONFINITE, "encode: non-finite input value");
     Payload p(4 * n);
-    if (n) std::memcpy(p.data(), h.data(), 4 * n);
+    cuda_check(cudaMemcpy(p.data(), y.p, 4 * n, cudaMemcpyDeviceToHost), "copy payload");
     return p;
   }
   if (kind == CodecKind::onebit) {  // codec.cpp:81-88
@@ -182,23 +188,46 @@ Payload compensate_encode(const Codec& codec, std::span<const float> x, std::spa
   const std::size_t n = x.size();
   if (delta.size() != n) throw Error(B2_ERR_INVALID, "compensate_encode: length mismatch");  // codec.cpp:129
   if (codec.kind == CodecKind::onebit) {  // y = x - delta, P = Q(y), delta = y - D(P) (codec.cpp:130-136)
-    std::vector<float> y = to_host(x), d = to_host(delta);
-    for (std::size_t k = 0; k < n; ++k) y[k] -= d[k];
-    Payload p = codec.encode(y);
-    std::vector<float> dec = codec.decode(p, n);
-    for (std::size_t k = 0; k < n; ++k) d[k] = y[k] - dec[k];
-    if (n) cuda_check(cudaMemcpy(delta.data(), d.data(), 4 * n, cudaMemcpyDefault), "delta out");
-    if (decoded) *decoded = std::move(dec);
+    const std::size_t ps = codec.payload_size(n);
+    DevBuf xs((n ? n : 1) * 4), ds((n ? n : 1) * 4), dec((n ? n : 4) * 4), wire((ps + 15) / 16 * 16);
+    if (n) {
+      cuda_check(cudaMemcpy(xs.p, x.data(), 4 * n, cudaMemcpyDefault), "stage x");
+      cuda_check(cudaMemcpy(ds.p, delta.data(), 4 * n, cudaMemcpyDefault), "stage delta");
+    }
+    check(b2_onebit_compensate_encode(xs.as<float>(), ds.as<float>(), n, wire.as<std::uint8_t>(), dec.as<float>(),
+                                      nullptr));
+    Payload p(ps);
+    cuda_check(cudaMemcpy(p.data(), wire.p, ps, cudaMemcpyDeviceToHost), "copy payload");
+    float scale;
+    std::memcpy(&scale, p.data(), 4);
+    if (std::isnan(scale)) throw Error(B2_ERR_NONFINITE, "encode: non-finite input value");  // before delta changes
+    if (n) cuda_check(cudaMemcpy(delta.data(), ds.p, 4 * n, cudaMemcpyDefault), "delta out");
+    if (decoded) {
+      decoded->resize(n);
+      if (n) cuda_check(cudaMemcpy(decoded->data(), dec.p, 4 * n, cudaMemcpyDeviceToHost), "decoded out");
+    }
     return p;
   }
   if (codec.kind == CodecKind::identity) {
-    std::vector<float> h = to_host(x), d = to_host(delta);
-    for (std::size_t k = 0; k < n; ++k) h[k] -= d[k];
-    Payload p = codec.encode(h);
-    std::vector<float> zero(n);
-    for (std::size_t k = 0; k < n; ++k) zero[k] = h[k] - h[k];
-    if (n) cuda_check(cudaMemcpy(delta.data(), zero.data(), 4 * n, cudaMemcpyDefault), "delta out");
-    if (decoded) *decoded = h;
+    DevBuf xs((n ? n : 1) * 4), ds((n ? n : 1) * 4), y((n ? n : 1) * 4), flag(sizeof(int));
+    if (n) {
+      cuda_check(cudaMemcpy(xs.p, x.data(), 4 * n, cudaMemcpyDefault), "stage x");
+      cuda_check(cudaMemcpy(ds.p, delta.data(), 4 * n, cudaMemcpyDefault), "stage delta");
+    }
+    cuda_check(cudaMemset(flag.p, 0, sizeof(int)), "memset");
+    check(b2_identity_compensate_encode(xs.as<float>(), ds.as<float>(), n, y.as<float>(), flag.as<int>(), nullptr));
+    int bad = 0;
+    cuda_check(cudaMemcpy(&bad, flag.p, sizeof(int), cudaMemcpyDeviceToHost), "flag");
+    if (bad) throw Error(B2_ERR_NONFINITE, "encode: non-finite input value");  // codec.cpp:24-27, delta untouched
+    Payload p(4 * n);
+    if (n) {
+      cuda_check(cudaMemcpy(p.data(), y.p, 4 * n, cudaMemcpyDeviceToHost), "copy payload");
+      cuda_check(cudaMemcpy(delta.data(), ds.p, 4 * n, cudaMemcpyDefault), "delta out");
+    }
+    if (decoded) {
+      decoded->resize(n);
+      if (n) std::memcpy(decoded->data(), p.data(), 4 * n);
+    }
     return p;
   }
   DevBuf xs((n ? n : 1) * 4), ds((n ? n : 1) * 4), codes(n + 64), hdr(B2_U8_HDR_BYTES), dec((n ? n : 1) * 4),
