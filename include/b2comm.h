@@ -163,6 +163,12 @@ int b2_comm_poll(b2_comm_t comm);
  * and every primitive is refused with B2_ERR_TIMEOUT until the communicator
  * is destroyed and re-created (there is no way to re-agree the epochs). */
 int b2_comm_set_timeout_ms(b2_comm_t comm, uint64_t ms);
+/* SM budget of every primitive launch: `sms` persistent CTAs (one per SM)
+ * instead of one per SM of the device, leaving the other SMs to compute that
+ * runs concurrently (communication overlapping backward, engine.cpp:113-153).
+ * 0 = all SMs (default).  Every rank must set the same budget (checked when a
+ * window is first exchanged). */
+int b2_comm_set_sm_budget(b2_comm_t comm, int sms);
 /* 1 when the communicator is poisoned by a rendezvous timeout (see above). */
 int b2_comm_poisoned(b2_comm_t comm);
 /* Collective (every rank, same bucket id): free every window of `bucket`

@@ -249,8 +249,12 @@ class OverlapEngine {
   std::span<float> arena(std::size_t bucket);    // device span of one bucket
   // layer's gradient is complete on compute_stream (cudaStream_t)
   void layer_done(std::size_t layer, void* compute_stream);
-  // compute_stream waits for every bucket issued since the last finish()
+  // compute_stream waits for every bucket issued since the last finish().
+  // Non-blocking: a device error of these buckets is thrown by synchronize(),
+  // or by the next finish() once they have completed (one iteration late).
   void finish(void* compute_stream);
+  // wait for every bucket issued so far; throw a latched device error
+  void synchronize();
 
  private:
   B200Endpoint& ep_;
@@ -261,6 +265,8 @@ class OverlapEngine {
   std::vector<std::size_t> bucket_of_, offset_;
   std::vector<float*> arenas_;
   void* comm_ = nullptr;  // cudaStream_t
+  void* done_ = nullptr;  // cudaEvent_t: the last finish()'s buckets complete
+  bool issued_ = false;
   std::size_t pending_ = 0;
 };
 

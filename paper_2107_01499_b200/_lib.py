@@ -54,6 +54,7 @@ _SIGS = {
     "b2_comm_set_timeout_ms": (C.c_int, [C.c_void_p, C.c_uint64]),
     "b2_comm_launches": (C.c_uint64, [C.c_void_p]),
     "b2_comm_poisoned": (C.c_int, [C.c_void_p]),
+    "b2_comm_set_sm_budget": (C.c_int, [C.c_void_p, C.c_int]),
     "b2_comm_release_bucket": (C.c_int, [C.c_void_p, C.c_uint32]),
     "b2_comm_window_bytes": (C.c_size_t, [C.c_void_p]),
     "b2_comm_enable_trace": (C.c_int, [C.c_void_p, C.c_int]),

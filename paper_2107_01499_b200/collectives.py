@@ -189,6 +189,16 @@ class B200Endpoint:
     def launches(self) -> int:
         return int(lib.b2_comm_launches(self._h))
 
+    def set_sm_budget(self, sms: int) -> None:
+        """Launch every primitive on `sms` SMs (0: all), leaving the others to
+        concurrent compute.  Every rank must set the same budget (b2comm.h)."""
+        check(lib.b2_comm_set_sm_budget(self._h, int(sms)))
+
+    def poll(self) -> None:
+        """Raise a latched device error (non-finite input, timeout) without
+        synchronizing."""
+        check(lib.b2_comm_poll(self._h))
+
     def poisoned(self) -> bool:
         """True once a rendezvous timed out: every further primitive raises
         until the endpoint is closed and re-created (b2comm.h)."""

@@ -34,6 +34,12 @@ void set_error(const char* fmt, ...);
 // Persistent-grid size for a kernel: SMs x resident CTAs per SM.
 int persistent_grid(const void* func, int threads, size_t smem = 0);
 int sm_count();
+// A persistent grid restricted to an SM budget (sms > 0): whole CTAs-per-SM
+// multiples of at most `sms` SMs.
+inline int budget_grid(int grid, int sms) {
+  const int per_sm = grid / (sm_count() > 0 ? sm_count() : 1);
+  return sms > 0 && sms < sm_count() ? sms * (per_sm > 0 ? per_sm : 1) : grid;
+}
 // Opt a ring kernel into the 192 KB dynamic shared memory (once per device).
 cudaError_t ensure_ring_smem(const void* fn);
 

@@ -1113,10 +1113,12 @@ __global__ void __launch_bounds__(kRingThreads, 1) decent_kernel(DecentArgs a) {
 }
 
 template <typename K, typename A>
-int launch_ring(K kernel, const A& args, cudaStream_t s) {
+int launch_ring(K kernel, const A& args, cudaStream_t s, int sms) {
   static_assert(sizeof(A) < 4000, "kernel argument block too large");
   B2_CUDA_TRY(ensure_ring_smem(reinterpret_cast<const void*>(kernel)));
-  const int grid = sm_count();  // one persistent CTA per SM; all co-resident
+  // one persistent CTA per SM (all co-resident), or the communicator's SM
+  // budget: fewer CTAs leave SMs to concurrent compute (the engine overlap)
+  const int grid = sms > 0 && sms < sm_count() ? sms : sm_count();
   A copy = args;
   void* params[] = {&copy};
   B2_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kernel), dim3(grid), dim3(kRingThreads),
@@ -1141,15 +1143,15 @@ cudaError_t ensure_ring_smem(const void* fn) {
   return e;
 }
 
-int launch_central(const CentralArgs& a, int codec, bool ec, cudaStream_t s) {
+int launch_central(const CentralArgs& a, int codec, bool ec, cudaStream_t s, int sms) {
   if (codec == kU8)
-    return ec ? launch_ring(central_kernel<kU8, true>, a, s) : launch_ring(central_kernel<kU8, false>, a, s);
-  return ec ? launch_ring(central_kernel<kIdentity, true>, a, s)
-            : launch_ring(central_kernel<kIdentity, false>, a, s);
+    return ec ? launch_ring(central_kernel<kU8, true>, a, s, sms) : launch_ring(central_kernel<kU8, false>, a, s, sms);
+  return ec ? launch_ring(central_kernel<kIdentity, true>, a, s, sms)
+            : launch_ring(central_kernel<kIdentity, false>, a, s, sms);
 }
 
-int launch_decent(const DecentArgs& a, int codec, cudaStream_t s) {
-  return codec == kU8 ? launch_ring(decent_kernel<kU8>, a, s) : launch_ring(decent_kernel<kIdentity>, a, s);
+int launch_decent(const DecentArgs& a, int codec, cudaStream_t s, int sms) {
+  return codec == kU8 ? launch_ring(decent_kernel<kU8>, a, s, sms) : launch_ring(decent_kernel<kIdentity>, a, s, sms);
 }
 
 int max_persistent_grid() { return sm_count() * 4; }

@@ -28,11 +28,11 @@
 #include "collectives.cuh"
 
 namespace b2 {
-int launch_central(const CentralArgs& a, int codec, bool ec, cudaStream_t s);
-int launch_decent(const DecentArgs& a, int codec, cudaStream_t s);
+int launch_central(const CentralArgs& a, int codec, bool ec, cudaStream_t s, int sms);
+int launch_decent(const DecentArgs& a, int codec, cudaStream_t s, int sms);
 int max_persistent_grid();
-int launch_onebit_central(const OnebitArgs& a, bool ec, cudaStream_t s);
-int launch_onebit_decent(const OnebitDecentArgs& a, cudaStream_t s);
+int launch_onebit_central(const OnebitArgs& a, bool ec, cudaStream_t s, int sms);
+int launch_onebit_decent(const OnebitDecentArgs& a, cudaStream_t s, int sms);
 size_t onebit_slot_bytes(size_t maxchunk);
 }  // namespace b2
 
@@ -80,6 +80,7 @@ struct b2_comm {
   int* status_d = nullptr;
   unsigned long long timeout_ns = 600000ull * 1000000ull;  // 10 min; tests and benches set their own
   bool poisoned = false;  // a rendezvous timed out: every further launch is refused
+  int sm_budget = 0;      // SMs per primitive launch (0: all); identical on every rank
   unsigned long long launches = 0;
   unsigned long long* trace = nullptr;  // device [max grid * kTraceSlots], when enabled
   int trace_grid = 0;
@@ -188,7 +189,7 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
     mine.ok = ok ? 1 : 0;
     mine.pid = static_cast<int>(getpid());
     mine.device = c->device;
-    mine.grid = sm_count();
+    mine.grid = c->sm_budget > 0 && c->sm_budget < sm_count() ? c->sm_budget : sm_count();
     mine.ptr = reinterpret_cast<unsigned long long>(w->local);
     mine.bytes = w->bytes;
     if (ok && cudaIpcGetMemHandle(&mine.handle, w->local) != cudaSuccess) {
@@ -213,7 +214,7 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
         return fail(B2_ERR_INVALID);
       }
       if (all[j].grid != mine.grid) {
-        set_error("rank %d runs %d CTAs per launch, rank %d runs %d: all GPUs must have the same SM count", j,
+        set_error("rank %d launches on %d SMs, rank %d on %d: the SM count and b2_comm_set_sm_budget must agree", j,
                   all[j].grid, c->rank, mine.grid);
         return fail(B2_ERR_INVALID);
       }
@@ -418,6 +419,15 @@ int b2_comm_read_trace(b2_comm_t c, uint64_t* out, int max_ctas, int* n_slots) {
   return B2_OK;
 }
 
+int b2_comm_set_sm_budget(b2_comm_t c, int sms) {
+  B2_REQUIRE(c, "null communicator");
+  B2_REQUIRE(sms >= 0, "SM budget %d is negative", sms);
+  DeviceGuard dg(c->device);
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->sm_budget = sms >= sm_count() ? 0 : sms;
+  return B2_OK;
+}
+
 int b2_comm_poisoned(b2_comm_t c) {
   if (!c) return 0;
   if (__atomic_load_n(c->status_h, __ATOMIC_ACQUIRE) & kStatusTimeout) c->poisoned = true;
@@ -541,7 +551,7 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   a.timeout_ns = c->timeout_ns;
   a.trace = c->trace;
   rc = launch_central(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity, delta != nullptr,
-                      static_cast<cudaStream_t>(stream));
+                      static_cast<cudaStream_t>(stream), c->sm_budget);
   if (rc == B2_OK) ++c->launches;
   return rc;
 }
@@ -580,7 +590,7 @@ static int onebit_central(b2_comm_t c, float* x, size_t n, float* delta, size_t 
   a.partials = reinterpret_cast<double*>(w->partials);
   a.status = w->fail;
   a.timeout_ns = c->timeout_ns;
-  rc = launch_onebit_central(a, delta != nullptr, static_cast<cudaStream_t>(stream));
+  rc = launch_onebit_central(a, delta != nullptr, static_cast<cudaStream_t>(stream), c->sm_budget);
   if (rc == B2_OK) ++c->launches;
   return rc;
 }
@@ -634,7 +644,7 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
     a.partials = reinterpret_cast<double*>(w->partials);
     a.status = w->fail;
     a.timeout_ns = c->timeout_ns;
-    rc = launch_onebit_decent(a, static_cast<cudaStream_t>(stream));
+    rc = launch_onebit_decent(a, static_cast<cudaStream_t>(stream), c->sm_budget);
     if (rc == B2_OK) {
       w->exp_reads[a.parity] += static_cast<unsigned long long>(n_nbrs - 1);  // symmetric: my readers
       ++c->launches;
@@ -669,7 +679,7 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
   a.timeout_ns = c->timeout_ns;
   a.trace = c->trace;
   rc = launch_decent(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity,
-                     static_cast<cudaStream_t>(stream));
+                     static_cast<cudaStream_t>(stream), c->sm_budget);
   if (rc == B2_OK) {
     w->exp_reads[a.parity] += static_cast<unsigned long long>(n_nbrs - 1);
     if (n_nbrs > 1)

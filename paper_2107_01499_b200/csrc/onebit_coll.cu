@@ -477,7 +477,7 @@ const void* onebit_fn(bool ec) {
             : reinterpret_cast<const void*>(onebit_central_kernel<G, false>);
 }
 
-int launch_onebit_central(const OnebitArgs& a, bool ec, cudaStream_t s) {
+int launch_onebit_central(const OnebitArgs& a, bool ec, cudaStream_t s, int sms) {
   const void* fn = nullptr;
   switch (a.g) {
     case 1: fn = onebit_fn<1>(ec); break;
@@ -490,14 +490,14 @@ int launch_onebit_central(const OnebitArgs& a, bool ec, cudaStream_t s) {
     case 8: fn = onebit_fn<8>(ec); break;
     default: set_error("onebit c_lp_s: %d ranks (1..%d supported)", a.g, kMaxRanks); return B2_ERR_INVALID;
   }
-  const int grid = persistent_grid(fn, kThr);
+  const int grid = budget_grid(persistent_grid(fn, kThr), sms);
   OnebitArgs args = a;
   void* params[] = {&args};
   B2_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThr), params, 0, s));
   return B2_OK;
 }
 
-int launch_onebit_decent(const OnebitDecentArgs& a, cudaStream_t s) {
+int launch_onebit_decent(const OnebitDecentArgs& a, cudaStream_t s, int sms) {
   const void* fn = nullptr;
   switch (a.nnb) {
     case 1: fn = reinterpret_cast<const void*>(onebit_decent_kernel<1>); break;
@@ -510,7 +510,7 @@ int launch_onebit_decent(const OnebitDecentArgs& a, cudaStream_t s) {
     case 8: fn = reinterpret_cast<const void*>(onebit_decent_kernel<8>); break;
     default: set_error("onebit d_lp_s: %d neighbours (1..%d supported)", a.nnb, kMaxRanks); return B2_ERR_INVALID;
   }
-  const int grid = persistent_grid(fn, kThr);
+  const int grid = budget_grid(persistent_grid(fn, kThr), sms);
   OnebitDecentArgs args = a;
   void* params[] = {&args};
   B2_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThr), params, 0, s));

@@ -77,7 +77,7 @@ class OverlapEngine:
     def __init__(self, ep: B200Endpoint, layer_sizes, capacity_bytes: int = DEFAULT_BUCKET_CAPACITY_BYTES,
                  fusion: bool = True, primitive: str = "c_lp_s", codec: Codec | None = None,
                  topology: Topology | None = None, mode: ReduceMode = ReduceMode.average,
-                 bucket_base: int = 1 << 20):
+                 bucket_base: int = 1 << 20, sm_budget: int | None = None):
         if primitive not in ("c_lp_s", "c_fp_s", "d_fp_s", "d_lp_s"):
             raise Error(f"engine: unknown primitive {primitive}")
         self.ep = ep
@@ -105,9 +105,14 @@ class OverlapEngine:
                 self._bucket_of[layer] = b.id
                 off += n
             self.arenas.append(arena)
-        self.comm_stream = torch.cuda.Stream(device=dev)
+        # high priority: as backward kernels retire, the scheduler hands their
+        # SMs to the communication CTAs first
+        self.comm_stream = torch.cuda.Stream(device=dev, priority=-1)
+        if sm_budget is not None:  # the SMs communication may take (the rest stay with backward)
+            ep.set_sm_budget(sm_budget)
         self.round = 0
         self._pending = 0
+        self._done = None
 
     def grad(self, layer: int) -> torch.Tensor:
         """Layer `layer`'s gradient: a view into its bucket's arena."""
@@ -141,11 +146,25 @@ class OverlapEngine:
         self._pending += 1
 
     def finish(self, stream: torch.cuda.Stream | None = None) -> None:
-        """The compute stream waits for every bucket issued this iteration."""
+        """The compute stream waits for every bucket issued this iteration.
+        Non-blocking: a device error of this iteration's buckets (non-finite
+        gradient, rendezvous timeout) is raised by synchronize(), or by the
+        next finish() once this iteration's buckets have completed (the
+        reference raises synchronously, codec.cpp:24-27; here the report can
+        lag by one iteration)."""
         if self._pending != len(self.buckets):
             raise Error(f"engine: {self._pending} of {len(self.buckets)} buckets issued this iteration")
+        if self._done is not None and self._done.query():
+            self.ep.poll()  # the previous iteration's buckets are complete: report their errors
         ev = torch.cuda.Event()
         ev.record(self.comm_stream)
         (stream or torch.cuda.current_stream(self.ep.device)).wait_event(ev)
+        self._done = ev
         self._pending = 0
         self.round += 1
+
+    def synchronize(self) -> None:
+        """Wait for every bucket issued so far and raise a latched device error."""
+        if self._done is not None:
+            self._done.synchronize()
+        self.ep.poll()

@@ -572,9 +572,14 @@ OverlapEngine::OverlapEngine(B200Endpoint& ep, std::vector<std::size_t> layer_si
       off += sizes_[l];
     }
   }
+  int lo = 0, hi = 0;  // highest priority: freed SMs go to the communication CTAs first
+  cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
   cudaStream_t s;
-  cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate comm");
+  cuda_check(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi), "cudaStreamCreate comm");
   comm_ = s;
+  cudaEvent_t ev;
+  cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+  done_ = ev;
 }
 
 OverlapEngine::~OverlapEngine() {
@@ -583,6 +588,7 @@ OverlapEngine::~OverlapEngine() {
     cudaStreamSynchronize(static_cast<cudaStream_t>(comm_));
     cudaStreamDestroy(static_cast<cudaStream_t>(comm_));
   }
+  if (done_) cudaEventDestroy(static_cast<cudaEvent_t>(done_));
   for (float* p : arenas_) cudaFree(p);
 }
 
@@ -615,13 +621,20 @@ void OverlapEngine::finish(void* compute_stream) {
     throw Error(B2_ERR_INVALID, "engine: " + std::to_string(pending_) + " of " + std::to_string(buckets_.size()) +
                                     " buckets issued this iteration");
   DeviceScope ds(ep_.device());
-  cudaEvent_t ev;
-  cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
-  cuda_check(cudaEventRecord(ev, static_cast<cudaStream_t>(comm_)), "cudaEventRecord");
-  cuda_check(cudaStreamWaitEvent(static_cast<cudaStream_t>(compute_stream), ev, 0), "cudaStreamWaitEvent");
-  cudaEventDestroy(ev);
-  check(b2_comm_poll(ep_.handle()));  // a latched device error of an earlier bucket
+  auto done = static_cast<cudaEvent_t>(done_);
+  // the previous iteration's buckets, once complete, report their errors
+  if (issued_ && cudaEventQuery(done) == cudaSuccess) check(b2_comm_poll(ep_.handle()));
+  cudaGetLastError();  // cudaErrorNotReady from the query is not an error
+  cuda_check(cudaEventRecord(done, static_cast<cudaStream_t>(comm_)), "cudaEventRecord");
+  cuda_check(cudaStreamWaitEvent(static_cast<cudaStream_t>(compute_stream), done, 0), "cudaStreamWaitEvent");
+  issued_ = true;
   pending_ = 0;
+}
+
+void OverlapEngine::synchronize() {
+  DeviceScope ds(ep_.device());
+  cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(comm_)), "cudaStreamSynchronize comm");
+  check(b2_comm_poll(ep_.handle()));
 }
 
 }  // namespace rcomm::b200

@@ -297,3 +297,31 @@ def test_d_lp_s_onebit_g1(ep, oracle, n):
         t = torch.as_tensor(x).cuda()
         b2.d_lp_s(ep, 0.0, t, topo, 0, OB, mode, bucket=44)
         assert np.array_equal(bits(t.cpu().numpy()), bits(oracle.d_lp_s_rank([x], 2, int(mode))))
+
+
+def test_engine_reports_nonfinite_gradient(oracle):
+    """OverlapEngine.finish() is non-blocking; a non-finite gradient of its
+    buckets (the reference throws from encode, codec.cpp:24-27) is raised by
+    synchronize(), or by the next finish() once those buckets completed."""
+    from paper_2107_01499_b200.engine import OverlapEngine
+    ep = b2.B200Endpoint(0, 1, 0)
+    eng = OverlapEngine(ep, [1000, 3000, 500], capacity_bytes=4 * 2000, sm_budget=32)
+    for layer in reversed(range(3)):
+        eng.grad(layer).copy_(torch.as_tensor(oracle.synth(eng.sizes[layer], 40 + layer)))
+        if layer == 1:
+            eng.grad(layer)[7] = float("nan")
+        eng.layer_done(layer)
+    eng.finish()
+    with pytest.raises(b2.Error):
+        eng.synchronize()
+    # a clean iteration afterwards works (a non-finite input does not poison)
+    for layer in reversed(range(3)):
+        eng.grad(layer).copy_(torch.as_tensor(oracle.synth(eng.sizes[layer], 50 + layer)))
+        eng.layer_done(layer)
+    eng.finish()
+    eng.synchronize()
+    for bk in eng.buckets:
+        xs = [np.concatenate([oracle.synth(eng.sizes[l], 50 + l) for l in bk.layers])]
+        oracle.c_lp_s(xs, codec=1)
+        assert np.array_equal(bits(eng.arenas[bk.id].cpu().numpy()), bits(xs[0]))
+    ep.close()
