@@ -244,7 +244,7 @@ __device__ __forceinline__ bool wait_geq(const unsigned long long* flag, unsigne
 // Kernel epilogue (one thread per CTA, after the CTA's last wait): a poison
 // set by a peer that timed out in this call turns the call into an error.
 __device__ __forceinline__ void fail_epilogue(Fail* f) {
-  if (poisoned(f)) atomicOr_system(f->host, kStatusTimeout);
+  if (f && poisoned(f)) atomicOr_system(f->host, kStatusTimeout);
 }
 
 // --------------------------------------------------- work decomposition

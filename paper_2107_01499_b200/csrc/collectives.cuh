@@ -109,6 +109,17 @@ struct OnebitDecentArgs {
   unsigned long long timeout_ns;
 };
 
+// Per-source decode constants of the small-bucket D_* kernel (small_coll.cu).
+struct SrcDecS {
+  float lo, step, c23;
+  int fast;
+};
+// Buckets up to this many elements try the register-resident D_* kernel
+// (small_coll.cu) before the TMA ring; its per-CTA counters need
+// gate_stride > kSmallMaxGridD.
+constexpr size_t kSmallDecentMax = 4000000;
+constexpr size_t kSmallMaxGridD = 1024;
+
 // Decentralized neighbourhood reduce (D_FP_S, D_LP_S).
 struct DecentArgs {
   float* x;

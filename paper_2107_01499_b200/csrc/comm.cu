@@ -30,6 +30,7 @@
 namespace b2 {
 int launch_central(const CentralArgs& a, int codec, bool ec, cudaStream_t s, int sms);
 int launch_decent(const DecentArgs& a, int codec, cudaStream_t s, int sms);
+int launch_decent_small(const DecentArgs& a, int codec, cudaStream_t s, int sms);
 int max_persistent_grid();
 int launch_onebit_central(const OnebitArgs& a, bool ec, cudaStream_t s, int sms);
 int launch_onebit_decent(const OnebitDecentArgs& a, cudaStream_t s, int sms);
@@ -155,7 +156,9 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
     // (+ one for the unaligned tail), cumulative over the calls in which that
     // rank was my neighbour (the relation is symmetric, so I know how many)
     const size_t nreg = n / (16 * kGateUnits) + 1;
-    w->gate_stride = nreg + 1;  // counters per source
+    // counters per source: the ring kernel's regions + tail, or the small
+    // kernel's one per CTA (small_coll.cu)
+    w->gate_stride = std::max(nreg + 1, kSmallMaxGridD + 1);
     w->off_gate = off;
     off += round_up(sizeof(unsigned long long) * w->gate_stride * size_t(g), 256);
     const size_t b = round_up(size_t(elem) * (n + 8), 256);
@@ -678,8 +681,11 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
   a.status = w->fail;
   a.timeout_ns = c->timeout_ns;
   a.trace = c->trace;
-  rc = launch_decent(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity,
-                     static_cast<cudaStream_t>(stream), c->sm_budget);
+  rc = launch_decent_small(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity, static_cast<cudaStream_t>(stream),
+                           c->sm_budget);
+  if (rc == B2_ERR_UNSUPPORTED)
+    rc = launch_decent(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity, static_cast<cudaStream_t>(stream),
+                       c->sm_budget);
   if (rc == B2_OK) {
     w->exp_reads[a.parity] += static_cast<unsigned long long>(n_nbrs - 1);
     if (n_nbrs > 1)
