@@ -57,6 +57,9 @@ struct CentralArgs {
   float* eps;                   // ErrorState::epsilon (owned len) or null
   uint8_t* win[kMaxRanks];      // every rank's window base (peer-mapped; win[me] local)
   size_t off_gate, off_recv1, slot_stride, off_out2;
+  // staggered C_LP_S (central_stag.cu): per-source arrival counters of my
+  // chunk [g][sgate_stride], my out2 publication counters, landing slots
+  size_t off_sgate, sgate_stride, off_qgate, off_land;
   float2* partials;             // local workspace [(kMaxRanks + 1) * grid]
   unsigned* cta_done;           // local workspace [kMaxRanks + 2]
   unsigned* gridbar;            // local workspace [2]: consumer grid barrier

@@ -31,6 +31,7 @@ namespace b2 {
 int launch_central(const CentralArgs& a, int codec, bool ec, cudaStream_t s, int sms);
 int launch_decent(const DecentArgs& a, int codec, cudaStream_t s, int sms);
 int launch_decent_small(const DecentArgs& a, int codec, cudaStream_t s, int sms);
+int launch_central_stag(const CentralArgs& a, bool ec, cudaStream_t s, int sms);
 int max_persistent_grid();
 int launch_onebit_central(const OnebitArgs& a, bool ec, cudaStream_t s, int sms);
 int launch_onebit_decent(const OnebitDecentArgs& a, cudaStream_t s, int sms);
@@ -49,6 +50,7 @@ struct Window {
   uint8_t* peer[kMaxRanks] = {};
   bool ipc_opened[kMaxRanks] = {};
   size_t off_gate = 0, gate_stride = 0, off_recv1 = 0, slot_stride = 0, off_out2 = 0, off_dbuf[2] = {0, 0};
+  size_t off_sgate = 0, sgate_stride = 0, off_qgate = 0, off_land = 0;  // central_stag.cu
   unsigned long long epoch = 0;
   unsigned long long exp_reads[2] = {0, 0};
   unsigned long long sends_from[kMaxRanks] = {};  // D_*: calls (|N| > 1) in which rank j sent to me
@@ -128,15 +130,26 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
   size_t off = 256;  // WinHdr
   if (family == kCentral) {
     const size_t maxchunk = (n + g - 1) / g;
+    const size_t nreg = maxchunk / (16 * kGateUnits) + 2;
     // uint8 phase-1 region counters of my chunk (PassDesc::gate)
     w->off_gate = off;
-    off += round_up(sizeof(unsigned long long) * (maxchunk / (16 * kGateUnits) + 2), 256);
+    off += round_up(sizeof(unsigned long long) * nreg, 256);
+    // staggered path: per-source region counters, out2 publication counters
+    w->sgate_stride = nreg;
+    w->off_sgate = off;
+    off += round_up(sizeof(unsigned long long) * nreg * size_t(g), 256);
+    w->off_qgate = off;
+    off += round_up(sizeof(unsigned long long) * nreg, 256);
     // chunk k sits at slot offset e - (lo_k & ~15): up to 15 elements of head room
     w->slot_stride = round_up(size_t(elem) * (maxchunk + 16), 256);
     w->off_recv1 = off;
     off += size_t(g) * w->slot_stride;
     w->off_out2 = off;
     off += w->slot_stride;
+    if (elem == 1 && g > 1) {  // uint8: landing slots of the staggered path
+      w->off_land = off;
+      off += size_t(g) * w->slot_stride;
+    }
   } else if (family == kOnebit) {
     // slot j = rank j's onebit payload of my chunk; out2 = my phase-2 payload
     w->slot_stride = onebit_slot_bytes((n + g - 1) / g);
@@ -505,6 +518,15 @@ int b2_comm_sync(b2_comm_t c, void* stream) {
   return b2_comm_poll(c);
 }
 
+// B2_STAG=0: the pre-staggered C_LP_S kernel for every shape (A/B measurements)
+static bool stag_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("B2_STAG");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // B2_STATIC_SCHED=1: static round-robin tile assignment (A/B measurements)
 static bool static_sched() {
   static const bool v = [] {
@@ -545,6 +567,10 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   a.off_recv1 = w->off_recv1;
   a.slot_stride = w->slot_stride;
   a.off_out2 = w->off_out2;
+  a.off_sgate = w->off_sgate;
+  a.sgate_stride = w->sgate_stride;
+  a.off_qgate = w->off_qgate;
+  a.off_land = w->off_land;
   a.partials = w->partials;
   a.cta_done = w->cta_done;
   a.gridbar = w->cta_done + kMaxRanks + 2;
@@ -553,8 +579,14 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   a.status = w->fail;
   a.timeout_ns = c->timeout_ns;
   a.trace = c->trace;
-  rc = launch_central(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity, delta != nullptr,
-                      static_cast<cudaStream_t>(stream), c->sm_budget);
+  // uint8 at g >= 2 with 16-aligned equal chunks: the staggered schedule
+  // (central_stag.cu); every rank decides identically from (n, g)
+  if (codec == B2_CODEC_UNIFORM8 && c->world >= 2 && n % (16 * size_t(c->world)) == 0 && stag_enabled() &&
+      (!eps || (reinterpret_cast<uintptr_t>(eps) & 15) == 0))
+    rc = launch_central_stag(a, delta != nullptr, static_cast<cudaStream_t>(stream), c->sm_budget);
+  else
+    rc = launch_central(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity, delta != nullptr,
+                        static_cast<cudaStream_t>(stream), c->sm_budget);
   if (rc == B2_OK) ++c->launches;
   return rc;
 }

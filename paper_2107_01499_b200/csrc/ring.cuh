@@ -238,6 +238,8 @@ struct Ring {
   // the Ring (either would put the whole per-thread Ring in local memory)
   Pipe cp;        // the pipe this thread's role works on now
   Pipe p0;        // the all-stage pipe, parked while in split mode
+  Pipe pA, pB;    // the split pipes, parked between split phases
+  bool split_init = false;
   int slot = 0;       // staging cursor (consumers and storer walk it in lock step)
   unsigned sphase = 0;
   bool producer;      // warp 0 (lane 0 works)
@@ -341,19 +343,24 @@ struct Ring {
   __device__ void split_begin() {
     split = true;
     p0 = cp;
+    if (!split_init) {  // the two pipes' barrier phases persist across split phases
+      pA = pipe_desc(1);
+      pB = pipe_desc(2);
+      split_init = true;
+    }
     if (producer) {
       if ((threadIdx.x & 31) == 0) {
         cp.drain();  // every stage buffer is free
         drained[0] = 1;
       }
-      cp = pipe_desc(1);
+      cp = pA;
     } else if (producer2) {
       if ((threadIdx.x & 31) == 0)
         while (drained[0] == 0) __nanosleep(32);
-      cp = pipe_desc(2);
+      cp = pB;
     } else if (ct >= 0) {
       const bool a = group_a();
-      cp = pipe_desc(a ? 1 : 2);
+      cp = a ? pA : pB;
       gct = a ? ct : ct - 32 * kSplitWarpsA;
       gn = a ? 32 * kSplitWarpsA : kConsumers - 32 * kSplitWarpsA;
     }
@@ -372,6 +379,10 @@ struct Ring {
         drained[0] = drained[1] = 0;
       }
     }
+    if (producer || group_a())
+      pA = cp;
+    else if (producer2 || group_b())
+      pB = cp;
     cp = p0;
     gct = ct;
     gn = kConsumers;
