@@ -40,6 +40,8 @@ inline int budget_grid(int grid, int sms) {
   const int per_sm = grid / (sm_count() > 0 ? sm_count() : 1);
   return sms > 0 && sms < sm_count() ? sms * (per_sm > 0 ? per_sm : 1) : grid;
 }
+// Resident CTAs per SM of `func` at `threads` threads (cached per device).
+int occupancy(const void* func, int threads, size_t smem = 0);
 // Opt a ring kernel into the 192 KB dynamic shared memory (once per device).
 cudaError_t ensure_ring_smem(const void* fn);
 

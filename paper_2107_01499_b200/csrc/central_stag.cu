@@ -117,6 +117,7 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
   __shared__ PassDesc s_b[kMaxRanks + 1]; // landing of source (me-1-i), then [g-1]: the fold
   __shared__ PassDesc s_q;                // Q2: the fold again
   __shared__ PassDesc s_pp[kMaxRanks];    // gather of owner (me+1+i)'s out2
+  __shared__ volatile int s_qgo;          // consumers -> producer: every CTA's phase S is complete
   const int G = gridDim.x, g = a.g, me = a.me;
   const size_t c = a.n / size_t(g);  // every chunk has c elements, 16-aligned
   const size_t mlo = size_t(me) * c;
@@ -124,6 +125,10 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
   const unsigned long long ep = a.epoch, gmul = (unsigned long long)g * ep;
   float4* x4 = reinterpret_cast<float4*>(a.x);
   float4* dl4 = reinterpret_cast<float4*>(a.delta);
+  // y2 of my chunk: recomputed in Q2 from the g local code slots at g = 2
+  // (the two-term fold is two FADDs, fold.cuh sum2_exact), cached in x's own
+  // chunk at g >= 3 (4 bytes written + read beat re-running the fp64 fold)
+  const bool cache_y2 = a.g >= 3;
   auto kstep = [&](int s) { return (me + 1 + s) % g; };  // chunk of step s; s = g-1: my own
   auto src_of = [&](int i) { return (me + g - 1 - i) % g; };  // landing pass i: source rank
   uint8_t* land = a.win[me] + a.off_land;
@@ -132,6 +137,7 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
     return (j == me ? own : land + size_t(j) * a.slot_stride) - mlo;
   };
   if (threadIdx.x == 0) {
+    s_qgo = 0;
     for (int s = 0; s < g; ++s) {
       const int k = kstep(s);
       PassDesc p = PassDesc::make();
@@ -177,6 +183,11 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
     s_q = f;
     s_q.gate = nullptr;  // after the grid barrier every slot is complete
     s_q.wait_flag = nullptr;
+    if (g >= 3) {  // the cached y2 in x's own chunk
+      s_q.eb = 4;
+      s_q.nsrc = 1;
+      s_q.base[0] = reinterpret_cast<const uint8_t*>(a.x);
+    }
     for (int i = 0; i + 1 < g; ++i) {
       const int k = (me + 1 + i) % g;
       PassDesc& p = s_pp[i];
@@ -320,9 +331,11 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
               fold2<kU8>(g, fast, st, gi, has1 ? g1 : gi, T, s_dec, 1.0, y0, y1);
               if (EC) y0 = sub4(y0, reinterpret_cast<const float4*>(a.eps)[((e0 - mlo) >> 2) + gi]);
               mm4(lo2, hi2, y0);
+              if (cache_y2) x4[(e0 >> 2) + gi] = y0;  // x's own chunk was consumed by my encode
               if (has1) {
                 if (EC) y1 = sub4(y1, reinterpret_cast<const float4*>(a.eps)[((e0 - mlo) >> 2) + g1]);
                 mm4(lo2, hi2, y1);
+                if (cache_y2) x4[(e0 >> 2) + g1] = y1;
               }
             }
           }
@@ -330,6 +343,7 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
         [&](int i) {
           if (i == g - 1) load_dec();
         });
+    fence_proxy_async();  // the cached y2 is read by Q2's TMA
     B2S_TRACE_B(kTrP2Ready);
   }
   r.split_end();
@@ -363,6 +377,7 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
       __threadfence_system();
       st_relaxed_sys(&mine->ready2, ep);
     }
+    if (r.ct == 0) s_qgo = 1;
   }
   B2S_TRACE(kTrP2A);
 
@@ -374,12 +389,32 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
   const int pq = 2 * (g + 1) + g;
   uint8_t* out2 = a.win[me] + a.off_out2;
   if (r.producer || r.group_a()) {
+    if (r.producer && (threadIdx.x & 31) == 0) {  // Q2 streams data other CTAs wrote in phase S
+      while (s_qgo == 0) __nanosleep(32);
+      fence_proxy_async();
+    }
     r.stream_at(
         &s_q, 1, pq,
         [&](int, const uint8_t* st, size_t e0, size_t units, int T) {
           const bool fast = s_fast != 0;
           const int ng = int(units * 4);
           r.slot_acquire();
+          if (cache_y2) {
+            const float4* ys = reinterpret_cast<const float4*>(st);
+            for (int gi = qct; gi < ng; gi += qn) {
+              const size_t e = e0 + 4 * size_t(gi);
+              const float4 v = ys[gi];  // y2 (- eps already applied in the fold)
+              const uint32_t q = quantize4(v, p2.lo, p2.inv);
+              *reinterpret_cast<uint32_t*>(out2 + (e - mlo)) = q;
+              const float4 d = dequant4(q, p2);
+              if (EC) reinterpret_cast<float4*>(a.eps)[(e - mlo) >> 2] = sub4(v, d);
+              __stcs(x4 + (e >> 2), d);
+            }
+            r.slot_commit(reinterpret_cast<unsigned long long*>(a.win[me] + a.off_qgate) +
+                              ((e0 >> 4) - (mlo >> 4)) / kGateUnits,
+                          unsigned(units));
+            return;
+          }
           for (int gi = qct; gi < ng; gi += 2 * qn) {
             const int g1 = gi + qn;
             const bool has1 = g1 < ng;

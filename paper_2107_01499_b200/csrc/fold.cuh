@@ -150,9 +150,40 @@ struct SrcDec {
 // inv != 1 scales the fp64 sums before the single rounding (D_*: average).
 // Identity sources may hold non-finite values; `special` reports them so the
 // caller can redo the group with the exact F2F fold.
+// Two terms, no scaling: (float)((0.0 + (double)d0) + (double)d1) is the
+// correctly rounded fp32 sum d0 + d1 -- binary64 has 53 >= 2*24 + 2 bits, so
+// rounding the exact sum to binary64 and then to binary32 equals rounding it
+// once (double rounding is innocuous at that precision) -- except that the
+// fp64 fold starts from +0.0 and so turns (-0) + (-0) into +0: + 0.0f
+// reproduces that.  Two FADDs per element instead of two widenings, two DFMAs
+// and an F2F.  Holds for every input, non-finite included.
+__device__ __forceinline__ float sum2_exact(float d0, float d1) { return __fadd_rn(__fadd_rn(d0, d1), 0.0f); }
+
 template <int NSRC, int CODEC>
 __device__ __forceinline__ void fold2_fast(const uint8_t* st, int gi0, int gi1, int T, const SrcDec* dec,
                                            double inv, float4& r0, float4& r1, bool& special) {
+  if (NSRC == 2 && inv == 1.0) {
+    float4 d[2], e[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (CODEC == kU8) {
+        const uint32_t* cs = reinterpret_cast<const uint32_t*>(st + size_t(j) * T * 16);
+        const SrcDec q = dec[j];
+        d[j] = dequant4_fast(cs[gi0], q.lo, q.step, q.c23);
+        e[j] = dequant4_fast(cs[gi1], q.lo, q.step, q.c23);
+      } else {
+        const float4* fs = reinterpret_cast<const float4*>(st + size_t(j) * T * 64);
+        d[j] = fs[gi0];
+        e[j] = fs[gi1];
+      }
+    }
+    r0 = make_float4(sum2_exact(d[0].x, d[1].x), sum2_exact(d[0].y, d[1].y), sum2_exact(d[0].z, d[1].z),
+                     sum2_exact(d[0].w, d[1].w));
+    r1 = make_float4(sum2_exact(e[0].x, e[1].x), sum2_exact(e[0].y, e[1].y), sum2_exact(e[0].z, e[1].z),
+                     sum2_exact(e[0].w, e[1].w));
+    special = false;
+    return;
+  }
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
   bool sp = false;
 #pragma unroll

@@ -242,8 +242,7 @@ __global__ void __launch_bounds__(kSmallThr) decent_small_kernel(DecentArgs a) {
 template <int CODEC, int R>
 int try_small(const DecentArgs& a, cudaStream_t s, int sms) {
   const void* fn = reinterpret_cast<const void*>(decent_small_kernel<CODEC, R>);
-  int per_sm = 0;
-  B2_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSmallThr, 0));
+  const int per_sm = occupancy(fn, kSmallThr);
   const int nsm = sms > 0 && sms < sm_count() ? sms : sm_count();
   const size_t cap = size_t(nsm) * size_t(per_sm > 0 ? per_sm : 0);
   const size_t per_block = size_t(kSmallThr) * R, ng = a.n >> 2;

@@ -242,6 +242,32 @@ def run(args):
         ck.eq(f"d_lp_s identity n={n}", t.cpu().numpy(),
               orc.d_fp_s_rank([xs[j] for j in topo.neighbors(rank, 0)], 1))
 
+    # ---- chunk-aligned shapes (n % 16g == 0): the staggered C_LP_S kernel
+    # (central_stag.cu), stateless and with error feedback, repeated calls
+    for n in (16 * g, 16 * g * 37, 16 * g * 4099, 16 * g * 65537):
+        bucket += 1
+        for it in range(3):
+            xs_it = [orc.synth(n, 7300 + 31 * it + r) for r in range(g)]
+            want = [x.copy() for x in xs_it]
+            orc.c_lp_s(want, codec=1)
+            t = torch.as_tensor(xs_it[rank]).cuda()
+            b2.c_lp_s(ep, 0.0, t, U8, None, bucket=bucket)
+            ck.eq(f"c_lp_s u8 aligned n={n} it={it}", t.cpu().numpy(), want[rank])
+        bucket += 1
+        own = b2.owned_partition_len(n, g, rank)
+        es = b2.ErrorState(n, own)
+        deltas = [np.zeros(n, np.float32) for _ in range(g)]
+        eps = [np.zeros(b2.owned_partition_len(n, g, r), np.float32) for r in range(g)]
+        for t_ in range(4):
+            grads = [orc.synth(n, 7400 + 1000 * r + t_) for r in range(g)]
+            want = [x.copy() for x in grads]
+            orc.c_lp_s(want, codec=1, deltas=deltas, eps=eps)
+            t = torch.as_tensor(grads[rank]).cuda()
+            b2.c_lp_s(ep, 0.0, t, U8, es, bucket=bucket, blocking=False)
+            ck.eq(f"c_lp_s+EC aligned n={n} round={t_} x", t.cpu().numpy(), want[rank])
+        ck.eq(f"c_lp_s+EC aligned n={n} delta", es.delta.cpu().numpy(), deltas[rank])
+        ck.eq(f"c_lp_s+EC aligned n={n} eps", es.epsilon.cpu().numpy(), eps[rank])
+
     # ---- C_LP_S uint8 + error feedback, acceptance c4 style (many rounds, state carried)
     for n, rounds in ((37, 200), (100_003, 10)):
         bucket += 1
@@ -358,7 +384,7 @@ def run(args):
     # counters, per-parity D_* buffers and counters with a random topology
     # whose |N| changes every round, a neighbour running a call ahead)
     for n, prim in ((100_003, "c_lp_s"), (100_003, "c_fp_s"), (100_003, "d_lp_s"), (100_003, "d_fp_s"),
-                    (1_000_037, "c_lp_s"), (1_000_037, "d_lp_s")):
+                    (1_000_037, "c_lp_s"), (1_000_037, "d_lp_s"), (16 * g * 65537, "c_lp_s")):
         bucket += 1
         calls = 16
         host = [[orc.synth(n, 900 + 10 * b + r) for r in range(g)] for b in range(2)]
