@@ -511,22 +511,24 @@ def _node_groups(nodes):
 
 def _hier_endpoints(ep: B200Endpoint, nodes):
     """Sub-communicators of one node layout, created once (collectively:
-    every rank creates every group in the same order)."""
+    every rank creates every group in the same order); -> (intra endpoint,
+    leader endpoint or None, intra gloo group, my leader's global rank)."""
     cache = ep.__dict__.setdefault("_hier", {})
     key = tuple(nodes)
     if key not in cache:
         import torch.distributed as dist
         members, leaders = _node_groups(nodes)
         me = ep.rank()
-        intra = lead = None
+        intra = lead = igroup = leader = None
         for m in members:
             grp = dist.new_group(m, backend="gloo")
             if me in m:
                 intra = B200Endpoint(m.index(me), len(m), ep.device, bootstrap=TorchBootstrap(grp))
+                igroup, leader = grp, m[0]
         grp = dist.new_group(leaders, backend="gloo")
         if me in leaders:
             lead = B200Endpoint(leaders.index(me), len(leaders), ep.device, bootstrap=TorchBootstrap(grp))
-        cache[key] = (intra, lead)
+        cache[key] = (intra, lead, igroup, leader)
     return cache[key]
 
 
@@ -539,14 +541,27 @@ def hierarchical_c(ep: B200Endpoint, now: float, x, codec: Codec, es: ErrorState
     leader's result.  nodes[r] = node of rank r (default: ep.node_of, i.e.
     one node).  Blocking.
 
-    One node, or a lossless codec: the result is the fp64 sum of every rank's
-    x rounded once, which is c_fp_s over all ranks (the reference's lossless
-    branch exchanges fp64 partials exactly so that it matches the flat
-    primitive, test_collectives.cpp:234-252; association order differs only
-    when those fp64 sums are inexact).  Lossy across nodes: c_fp_s inside the
-    node (every member holds the leader's (float) node sum), c_lp_s among the
-    leaders, then c_fp_s inside the node with the members contributing +0 --
-    exactly the leader's values (a -0.0 arrives as +0.0; compare with ==)."""
+    One node: the reference sums the members in fp64 in ascending rank order
+    from +0.0 and rounds once (collectives.cpp:377-380) -- exactly c_fp_s
+    over all ranks (ranks >= 2; one rank: (float)(0.0 + (double)x), i.e.
+    D_FP_S over the singleton neighbourhood).
+
+    Several nodes, lossless codec: the reference keeps fp64 partials on the
+    wire and adds them leader-partial first, then the other leaders in
+    ascending order (collectives.cpp:344-372); here c_fp_s folds all ranks
+    in ascending order from +0.0.  The two fp64 sums are equal whenever
+    they are exact and otherwise differ by a few fp64 ulps, so the fp32
+    results agree to within ONE fp32 ulp (tests/mp_parity.py checks gaussian
+    inputs against the reference's order with that tolerance).
+
+    Several nodes, lossy codec: c_fp_s inside the node (every member holds
+    its leader's (float) node sum, the reference's order), c_lp_s among the
+    leaders (scatter_reduce_lp over the leader group, with es), then the
+    leader's values are BROADCAST to the members as plain bytes (the
+    reference sends float_bytes(x), collectives.cpp:382-384) -- bit-exact,
+    -0.0 included.  The byte broadcast runs over the intra-node
+    torch.distributed group (this path's inter-node leg has no transport of
+    its own)."""
     codec._check_supported(rng)
     g, me = ep.world_size(), ep.rank()
     nodes = list(nodes) if nodes is not None else [ep.node_of(r) for r in range(g)]
@@ -554,14 +569,24 @@ def hierarchical_c(ep: B200Endpoint, now: float, x, codec: Codec, es: ErrorState
         raise Error("hierarchical: node list does not match the world size")
     members, leaders = _node_groups(nodes)
     if len(leaders) == 1 or codec.lossless():
+        if g == 1:
+            return d_fp_s(ep, now, x, Topology(TopologyKind.full, 1), 0, ReduceMode.sum, bucket)
         return c_fp_s(ep, now, x, bucket)
-    intra, lead = _hier_endpoints(ep, nodes)
-    c_fp_s(intra, now, x, bucket)
+    intra, lead, igroup, leader = _hier_endpoints(ep, nodes)
+    if intra.world_size() == 1:  # the leader alone: (float)(0.0 + (double)x), -0.0 -> +0.0 as in the reference
+        d_fp_s(intra, now, x, Topology(TopologyKind.full, 1), 0, ReduceMode.sum, bucket)
+    else:
+        c_fp_s(intra, now, x, bucket)
     if lead is not None:
         c_lp_s(lead, now, x, codec, es, rng, bucket)
-    else:
-        x.zero_()
-    c_fp_s(intra, now, x, bucket)  # down: the leader's values to its members
+    # down: the leader's values to its members, as bytes
+    import torch.distributed as dist
+    b = _Bucket(ep, x)
+    if intra.world_size() > 1:
+        buf = b.dev.cpu()
+        dist.broadcast(buf, src=leader, group=igroup)
+        b.dev.copy_(buf.to(b.dev.device))
+    _finish(ep, b, True)
     return now
 
 

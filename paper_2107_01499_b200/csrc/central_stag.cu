@@ -381,50 +381,74 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
   }
   B2S_TRACE(kTrP2A);
 
-  // =============================================== Q2 || gather
+  // =============================================== Q2 + gather, one ring
+  // Q2 (local: y2 -> out2, my own chunk of x) and the gather of every other
+  // owner's out2 (NVLink, each region as soon as its owner published it)
+  // share all stages and consumer warps: the producer serves Q2 tiles while
+  // no remote region is ready.  (Split pipes starve the gather: 2 stages and
+  // 7 warps pulled at ~440 GB/s.)
   r.timed = a.trace != nullptr;
-  r.split_begin();
-  const int qct = r.gct, qn = r.gn;
-  if (r.storer && (threadIdx.x & 31) == 0) r.signal_loop();  // Q2's publication credits
   const int pq = 2 * (g + 1) + g;
   uint8_t* out2 = a.win[me] + a.off_out2;
-  if (r.producer || r.group_a()) {
-    if (r.producer && (threadIdx.x & 31) == 0) {  // Q2 streams data other CTAs wrote in phase S
-      while (s_qgo == 0) __nanosleep(32);
-      fence_proxy_async();
-    }
-    r.stream_at(
-        &s_q, 1, pq,
-        [&](int, const uint8_t* st, size_t e0, size_t units, int T) {
-          const bool fast = s_fast != 0;
-          const int ng = int(units * 4);
-          r.slot_acquire();
-          if (cache_y2) {
-            const float4* ys = reinterpret_cast<const float4*>(st);
-            for (int gi = qct; gi < ng; gi += qn) {
-              const size_t e = e0 + 4 * size_t(gi);
-              const float4 v = ys[gi];  // y2 (- eps already applied in the fold)
-              const uint32_t q = quantize4(v, p2.lo, p2.inv);
-              *reinterpret_cast<uint32_t*>(out2 + (e - mlo)) = q;
-              const float4 d = dequant4(q, p2);
-              if (EC) reinterpret_cast<float4*>(a.eps)[(e - mlo) >> 2] = sub4(v, d);
-              __stcs(x4 + (e >> 2), d);
-            }
-            r.slot_commit(reinterpret_cast<unsigned long long*>(a.win[me] + a.off_qgate) +
-                              ((e0 >> 4) - (mlo >> 4)) / kGateUnits,
-                          unsigned(units));
-            return;
+  __shared__ PassDesc s_q3[kMaxRanks];  // [0]: Q2, [1 + i]: gather of owner (me+1+i)
+  if (threadIdx.x == 0) {
+    s_q3[0] = s_q;
+    for (int i = 0; i + 1 < g; ++i) s_q3[1 + i] = s_pp[i];
+  }
+  __syncthreads();
+  if (r.storer && (threadIdx.x & 31) == 0) r.signal_loop();  // Q2's publication credits
+  if (r.producer && (threadIdx.x & 31) == 0) {  // Q2 streams data other CTAs wrote in phase S
+    while (s_qgo == 0) __nanosleep(32);
+    fence_proxy_async();
+  }
+  auto load_hdr = [&](int i) {
+    if (i == 0) return;
+    const int k = (me + i) % g;
+    const float2 h = ld_peer_f2(&hdr_at(a.win[k])->hdr2);
+    const U8Params q = u8_params(h.x, h.y);
+    s_dec3[i] = SrcDec{q.lo, q.step, q.c23};
+    s_fast3[i] = q.fastdec;
+  };
+  r.stream_at(
+      s_q3, g, pq,
+      [&](int i, const uint8_t* st, size_t e0, size_t units, int T) {
+        const int ct = r.ct;
+        if (i > 0) {  // gather: owner (me+i)'s out2 -> x
+          const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
+          const SrcDec kd = s_dec3[i];
+          if (s_fast3[i]) {
+            for (int gi = ct; gi < int(units * 4); gi += kConsumers)
+              __stcs(x4 + ((e0 >> 2) + gi), dequant4_fast(cs[gi], kd.lo, kd.step, kd.c23));
+          } else {
+            for (int gi = ct; gi < int(units * 4); gi += kConsumers)
+              __stcs(x4 + ((e0 >> 2) + gi), dequant4(cs[gi], kd.lo, kd.step));
           }
-          for (int gi = qct; gi < ng; gi += 2 * qn) {
-            const int g1 = gi + qn;
+          return;
+        }
+        r.slot_acquire();
+        const int ng = int(units * 4);
+        if (cache_y2) {
+          const float4* ys = reinterpret_cast<const float4*>(st);
+          for (int gi = ct; gi < ng; gi += kConsumers) {
+            const size_t e = e0 + 4 * size_t(gi);
+            const float4 v = ys[gi];  // y2 (- eps already applied in the fold)
+            const uint32_t q = quantize4(v, p2.lo, p2.inv);
+            *reinterpret_cast<uint32_t*>(out2 + (e - mlo)) = q;
+            const float4 d = dequant4(q, p2);
+            if (EC) reinterpret_cast<float4*>(a.eps)[(e - mlo) >> 2] = sub4(v, d);
+            __stcs(x4 + (e >> 2), d);
+          }
+        } else {
+          const bool fast = s_fast != 0;
+          for (int gi = ct; gi < ng; gi += 2 * kConsumers) {
+            const int g1 = gi + kConsumers;
             const bool has1 = g1 < ng;
             float4 y[2];
             fold2<kU8>(g, fast, st, gi, has1 ? g1 : gi, T, s_dec, 1.0, y[0], y[1]);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               if (h == 1 && !has1) break;
-              const int gg = h ? g1 : gi;
-              const size_t e = e0 + 4 * size_t(gg);
+              const size_t e = e0 + 4 * size_t(h ? g1 : gi);
               float4 v = y[h];
               if (EC) v = sub4(v, reinterpret_cast<const float4*>(a.eps)[(e - mlo) >> 2]);
               const uint32_t q = quantize4(v, p2.lo, p2.inv);
@@ -434,45 +458,21 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
               __stcs(x4 + (e >> 2), d);  // my own chunk of x: D2(Q2(y2))
             }
           }
-          r.slot_commit(reinterpret_cast<unsigned long long*>(a.win[me] + a.off_qgate) +
-                            ((e0 >> 4) - (mlo >> 4)) / kGateUnits,
-                        unsigned(units));
-        },
-        [](int) {});
-    if (r.group_a()) {
-      r.slot_acquire();
-      r.slot_commit(nullptr, 0u, true);
-    }
-    B2S_TRACE(kTrP2Done);
-  } else if (r.producer2 || r.group_b()) {
-    auto load_hdr = [&](int i) {
-      const int k = (me + 1 + i) % g;
-      const float2 h = ld_peer_f2(&hdr_at(a.win[k])->hdr2);
-      const U8Params q = u8_params(h.x, h.y);
-      s_dec3[i] = SrcDec{q.lo, q.step, q.c23};
-      s_fast3[i] = q.fastdec;
-    };
-    r.stream_at(
-        s_pp, g - 1, pq + 1,
-        [&](int i, const uint8_t* st, size_t e0, size_t units, int) {
-          const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
-          const SrcDec kd = s_dec3[i];
-          if (s_fast3[i]) {
-            for (int gi = qct; gi < int(units * 4); gi += qn)
-              __stcs(x4 + ((e0 >> 2) + gi), dequant4_fast(cs[gi], kd.lo, kd.step, kd.c23));
-          } else {
-            for (int gi = qct; gi < int(units * 4); gi += qn)
-              __stcs(x4 + ((e0 >> 2) + gi), dequant4(cs[gi], kd.lo, kd.step));
-          }
-        },
-        load_hdr);
-    B2S_TRACE_B(kTrP3First);
+        }
+        r.slot_commit_all(reinterpret_cast<unsigned long long*>(a.win[me] + a.off_qgate) +
+                              ((e0 >> 4) - (mlo >> 4)) / kGateUnits,
+                          unsigned(units));
+      },
+      load_hdr);
+  if (cons) {  // marker: the signaller confirms everything and stops
+    r.slot_acquire();
+    r.slot_commit_all(nullptr, 0u, true);
   }
-  r.split_end();
+  B2S_TRACE(kTrP2Done);
   r.npass = pq + g;
   if (a.trace) {
     unsigned long long* tw = a.trace + size_t(blockIdx.x) * kTraceSlots + kTrWait;
-    if (r.producer2 && threadIdx.x == kProducer2) tw[0] = r.wt[0];  // gather producer: gates
+    if (r.producer && threadIdx.x == 0) tw[3] = r.wt[0];  // Q-phase producer: gates
   }
   r.timed = false;
   B2S_TRACE(kTrEnd);

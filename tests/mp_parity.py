@@ -349,22 +349,42 @@ def run(args):
     ep.sync()
     ck.close("d_lp_s onebit back-to-back random topology", t.cpu().numpy(), cur[rank])
 
-    # ---- hierarchical_c over virtual node layouts (collectives.cpp:290-385)
+    # ---- hierarchical_c over virtual node layouts (collectives.cpp:290-385),
+    # on grid inputs (exact fp64 sums) and on mixed-magnitude gaussians
+    # (inexact sums: the lossless multi-node branch folds in a different fp64
+    # order than the reference, declared tolerance 1 fp32 ulp; lossy branches
+    # bit-exact, -0.0 included -- the down phase is a byte broadcast)
     layouts = {2: [[0, 1], [0, 0]], 3: [[0, 0, 1], [0, 1, 2]], 4: [[0, 0, 1, 1], [0, 1, 1, 2], [1, 0, 1, 0]]}
+
+    def gauss(n, seed):
+        rs = np.random.default_rng(seed)
+        v = (rs.standard_normal(n) * 10.0 ** rs.uniform(-6, 6, n)).astype(np.float32)
+        v[::97] = -0.0
+        return v
+
     for nodes in layouts.get(g, [[0] * g]):
+        multi = len(set(nodes)) > 1
         for codec_kind, codec in ((0, ID), (1, U8), (2, OB)):
-            for n in (37, 100_003):
+            for n, gen in ((37, "grid"), (100_003, "grid"), (100_003, "gauss")):
                 bucket += 1
-                xs = [orc.synth(n, 7700 + r) for r in range(g)]
+                xs = [orc.synth(n, 7700 + r) if gen == "grid" else gauss(n, 7800 + r) for r in range(g)]
                 want = [x.copy() for x in xs]
                 orc.hierarchical_c(want, nodes, codec_kind)
                 t = torch.as_tensor(xs[rank]).cuda()
                 b2.hierarchical_c(ep, 0.0, t, codec, None, bucket=bucket, nodes=nodes)
                 got = t.cpu().numpy()
-                if np.array_equal(got, want[rank]):  # == : a -0.0 leader value reaches members as +0.0
-                    ck.passed += 1
+                name = f"hierarchical_c nodes={nodes} codec={codec_kind} n={n} {gen}"
+                if codec_kind == 2:
+                    ck.close(name, got, want[rank])
+                elif codec_kind == 0 and multi and gen == "gauss":
+                    w = want[rank]
+                    ok = np.all(np.abs(got.astype(np.float64) - w) <= np.spacing(np.abs(w)))
+                    if ok:
+                        ck.passed += 1
+                    else:
+                        ck.fail.append(f"rank{rank} {name}: beyond 1 ulp")
                 else:
-                    ck.fail.append(f"rank{rank} hierarchical_c nodes={nodes} codec={codec_kind} n={n}")
+                    ck.eq(name, got, want[rank])
 
     # ---- interleaved buckets, non-blocking issue, one sync (overlap of buckets)
     bucket += 1
