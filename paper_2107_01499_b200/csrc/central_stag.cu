@@ -359,8 +359,18 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
 
   // =============================================== second header
   U8Params p2{};
+  __shared__ int s_slot;
+  __shared__ unsigned s_sph;
   if (cons) {
+    // only group A took credits in phase S: every consumer continues from
+    // its slot cursor (all of them take Q2's credits below)
+    if (r.ct == 0) {
+      s_slot = r.slot;
+      s_sph = r.sphase;
+    }
     const float2 m = consumer_minmax(lo2, hi2, redAll);
+    r.slot = s_slot;  // consumer_minmax's barriers order the write above
+    r.sphase = s_sph;
     if (r.ct == 0) a.partials[size_t(kMaxRanks) * G + blockIdx.x] = m;
     consumer_grid_sync(a.gridbar);
     float l2 = kInfS, h2 = -kInfS;
