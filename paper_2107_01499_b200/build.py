@@ -126,6 +126,29 @@ def build_host_test(force: bool = False) -> str | None:
     return HOST_TEST_BIN
 
 
+NVL_PROBE_SRC = os.path.join(REPO, "tests", "cpp", "nvl_probe.cpp")
+NVL_PROBE_BIN = os.path.join(REPO, "tests", "cpp", "nvl_probe")
+
+
+def build_nvl_probe(force: bool = False) -> str | None:
+    """Dev probe: every GPU in one process (thread per GPU) running a
+    primitive back to back, so ncu --devices 0 can count NVLink bytes."""
+    if not (os.path.exists(NVL_PROBE_SRC) and os.path.exists(HOSTLIB)):
+        return None
+    if not force and not _stale(NVL_PROBE_BIN, [NVL_PROBE_SRC, HOSTLIB, LIB]):
+        return NVL_PROBE_BIN
+    cmd = ["g++", "-std=c++20", "-O2", "-I", INCLUDE, "-I", "/usr/local/cuda/include", NVL_PROBE_SRC,
+           "-o", NVL_PROBE_BIN + ".tmp", "-L", PKG_DIR, "-lrcomm_b200", "-lb2comm", "-L/usr/local/cuda/lib64",
+           "-lcudart", "-lpthread", "-Wl,-rpath,$ORIGIN/../../paper_2107_01499_b200",
+           f"-Wl,-rpath,{PKG_DIR}:/usr/local/cuda/lib64"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("g++ failed on nvl_probe")
+    os.replace(NVL_PROBE_BIN + ".tmp", NVL_PROBE_BIN)
+    return NVL_PROBE_BIN
+
+
 REF_PROJ = "/root/reference/proj"
 DROPIN_SRC = os.path.join(REPO, "tests", "cpp", "algo_dropin.cpp")
 DROPIN_REF_BIN = os.path.join(REPO, "tests", "cpp", "algo_dropin_ref")

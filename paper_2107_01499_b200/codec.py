@@ -61,7 +61,12 @@ class Codec:
         return self.kind == CodecKind.identity
 
     def payload_size(self, n: int) -> int:
-        return int(lib.b2_payload_size(int(self.kind), n))
+        """codec.cpp:31-38 (cached per length: the per-call host cost matters for small buckets)."""
+        cache = self.__dict__.setdefault("_psize", {})
+        v = cache.get(n)
+        if v is None:
+            v = cache[n] = int(lib.b2_payload_size(int(self.kind), n))
+        return v
 
     def _check_supported(self, rng, collective: bool = True) -> None:
         if self.kind == CodecKind.uniform8 and self.rounding == Rounding.stochastic:
