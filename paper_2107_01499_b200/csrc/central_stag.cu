@@ -33,10 +33,14 @@
 //   pipe B                   gather: pull every other owner's out2 region by
 //                            region as it is published, decode into x
 //
-// Taken when every chunk is 16-element aligned (n % (16 g) == 0: the
-// BASELINE sizes); other shapes use central_kernel.  Results are identical
-// to central_kernel's (the same arithmetic per element, bit-exact vs the
-// reference).
+// Taken at g = 2 when every chunk is 16-element aligned (n % 32 == 0: the
+// BASELINE sizes; comm.cu).  Measured at 100M: g = 2
+// 0.360 ms against 0.381-0.386 for central_kernel; at g = 4 the landing and
+// the fold (7 warps, fp64) finish ~55 us after the last encode and the split
+// gather pulls at ~440 GB/s, 0.488 against 0.428 ms -- so g >= 3 keeps
+// central_kernel (B2_STAG=<g> forces this kernel for A/B runs).  Results are
+// identical to central_kernel's (the same arithmetic per element, bit-exact
+// vs the reference).
 #include <cuda_runtime.h>
 
 #include "b2_host.h"
@@ -359,18 +363,8 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
 
   // =============================================== second header
   U8Params p2{};
-  __shared__ int s_slot;
-  __shared__ unsigned s_sph;
   if (cons) {
-    // only group A took credits in phase S: every consumer continues from
-    // its slot cursor (all of them take Q2's credits below)
-    if (r.ct == 0) {
-      s_slot = r.slot;
-      s_sph = r.sphase;
-    }
     const float2 m = consumer_minmax(lo2, hi2, redAll);
-    r.slot = s_slot;  // consumer_minmax's barriers order the write above
-    r.sphase = s_sph;
     if (r.ct == 0) a.partials[size_t(kMaxRanks) * G + blockIdx.x] = m;
     consumer_grid_sync(a.gridbar);
     float l2 = kInfS, h2 = -kInfS;
@@ -391,74 +385,50 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
   }
   B2S_TRACE(kTrP2A);
 
-  // =============================================== Q2 + gather, one ring
-  // Q2 (local: y2 -> out2, my own chunk of x) and the gather of every other
-  // owner's out2 (NVLink, each region as soon as its owner published it)
-  // share all stages and consumer warps: the producer serves Q2 tiles while
-  // no remote region is ready.  (Split pipes starve the gather: 2 stages and
-  // 7 warps pulled at ~440 GB/s.)
+  // =============================================== Q2 || gather
   r.timed = a.trace != nullptr;
+  r.split_begin();
+  const int qct = r.gct, qn = r.gn;
+  if (r.storer && (threadIdx.x & 31) == 0) r.signal_loop();  // Q2's publication credits
   const int pq = 2 * (g + 1) + g;
   uint8_t* out2 = a.win[me] + a.off_out2;
-  __shared__ PassDesc s_q3[kMaxRanks];  // [0]: Q2, [1 + i]: gather of owner (me+1+i)
-  if (threadIdx.x == 0) {
-    s_q3[0] = s_q;
-    for (int i = 0; i + 1 < g; ++i) s_q3[1 + i] = s_pp[i];
-  }
-  __syncthreads();
-  if (r.storer && (threadIdx.x & 31) == 0) r.signal_loop();  // Q2's publication credits
-  if (r.producer && (threadIdx.x & 31) == 0) {  // Q2 streams data other CTAs wrote in phase S
-    while (s_qgo == 0) __nanosleep(32);
-    fence_proxy_async();
-  }
-  auto load_hdr = [&](int i) {
-    if (i == 0) return;
-    const int k = (me + i) % g;
-    const float2 h = ld_peer_f2(&hdr_at(a.win[k])->hdr2);
-    const U8Params q = u8_params(h.x, h.y);
-    s_dec3[i] = SrcDec{q.lo, q.step, q.c23};
-    s_fast3[i] = q.fastdec;
-  };
-  r.stream_at(
-      s_q3, g, pq,
-      [&](int i, const uint8_t* st, size_t e0, size_t units, int T) {
-        const int ct = r.ct;
-        if (i > 0) {  // gather: owner (me+i)'s out2 -> x
-          const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
-          const SrcDec kd = s_dec3[i];
-          if (s_fast3[i]) {
-            for (int gi = ct; gi < int(units * 4); gi += kConsumers)
-              __stcs(x4 + ((e0 >> 2) + gi), dequant4_fast(cs[gi], kd.lo, kd.step, kd.c23));
-          } else {
-            for (int gi = ct; gi < int(units * 4); gi += kConsumers)
-              __stcs(x4 + ((e0 >> 2) + gi), dequant4(cs[gi], kd.lo, kd.step));
-          }
-          return;
-        }
-        r.slot_acquire();
-        const int ng = int(units * 4);
-        if (cache_y2) {
-          const float4* ys = reinterpret_cast<const float4*>(st);
-          for (int gi = ct; gi < ng; gi += kConsumers) {
-            const size_t e = e0 + 4 * size_t(gi);
-            const float4 v = ys[gi];  // y2 (- eps already applied in the fold)
-            const uint32_t q = quantize4(v, p2.lo, p2.inv);
-            *reinterpret_cast<uint32_t*>(out2 + (e - mlo)) = q;
-            const float4 d = dequant4(q, p2);
-            if (EC) reinterpret_cast<float4*>(a.eps)[(e - mlo) >> 2] = sub4(v, d);
-            __stcs(x4 + (e >> 2), d);
-          }
-        } else {
+  if (r.producer || r.group_a()) {
+    if (r.producer && (threadIdx.x & 31) == 0) {  // Q2 streams data other CTAs wrote in phase S
+      while (s_qgo == 0) __nanosleep(32);
+      fence_proxy_async();
+    }
+    r.stream_at(
+        &s_q, 1, pq,
+        [&](int, const uint8_t* st, size_t e0, size_t units, int T) {
           const bool fast = s_fast != 0;
-          for (int gi = ct; gi < ng; gi += 2 * kConsumers) {
-            const int g1 = gi + kConsumers;
+          const int ng = int(units * 4);
+          r.slot_acquire();
+          if (cache_y2) {
+            const float4* ys = reinterpret_cast<const float4*>(st);
+            for (int gi = qct; gi < ng; gi += qn) {
+              const size_t e = e0 + 4 * size_t(gi);
+              const float4 v = ys[gi];  // y2 (- eps already applied in the fold)
+              const uint32_t q = quantize4(v, p2.lo, p2.inv);
+              *reinterpret_cast<uint32_t*>(out2 + (e - mlo)) = q;
+              const float4 d = dequant4(q, p2);
+              if (EC) reinterpret_cast<float4*>(a.eps)[(e - mlo) >> 2] = sub4(v, d);
+              __stcs(x4 + (e >> 2), d);
+            }
+            r.slot_commit(reinterpret_cast<unsigned long long*>(a.win[me] + a.off_qgate) +
+                              ((e0 >> 4) - (mlo >> 4)) / kGateUnits,
+                          unsigned(units));
+            return;
+          }
+          for (int gi = qct; gi < ng; gi += 2 * qn) {
+            const int g1 = gi + qn;
             const bool has1 = g1 < ng;
             float4 y[2];
             fold2<kU8>(g, fast, st, gi, has1 ? g1 : gi, T, s_dec, 1.0, y[0], y[1]);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               if (h == 1 && !has1) break;
-              const size_t e = e0 + 4 * size_t(h ? g1 : gi);
+              const int gg = h ? g1 : gi;
+              const size_t e = e0 + 4 * size_t(gg);
               float4 v = y[h];
               if (EC) v = sub4(v, reinterpret_cast<const float4*>(a.eps)[(e - mlo) >> 2]);
               const uint32_t q = quantize4(v, p2.lo, p2.inv);
@@ -468,21 +438,45 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
               __stcs(x4 + (e >> 2), d);  // my own chunk of x: D2(Q2(y2))
             }
           }
-        }
-        r.slot_commit_all(reinterpret_cast<unsigned long long*>(a.win[me] + a.off_qgate) +
-                              ((e0 >> 4) - (mlo >> 4)) / kGateUnits,
-                          unsigned(units));
-      },
-      load_hdr);
-  if (cons) {  // marker: the signaller confirms everything and stops
-    r.slot_acquire();
-    r.slot_commit_all(nullptr, 0u, true);
+          r.slot_commit(reinterpret_cast<unsigned long long*>(a.win[me] + a.off_qgate) +
+                            ((e0 >> 4) - (mlo >> 4)) / kGateUnits,
+                        unsigned(units));
+        },
+        [](int) {});
+    if (r.group_a()) {
+      r.slot_acquire();
+      r.slot_commit(nullptr, 0u, true);
+    }
+    B2S_TRACE(kTrP2Done);
+  } else if (r.producer2 || r.group_b()) {
+    auto load_hdr = [&](int i) {
+      const int k = (me + 1 + i) % g;
+      const float2 h = ld_peer_f2(&hdr_at(a.win[k])->hdr2);
+      const U8Params q = u8_params(h.x, h.y);
+      s_dec3[i] = SrcDec{q.lo, q.step, q.c23};
+      s_fast3[i] = q.fastdec;
+    };
+    r.stream_at(
+        s_pp, g - 1, pq + 1,
+        [&](int i, const uint8_t* st, size_t e0, size_t units, int) {
+          const uint32_t* cs = reinterpret_cast<const uint32_t*>(st);
+          const SrcDec kd = s_dec3[i];
+          if (s_fast3[i]) {
+            for (int gi = qct; gi < int(units * 4); gi += qn)
+              __stcs(x4 + ((e0 >> 2) + gi), dequant4_fast(cs[gi], kd.lo, kd.step, kd.c23));
+          } else {
+            for (int gi = qct; gi < int(units * 4); gi += qn)
+              __stcs(x4 + ((e0 >> 2) + gi), dequant4(cs[gi], kd.lo, kd.step));
+          }
+        },
+        load_hdr);
+    B2S_TRACE_B(kTrP3First);
   }
-  B2S_TRACE(kTrP2Done);
+  r.split_end();
   r.npass = pq + g;
   if (a.trace) {
     unsigned long long* tw = a.trace + size_t(blockIdx.x) * kTraceSlots + kTrWait;
-    if (r.producer && threadIdx.x == 0) tw[3] = r.wt[0];  // Q-phase producer: gates
+    if (r.producer2 && threadIdx.x == kProducer2) tw[0] = r.wt[0];  // gather producer: gates
   }
   r.timed = false;
   B2S_TRACE(kTrEnd);

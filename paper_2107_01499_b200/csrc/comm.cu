@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <map>
@@ -518,11 +519,12 @@ int b2_comm_sync(b2_comm_t c, void* stream) {
   return b2_comm_poll(c);
 }
 
-// B2_STAG=0: the pre-staggered C_LP_S kernel for every shape (A/B measurements)
-static bool stag_enabled() {
-  static const bool v = [] {
+// The world size that takes the staggered C_LP_S (default 2; B2_STAG=0
+// disables it, B2_STAG=<g> selects another world size for A/B measurements)
+static int stag_world() {
+  static const int v = [] {
     const char* e = getenv("B2_STAG");
-    return !(e && e[0] == '0');
+    return e ? std::atoi(e) : 2;
   }();
   return v;
 }
@@ -579,9 +581,10 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   a.status = w->fail;
   a.timeout_ns = c->timeout_ns;
   a.trace = c->trace;
-  // uint8 at g >= 2 with 16-aligned equal chunks: the staggered schedule
-  // (central_stag.cu); every rank decides identically from (n, g)
-  if (codec == B2_CODEC_UNIFORM8 && c->world >= 2 && n % (16 * size_t(c->world)) == 0 && stag_enabled() &&
+  // uint8 at g == 2 with 16-aligned equal chunks: the staggered schedule
+  // (central_stag.cu; measured faster at g = 2 only); every
+  // rank decides identically from (n, g)
+  if (codec == B2_CODEC_UNIFORM8 && c->world == stag_world() && n % (16 * size_t(c->world)) == 0 &&
       (!eps || (reinterpret_cast<uintptr_t>(eps) & 15) == 0))
     rc = launch_central_stag(a, delta != nullptr, static_cast<cudaStream_t>(stream), c->sm_budget);
   else

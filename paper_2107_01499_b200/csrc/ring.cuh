@@ -415,19 +415,6 @@ struct Ring {
     if ((threadIdx.x & 31) == 0) mbar_arrive(staged + slot);
     advance_slot();
   }
-  // Outside split mode every consumer warp works on every tile: all of them
-  // sync, then group A's warps (the ones the staged barriers count) arrive.
-  __device__ __forceinline__ void slot_commit_all(unsigned long long* sig, unsigned sigv, bool marker = false) {
-    if (ct == 0) {
-      slot_sig[slot] = sig;
-      slot_sigv[slot] = sigv;
-      slot_len[slot] = marker ? 0u : 1u;
-    }
-    fence_proxy_async();
-    consumer_sync();
-    if (group_a() && (threadIdx.x & 31) == 0) mbar_arrive(staged + slot);
-    advance_slot();
-  }
   // signaller lane 0: serve credits until the marker; returns after it.
   // emit(sig, value) performs one credit's signal after the batch fence
   // (default: a relaxed system-scope red on sig).
