@@ -391,6 +391,11 @@ def run_b200(args, rank: int, world: int):
         roof = {"bound": "hbm", "achieved": round(hbm_b / t_s / 1e9, 2), "peak": hbm_peak, "unit": "GB/s",
                 "peak_kind": f"{peak_kind} HBM copy (MEASURED_PEAKS.json)"}
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4) if roof["bound"] != "none" else None
+    if nvl_b:  # the NVLink leg against both peaks (BASELINE.md 3 / SURVEY.md 8d quote the 900 GB/s nominal)
+        roof["nvlink"] = {"achieved": round(nvl_b / t_s / 1e9, 2),
+                          "frac_measured_770": round(nvl_b / t_s / 1e9 / NVL_PEER_GBS, 4),
+                          "frac_nominal_900": round(nvl_b / t_s / 1e9 / NVL_NOMINAL_GBS, 4)}
+        roof["hbm_leg"] = {"achieved": round(hbm_b / t_s / 1e9, 2), "frac": round(hbm_b / t_s / 1e9 / hbm_peak, 4)}
     roof["traffic"] = args.traffic if args.traffic is not None else ncu_traffic(prim, g)
     roof["algorithmic_bytes"] = {"hbm": hbm_b, "nvlink_ingress": nvl_b}
     roof["t_roof_us"] = round(max(t_roof_hbm, t_roof_nvl) * 1e6, 1)
@@ -426,6 +431,10 @@ def run_b200(args, rank: int, world: int):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if world > 1:  # every rank's GPU clocks during its timed region (run-to-run spread)
+        per = [None] * world
+        dist.all_gather_object(per, {"rank": rank, "device": dev, **clk.summary()})
+        line["clocks_per_rank"] = per
     if rank == 0 and world == 1 and not args.no_cpu_baseline and prim != "c_fp_s":
         n_sample = min(n, args.cpu_sample or n)
         secs, backend = cpu_reference_gbs(PRIMS[prim][1], 1, n_sample, 4)

@@ -416,7 +416,7 @@ int b2_comm_enable_trace(b2_comm_t c, int on) {
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard dg(c->device);
   if (on && !c->trace) {
-    c->trace_grid = max_persistent_grid();
+    c->trace_grid = std::max(max_persistent_grid(), int(kSmallMaxGridD));  // small_coll.cu grids reach 1024
     B2_CUDA_TRY(cudaMalloc(&c->trace, sizeof(unsigned long long) * kTraceSlots * c->trace_grid));
     B2_CUDA_TRY(cudaMemset(c->trace, 0, sizeof(unsigned long long) * kTraceSlots * c->trace_grid));
   } else if (!on && c->trace) {

@@ -57,6 +57,9 @@ __global__ void __launch_bounds__(kSmallThr) decent_small_kernel(DecentArgs a) {
   float4* x4 = reinterpret_cast<float4*>(a.x);
   WinHdr* mine = whdr(a.win[me]);
   if (threadIdx.x == 0) s_bad = 0;
+  // phase stamps (b2_comm_enable_trace): start, header final, published, neighbours in, end
+  unsigned long long* tr = a.trace ? a.trace + size_t(b) * kTraceSlots : nullptr;
+  if (tr && threadIdx.x == 0) tr[kTrStart] = globaltimer();
   // ---- 1: x into registers
   float4 y[R];
   float yt[3] = {0.f, 0.f, 0.f};
@@ -111,6 +114,7 @@ __global__ void __launch_bounds__(kSmallThr) decent_small_kernel(DecentArgs a) {
     hi = warp_max_nan(v.y);
     q = u8_params(lo, hi);
     if (gt == 0 && n && !(finite_f(lo) && finite_f(hi))) latch(a.status, kStatusNonFinite);
+    if (tr && threadIdx.x == 0) tr[kTrP1FirstA] = globaltimer();
   }
   uint32_t c[R];
   uint8_t ct[3] = {0, 0, 0};
@@ -171,6 +175,7 @@ __global__ void __launch_bounds__(kSmallThr) decent_small_kernel(DecentArgs a) {
                             size_t(me) * a.gate_stride + b,
                         1ull);
   }
+  if (tr && threadIdx.x == 0) tr[kTrP1Done] = globaltimer();
   // ---- 4: wait for every neighbour's CTA b, fold in ascending neighbour order
   __shared__ SrcDecS s_dec[kMaxRanks];
   if (threadIdx.x < a.nnb) {
@@ -185,6 +190,7 @@ __global__ void __launch_bounds__(kSmallThr) decent_small_kernel(DecentArgs a) {
     }
   }
   __syncthreads();
+  if (tr && threadIdx.x == 0) tr[kTrP2Ready] = globaltimer();
   const double inv = a.inv;
 #pragma unroll
   for (int k = 0; k < R; ++k) {
@@ -236,6 +242,7 @@ __global__ void __launch_bounds__(kSmallThr) decent_small_kernel(DecentArgs a) {
   if (threadIdx.x == 0) {
     if (s_bad) latch(a.status, kStatusNonFinite);
     fail_epilogue(a.status);
+    if (tr) tr[kTrEnd] = globaltimer();
   }
 }
 
