@@ -45,7 +45,10 @@ constexpr int kSmallMaxGrid = int(kSmallMaxGridD);  // per-source CTA counters (
 
 __device__ __forceinline__ WinHdr* whdr(uint8_t* w) { return reinterpret_cast<WinHdr*>(w); }
 
-template <int CODEC, int R>
+// NB > 0: the neighbourhood size is a compile-time constant (every remote load
+// of a thread is issued before the fold: one NVLink round trip); NB = 0:
+// runtime size, loads interleaved with the fold.
+template <int CODEC, int R, int NB>
 __global__ void __launch_bounds__(kSmallThr) decent_small_kernel(DecentArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ float2 wred[kSmallThr / 32];
@@ -170,7 +173,9 @@ __global__ void __launch_bounds__(kSmallThr) decent_small_kernel(DecentArgs a) {
   if (CODEC == kU8 && threadIdx.x == 0) mine->dhdr[p] = make_float2(lo, hi);
   __syncthreads();
   if (threadIdx.x < a.nnb && a.nbrs[threadIdx.x] != me) {
-    __threadfence_system();  // the CTA's stores (ordered by bar.sync) before the signal
+    // the CTA's stores (ordered by bar.sync) before the signal; peers read
+    // this buffer through this GPU's L2, so gpu scope suffices for the data
+    __threadfence();
     red_relaxed_sys_add(reinterpret_cast<unsigned long long*>(a.win[a.nbrs[threadIdx.x]] + a.off_gate) +
                             size_t(me) * a.gate_stride + b,
                         1ull);
@@ -192,20 +197,48 @@ __global__ void __launch_bounds__(kSmallThr) decent_small_kernel(DecentArgs a) {
   __syncthreads();
   if (tr && threadIdx.x == 0) tr[kTrP2Ready] = globaltimer();
   const double inv = a.inv;
+  constexpr int NBX = NB > 0 ? NB : 1;
+  const int nnb = NB > 0 ? NB : a.nnb;
+  // NB > 0: every remote load of this thread first (one NVLink round trip)
+  uint32_t rc[R][NBX];
+  float4 rf[CODEC == kU8 ? 1 : R][CODEC == kU8 ? 1 : NBX];
+  if (NB > 0) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const size_t g = gt + size_t(k) * T;
+#pragma unroll
+      for (int i = 0; i < NBX; ++i) {
+        const int j = a.nbrs[i];
+        if (g < ng && j != me) {
+          if (CODEC == kU8)
+            rc[k][i] = __ldcg(reinterpret_cast<const uint32_t*>(a.win[j] + a.off_dbuf) + g);
+          else
+            rf[CODEC == kU8 ? 0 : k][CODEC == kU8 ? 0 : i] =
+                __ldcg(reinterpret_cast<const float4*>(a.win[j] + a.off_dbuf) + g);
+        }
+      }
+    }
+  }
 #pragma unroll
   for (int k = 0; k < R; ++k) {
     const size_t g = gt + size_t(k) * T;
     if (g < ng) {
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      for (int i = 0; i < a.nnb; ++i) {
+#pragma unroll
+      for (int i = 0; i < (NB > 0 ? NBX : kMaxRanks); ++i) {
+        if (NB == 0 && i >= nnb) break;
         const int j = a.nbrs[i];
         float4 d;
         if (CODEC == kU8) {
-          const uint32_t cj = j == me ? c[k] : __ldcg(reinterpret_cast<const uint32_t*>(a.win[j] + a.off_dbuf) + g);
+          const uint32_t cj = j == me ? c[k]
+                              : NB > 0 ? rc[k][NB > 0 ? i : 0]
+                                       : __ldcg(reinterpret_cast<const uint32_t*>(a.win[j] + a.off_dbuf) + g);
           const SrcDecS sd = s_dec[i];
           d = sd.fast ? dequant4_fast(cj, sd.lo, sd.step, sd.c23) : dequant4(cj, sd.lo, sd.step);
         } else {
-          d = j == me ? y[k] : __ldcg(reinterpret_cast<const float4*>(a.win[j] + a.off_dbuf) + g);
+          d = j == me ? y[k]
+              : NB > 0 ? rf[CODEC == kU8 ? 0 : k][CODEC == kU8 ? 0 : (NB > 0 ? i : 0)]
+                       : __ldcg(reinterpret_cast<const float4*>(a.win[j] + a.off_dbuf) + g);
         }
         a0 = __dadd_rn(a0, double(d.x));
         a1 = __dadd_rn(a1, double(d.y));
@@ -235,10 +268,8 @@ __global__ void __launch_bounds__(kSmallThr) decent_small_kernel(DecentArgs a) {
   // ---- 5: my reads of CTA b's elements are done: acknowledge to every neighbour
   if (bad) atomicOr(&s_bad, 1);
   __syncthreads();
-  if (threadIdx.x < a.nnb && a.nbrs[threadIdx.x] != me) {
-    fence_acq_rel_sys();
+  if (threadIdx.x < a.nnb && a.nbrs[threadIdx.x] != me)  // every remote load of the CTA was consumed above
     red_relaxed_sys_add(&whdr(a.win[a.nbrs[threadIdx.x]])->dreads[p], 1ull);
-  }
   if (threadIdx.x == 0) {
     if (s_bad) latch(a.status, kStatusNonFinite);
     fail_epilogue(a.status);
@@ -248,7 +279,9 @@ __global__ void __launch_bounds__(kSmallThr) decent_small_kernel(DecentArgs a) {
 
 template <int CODEC, int R>
 int try_small(const DecentArgs& a, cudaStream_t s, int sms) {
-  const void* fn = reinterpret_cast<const void*>(decent_small_kernel<CODEC, R>);
+  const void* fn = a.nnb == 2   ? reinterpret_cast<const void*>(decent_small_kernel<CODEC, R, 2>)
+                   : a.nnb == 3 ? reinterpret_cast<const void*>(decent_small_kernel<CODEC, R, 3>)
+                                : reinterpret_cast<const void*>(decent_small_kernel<CODEC, R, 0>);
   const int per_sm = occupancy(fn, kSmallThr);
   const int nsm = sms > 0 && sms < sm_count() ? sms : sm_count();
   const size_t cap = size_t(nsm) * size_t(per_sm > 0 ? per_sm : 0);
