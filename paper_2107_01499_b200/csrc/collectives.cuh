@@ -120,7 +120,7 @@ struct SrcDecS {
 // Buckets up to this many elements try the register-resident D_* kernel
 // (small_coll.cu) before the TMA ring; its per-CTA counters need
 // gate_stride > kSmallMaxGridD.
-constexpr size_t kSmallDecentMax = 4000000;
+constexpr size_t kSmallDecentMax = 16000000;
 constexpr size_t kSmallMaxGridD = 1024;
 
 // Decentralized neighbourhood reduce (D_FP_S, D_LP_S).

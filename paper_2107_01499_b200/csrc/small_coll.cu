@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -277,6 +278,203 @@ __global__ void __launch_bounds__(kSmallThr) decent_small_kernel(DecentArgs a) {
   }
 }
 
+// Buckets beyond the register capacity (4M-25M elements): the same per-CTA
+// protocol, streaming -- x is read for the (min, max), again (from L2) to
+// quantize into my window, and my own codes are re-read for the self term.
+template <int CODEC>
+__global__ void __launch_bounds__(kSmallThr) decent_stream_kernel(DecentArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ float2 wred[kSmallThr / 32];
+  __shared__ int s_bad;
+  __shared__ SrcDecS s_dec[kMaxRanks];
+  const int me = a.me, p = a.parity, b = blockIdx.x;
+  const size_t T = size_t(gridDim.x) * kSmallThr, gt = size_t(b) * kSmallThr + threadIdx.x;
+  const size_t n = a.n, ng = n >> 2;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  float4* x4 = reinterpret_cast<float4*>(a.x);
+  WinHdr* mine = whdr(a.win[me]);
+  uint8_t* mybuf = a.win[me] + a.off_dbuf;
+  if (threadIdx.x == 0) s_bad = 0;
+  unsigned long long* tr = a.trace ? a.trace + size_t(b) * kTraceSlots : nullptr;
+  if (tr && threadIdx.x == 0) tr[kTrStart] = globaltimer();
+  const bool tail = gt == T - 1 && (n & 3);
+  int bad = 0;
+  U8Params q{};
+  float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
+  if (CODEC == kU8) {  // ---- 1-2: the bucket's (min, max), collectives.cpp:266
+    for (size_t g = gt; g < ng; g += T) {
+      const float4 v = __ldcg(x4 + g);
+      lo = fmin_nan(lo, fmin_nan(fmin_nan(v.x, v.y), fmin_nan(v.z, v.w)));
+      hi = fmax_nan(hi, fmax_nan(fmax_nan(v.x, v.y), fmax_nan(v.z, v.w)));
+    }
+    if (tail)
+      for (size_t e = 4 * ng; e < n; ++e) {
+        lo = fmin_nan(lo, a.x[e]);
+        hi = fmax_nan(hi, a.x[e]);
+      }
+    lo = warp_min_nan(lo);
+    hi = warp_max_nan(hi);
+    if (l == 0) wred[w] = make_float2(lo, hi);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const float2 v = l < kSmallThr / 32 ? wred[l] : wred[0];
+      const float mn = warp_min_nan(v.x), mx = warp_max_nan(v.y);
+      if (l == 0) a.partials[b] = make_float2(mn, mx);
+    }
+    grid.sync();
+    lo = __int_as_float(0x7f800000);
+    hi = -__int_as_float(0x7f800000);
+    for (unsigned c = threadIdx.x; c < gridDim.x; c += kSmallThr) {
+      const float2 v = __ldcg(a.partials + c);
+      lo = fmin_nan(lo, v.x);
+      hi = fmax_nan(hi, v.y);
+    }
+    lo = warp_min_nan(lo);
+    hi = warp_max_nan(hi);
+    __syncthreads();
+    if (l == 0) wred[w] = make_float2(lo, hi);
+    __syncthreads();
+    const float2 v = l < kSmallThr / 32 ? wred[l] : wred[0];
+    lo = warp_min_nan(v.x);
+    hi = warp_max_nan(v.y);
+    q = u8_params(lo, hi);
+    if (gt == 0 && n && !(finite_f(lo) && finite_f(hi))) latch(a.status, kStatusNonFinite);
+    if (tr && threadIdx.x == 0) tr[kTrP1FirstA] = globaltimer();
+  }
+  if (a.nnb == 1) {  // {self}: x' = D(Q(x)) + 0.0f (identity: x + 0.0f)
+    for (size_t g = gt; g < ng; g += T) {
+      const float4 v = x4[g];
+      if (CODEC != kU8 && a.check_finite) bad |= !(finite_f(v.x) && finite_f(v.y) && finite_f(v.z) && finite_f(v.w));
+      const float4 d = CODEC == kU8 ? dequant4(quantize4(v, q.lo, q.inv), q) : v;
+      x4[g] = make_float4(__fadd_rn(d.x, 0.0f), __fadd_rn(d.y, 0.0f), __fadd_rn(d.z, 0.0f), __fadd_rn(d.w, 0.0f));
+    }
+    if (tail)
+      for (size_t e = 4 * ng; e < n; ++e) {
+        if (CODEC != kU8 && a.check_finite) bad |= !finite_f(a.x[e]);
+        a.x[e] = __fadd_rn(CODEC == kU8 ? dequant1(quantize1(a.x[e], q.lo, q.inv), q) : a.x[e], 0.0f);
+      }
+    if (bad) atomicOr(&s_bad, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (s_bad) latch(a.status, kStatusNonFinite);
+      fail_epilogue(a.status);
+    }
+    return;
+  }
+  // ---- 3: publish CTA b's elements
+  if (threadIdx.x == 0 && a.expected_reads)
+    wait_geq(&mine->dreads[p], a.expected_reads * gridDim.x, a.timeout_ns, a.status);
+  __syncthreads();
+  for (size_t g = gt; g < ng; g += T) {
+    const float4 v = x4[g];
+    if (CODEC == kU8) {
+      reinterpret_cast<uint32_t*>(mybuf)[g] = quantize4(v, q.lo, q.inv);
+    } else {
+      reinterpret_cast<float4*>(mybuf)[g] = v;
+      if (a.check_finite) bad |= !(finite_f(v.x) && finite_f(v.y) && finite_f(v.z) && finite_f(v.w));
+    }
+  }
+  if (tail)
+    for (size_t e = 4 * ng; e < n; ++e) {
+      if (CODEC == kU8) {
+        mybuf[e] = quantize1(a.x[e], q.lo, q.inv);
+      } else {
+        reinterpret_cast<float*>(mybuf)[e] = a.x[e];
+        if (a.check_finite) bad |= !finite_f(a.x[e]);
+      }
+    }
+  if (CODEC == kU8 && threadIdx.x == 0) mine->dhdr[p] = make_float2(lo, hi);
+  __syncthreads();
+  if (threadIdx.x < a.nnb && a.nbrs[threadIdx.x] != me) {
+    __threadfence();  // peers read this buffer through this GPU's L2
+    red_relaxed_sys_add(reinterpret_cast<unsigned long long*>(a.win[a.nbrs[threadIdx.x]] + a.off_gate) +
+                            size_t(me) * a.gate_stride + b,
+                        1ull);
+  }
+  if (tr && threadIdx.x == 0) tr[kTrP1Done] = globaltimer();
+  // ---- 4: every neighbour's CTA b in, fold in ascending neighbour order
+  if (threadIdx.x < a.nnb) {
+    const int j = a.nbrs[threadIdx.x];
+    if (j != me)
+      wait_geq(reinterpret_cast<const unsigned long long*>(a.win[me] + a.off_gate) + size_t(j) * a.gate_stride + b,
+               a.sends[threadIdx.x], a.timeout_ns, a.status);
+    if (CODEC == kU8) {
+      const float2 h = j == me ? make_float2(lo, hi) : __ldcg(&whdr(a.win[j])->dhdr[p]);
+      const U8Params qj = u8_params(h.x, h.y);
+      s_dec[threadIdx.x] = SrcDecS{qj.lo, qj.step, qj.c23, qj.fastdec ? 1 : 0};
+    }
+  }
+  __syncthreads();
+  if (tr && threadIdx.x == 0) tr[kTrP2Ready] = globaltimer();
+  const double inv = a.inv;
+  const int nnb = a.nnb;
+  for (size_t g = gt; g < ng; g += T) {
+    uint32_t cw[kMaxRanks];
+    float4 fw[CODEC == kU8 ? 1 : kMaxRanks];
+#pragma unroll
+    for (int i = 0; i < kMaxRanks; ++i)  // every load of this group first: one NVLink round trip
+      if (i < nnb) {
+        const uint8_t* src = a.win[a.nbrs[i]] + a.off_dbuf;
+        if (CODEC == kU8)
+          cw[i] = __ldcg(reinterpret_cast<const uint32_t*>(src) + g);
+        else
+          fw[CODEC == kU8 ? 0 : i] = __ldcg(reinterpret_cast<const float4*>(src) + g);
+      }
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int i = 0; i < kMaxRanks; ++i)
+      if (i < nnb) {
+        float4 d;
+        if (CODEC == kU8) {
+          const SrcDecS sd = s_dec[i];
+          d = sd.fast ? dequant4_fast(cw[i], sd.lo, sd.step, sd.c23) : dequant4(cw[i], sd.lo, sd.step);
+        } else {
+          d = fw[CODEC == kU8 ? 0 : i];
+        }
+        a0 = __dadd_rn(a0, double(d.x));
+        a1 = __dadd_rn(a1, double(d.y));
+        a2 = __dadd_rn(a2, double(d.z));
+        a3 = __dadd_rn(a3, double(d.w));
+      }
+    __stcs(x4 + g, make_float4(__double2float_rn(__dmul_rn(a0, inv)), __double2float_rn(__dmul_rn(a1, inv)),
+                               __double2float_rn(__dmul_rn(a2, inv)), __double2float_rn(__dmul_rn(a3, inv))));
+  }
+  if (tail)
+    for (size_t e = 4 * ng; e < n; ++e) {
+      double acc = 0.0;
+      for (int i = 0; i < nnb; ++i) {
+        const uint8_t* src = a.win[a.nbrs[i]] + a.off_dbuf;
+        const float d = CODEC == kU8 ? dequant1(__ldcg(src + e), s_dec[i].lo, s_dec[i].step)
+                                     : __ldcg(reinterpret_cast<const float*>(src) + e);
+        acc = __dadd_rn(acc, double(d));
+      }
+      a.x[e] = __double2float_rn(__dmul_rn(acc, inv));
+    }
+  // ---- 5: acknowledge the reads
+  if (bad) atomicOr(&s_bad, 1);
+  __syncthreads();
+  if (threadIdx.x < a.nnb && a.nbrs[threadIdx.x] != me)
+    red_relaxed_sys_add(&whdr(a.win[a.nbrs[threadIdx.x]])->dreads[p], 1ull);
+  if (threadIdx.x == 0) {
+    if (s_bad) latch(a.status, kStatusNonFinite);
+    fail_epilogue(a.status);
+    if (tr) tr[kTrEnd] = globaltimer();
+  }
+}
+
+template <int CODEC>
+int try_stream(const DecentArgs& a, cudaStream_t s, int sms) {
+  const void* fn = reinterpret_cast<const void*>(decent_stream_kernel<CODEC>);
+  const int per_sm = occupancy(fn, kSmallThr);
+  if (per_sm < 1) return B2_ERR_UNSUPPORTED;
+  const int nsm = sms > 0 && sms < sm_count() ? sms : sm_count();
+  const int grid = std::min(nsm * per_sm, kSmallMaxGrid);
+  DecentArgs copy = a;
+  void* params[] = {&copy};
+  B2_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kSmallThr), params, 0, s));
+  return B2_OK;
+}
+
 template <int CODEC, int R>
 int try_small(const DecentArgs& a, cudaStream_t s, int sms) {
   const void* fn = a.nnb == 2   ? reinterpret_cast<const void*>(decent_small_kernel<CODEC, R, 2>)
@@ -304,6 +502,7 @@ int small_decent(const DecentArgs& a, cudaStream_t s, int sms) {
   int rc = try_small<CODEC, 2>(a, s, sms);
   if (rc == B2_ERR_UNSUPPORTED) rc = try_small<CODEC, 4>(a, s, sms);
   if (rc == B2_ERR_UNSUPPORTED) rc = try_small<CODEC, 8>(a, s, sms);
+  if (rc == B2_ERR_UNSUPPORTED) rc = try_stream<CODEC>(a, s, sms);
   return rc;
 }
 
@@ -313,7 +512,11 @@ int small_decent(const DecentArgs& a, cudaStream_t s, int sms) {
 // (the caller then takes the TMA-ring kernel).  The choice depends only on
 // (n, SM count, budget), so all ranks of a window take the same path.
 int launch_decent_small(const DecentArgs& a, int codec, cudaStream_t s, int sms) {
-  if (a.n > kSmallDecentMax) return B2_ERR_UNSUPPORTED;
+  static const size_t limit = [] {  // B2_SMALL_MAX=<elements> moves the cut-over (A/B runs)
+    const char* e = getenv("B2_SMALL_MAX");
+    return e ? size_t(std::strtoull(e, nullptr, 10)) : kSmallDecentMax;
+  }();
+  if (a.n > limit) return B2_ERR_UNSUPPORTED;
   return codec == kU8 ? small_decent<kU8>(a, s, sms) : small_decent<kIdentity>(a, s, sms);
 }
 

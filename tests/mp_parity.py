@@ -242,6 +242,24 @@ def run(args):
         ck.eq(f"d_lp_s identity n={n}", t.cpu().numpy(),
               orc.d_fp_s_rank([xs[j] for j in topo.neighbors(rank, 0)], 1))
 
+    # ---- D_* between the register capacity and the ring cut-over: the
+    # streaming per-CTA kernel (small_coll.cu decent_stream_kernel)
+    for n in (6_000_001, 16_000_000):
+        bucket += 1
+        xs = [orc.synth(n, 8100 + r) for r in range(g)]
+        for kind in (b2.TopologyKind.ring, b2.TopologyKind.random):
+            topo = b2.Topology(kind, g, 11)
+            for rnd in range(2):
+                nb = topo.neighbors(rank, rnd)
+                t = torch.as_tensor(xs[rank]).cuda()
+                b2.d_lp_s(ep, 0.0, t, topo, rnd, U8, b2.ReduceMode.average, bucket=bucket)
+                ck.eq(f"d_lp_s stream {kind.name} r{rnd} n={n}", t.cpu().numpy(),
+                      orc.d_lp_s_rank([xs[j] for j in nb], 1, 1))
+                t = torch.as_tensor(xs[rank]).cuda()
+                b2.d_fp_s(ep, 0.0, t, topo, rnd, b2.ReduceMode.sum, bucket=bucket)
+                ck.eq(f"d_fp_s stream {kind.name} r{rnd} n={n}", t.cpu().numpy(),
+                      orc.d_fp_s_rank([xs[j] for j in nb], 0))
+
     # ---- chunk-aligned shapes (n % 16g == 0): the staggered C_LP_S kernel
     # (central_stag.cu), stateless and with error feedback, repeated calls
     for n in (16 * g, 16 * g * 37, 16 * g * 4099, 16 * g * 65537):
