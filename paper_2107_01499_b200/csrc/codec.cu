@@ -174,6 +174,9 @@ __global__ void __launch_bounds__(kSmallThreads) encode_small_kernel(const float
   __shared__ float2 wred[kSmallThreads / 32];
   const size_t T = size_t(gridDim.x) * kSmallThreads, gt = size_t(blockIdx.x) * kSmallThreads + threadIdx.x;
   const size_t ng = n >> 2;  // whole float4 groups; the (< 4) tail goes to the last thread
+  // programmatic dependent launch (small_launch): the previous kernel on the
+  // stream is complete and visible past this point; a no-op otherwise
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const float4* x4 = reinterpret_cast<const float4*>(x);
   float4 y[R];
   float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
@@ -208,6 +211,7 @@ __global__ void __launch_bounds__(kSmallThreads) encode_small_kernel(const float
     if (l == 0) partials[blockIdx.x] = make_float2(a, b);
   }
   grid.sync();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the decode may start launching
   lo = __int_as_float(0x7f800000);
   hi = -__int_as_float(0x7f800000);
   for (unsigned c = threadIdx.x; c < gridDim.x; c += kSmallThreads) {
@@ -262,6 +266,8 @@ __global__ void __launch_bounds__(kSmallThreads) encode_small_kernel(const float
 __global__ void __launch_bounds__(kSmallThreads) decode_small_kernel(const uint8_t* __restrict__ codes,
                                                                      const float* hdr, size_t n,
                                                                      float* __restrict__ out) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the encode's codes and header are complete
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const U8Params q = u8_params(hdr[0], hdr[1]);
   const size_t ng = n >> 2;
   const uint32_t* c32 = reinterpret_cast<const uint32_t*>(codes);
@@ -625,7 +631,18 @@ static int try_small_encode(const float* x, float* delta, size_t n, uint8_t* cod
   float2* partials = small_partials();
   if (!partials) return B2_ERR_CUDA;
   void* params[] = {&x, &delta, &n, &codes, &hdr, &decoded, &partials};
-  B2_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kSmallThreads), params, 0, s));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kSmallThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the launch with the previous kernel's tail
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  B2_CUDA_TRY(cudaLaunchKernelExC(&cfg, fn, params));
   return B2_OK;
 }
 
@@ -733,7 +750,16 @@ int b2_u8_decode(const uint8_t* codes, const float* hdr, size_t n, float* out, v
   if (n <= (size_t(64) << 20)) {  // small buckets: one 32-bit load -> one float4 store per thread
     const size_t ng = std::max<size_t>(n >> 2, 1);
     const int grid = int(std::min<size_t>((ng + kSmallThreads - 1) / kSmallThreads, size_t(sm_count()) * 16));
-    decode_small_kernel<<<grid, kSmallThreads, 0, static_cast<cudaStream_t>(stream)>>>(codes, hdr, n, out);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kSmallThreads);
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    B2_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_small_kernel, codes, hdr, n, out));
     B2_CUDA_TRY(cudaGetLastError());
     return B2_OK;
   }

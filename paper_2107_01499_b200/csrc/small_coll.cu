@@ -408,36 +408,48 @@ __global__ void __launch_bounds__(kSmallThr) decent_stream_kernel(DecentArgs a) 
   if (tr && threadIdx.x == 0) tr[kTrP2Ready] = globaltimer();
   const double inv = a.inv;
   const int nnb = a.nnb;
-  for (size_t g = gt; g < ng; g += T) {
-    uint32_t cw[kMaxRanks];
-    float4 fw[CODEC == kU8 ? 1 : kMaxRanks];
+  // U groups per iteration: every load of the U groups first (one NVLink
+  // round trip per U groups, not per group), then the folds
+  constexpr int U = CODEC == kU8 ? 4 : 2;
+  for (size_t g0 = gt; g0 < ng; g0 += U * T) {
+    uint32_t cw[U][kMaxRanks];
+    float4 fw[CODEC == kU8 ? 1 : U][CODEC == kU8 ? 1 : kMaxRanks];
 #pragma unroll
-    for (int i = 0; i < kMaxRanks; ++i)  // every load of this group first: one NVLink round trip
-      if (i < nnb) {
-        const uint8_t* src = a.win[a.nbrs[i]] + a.off_dbuf;
-        if (CODEC == kU8)
-          cw[i] = __ldcg(reinterpret_cast<const uint32_t*>(src) + g);
-        else
-          fw[CODEC == kU8 ? 0 : i] = __ldcg(reinterpret_cast<const float4*>(src) + g);
-      }
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int u = 0; u < U; ++u) {
+      const size_t g = g0 + size_t(u) * T;
 #pragma unroll
-    for (int i = 0; i < kMaxRanks; ++i)
-      if (i < nnb) {
-        float4 d;
-        if (CODEC == kU8) {
-          const SrcDecS sd = s_dec[i];
-          d = sd.fast ? dequant4_fast(cw[i], sd.lo, sd.step, sd.c23) : dequant4(cw[i], sd.lo, sd.step);
-        } else {
-          d = fw[CODEC == kU8 ? 0 : i];
+      for (int i = 0; i < kMaxRanks; ++i)
+        if (i < nnb && g < ng) {
+          const uint8_t* src = a.win[a.nbrs[i]] + a.off_dbuf;
+          if (CODEC == kU8)
+            cw[u][i] = __ldcg(reinterpret_cast<const uint32_t*>(src) + g);
+          else
+            fw[CODEC == kU8 ? 0 : u][CODEC == kU8 ? 0 : i] = __ldcg(reinterpret_cast<const float4*>(src) + g);
         }
-        a0 = __dadd_rn(a0, double(d.x));
-        a1 = __dadd_rn(a1, double(d.y));
-        a2 = __dadd_rn(a2, double(d.z));
-        a3 = __dadd_rn(a3, double(d.w));
-      }
-    __stcs(x4 + g, make_float4(__double2float_rn(__dmul_rn(a0, inv)), __double2float_rn(__dmul_rn(a1, inv)),
-                               __double2float_rn(__dmul_rn(a2, inv)), __double2float_rn(__dmul_rn(a3, inv))));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const size_t g = g0 + size_t(u) * T;
+      if (g >= ng) break;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+      for (int i = 0; i < kMaxRanks; ++i)
+        if (i < nnb) {
+          float4 d;
+          if (CODEC == kU8) {
+            const SrcDecS sd = s_dec[i];
+            d = sd.fast ? dequant4_fast(cw[u][i], sd.lo, sd.step, sd.c23) : dequant4(cw[u][i], sd.lo, sd.step);
+          } else {
+            d = fw[CODEC == kU8 ? 0 : u][CODEC == kU8 ? 0 : i];
+          }
+          a0 = __dadd_rn(a0, double(d.x));
+          a1 = __dadd_rn(a1, double(d.y));
+          a2 = __dadd_rn(a2, double(d.z));
+          a3 = __dadd_rn(a3, double(d.w));
+        }
+      __stcs(x4 + g, make_float4(__double2float_rn(__dmul_rn(a0, inv)), __double2float_rn(__dmul_rn(a1, inv)),
+                                 __double2float_rn(__dmul_rn(a2, inv)), __double2float_rn(__dmul_rn(a3, inv))));
+    }
   }
   if (tail)
     for (size_t e = 4 * ng; e < n; ++e) {
