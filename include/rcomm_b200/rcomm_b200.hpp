@@ -24,6 +24,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <functional>
+#include <map>
 #include <memory>
 #include <random>
 #include <span>
@@ -152,6 +153,8 @@ class B200Endpoint {
   }
   // Synchronize this endpoint's stream, throw on a latched device error.
   void sync();
+  // Device staging buffer of a host bucket, cached per (bucket, length).
+  float* staging(std::uint32_t bucket, std::size_t n);
 
  private:
   static int gather_trampoline(void* user, const void* send, std::size_t bytes, void* recv);
@@ -160,6 +163,7 @@ class B200Endpoint {
   b2_comm_t comm_ = nullptr;
   void* stream_ = nullptr;  // cudaStream_t owned by the endpoint
   std::uint64_t bytes_sent_ = 0, messages_sent_ = 0;
+  std::map<std::pair<std::uint32_t, std::size_t>, void*> staging_;
 };
 
 // collectives.hpp:50-72 -- same names, argument order and meaning.

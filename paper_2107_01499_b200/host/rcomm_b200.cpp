@@ -65,28 +65,30 @@ struct DevBuf {  // owned device allocation
 };
 
 // A float span resolved to a 16-byte aligned device buffer; host spans (and
-// misaligned device spans) are staged and written back by finish().
+// misaligned device spans) are staged through a device buffer cached per
+// (endpoint, bucket, length) and written back by finish() -- which the
+// primitives call only after ep.sync() has checked the device status, so a
+// failing call leaves x untouched (the reference throws from encode before x
+// changes, codec.cpp:24-27).
 struct Staged {
   std::span<float> user;
   float* dev = nullptr;
-  std::unique_ptr<DevBuf> own;
-  bool host = false;
-  Staged(std::span<float> x, cudaStream_t s) : user(x) {
-    const bool on_dev = is_device_ptr(x.data());
-    host = !on_dev;
-    if (on_dev && (reinterpret_cast<std::uintptr_t>(x.data()) & 15) == 0) {
+  bool staged = false;
+  Staged(B200Endpoint& ep, std::uint32_t bucket, std::span<float> x, cudaStream_t s) : user(x) {
+    if (is_device_ptr(x.data()) && (reinterpret_cast<std::uintptr_t>(x.data()) & 15) == 0) {
       dev = x.data();
       return;
     }
-    own = std::make_unique<DevBuf>(std::max<std::size_t>(x.size(), 1) * sizeof(float));
-    dev = own->as<float>();
+    staged = true;
+    dev = ep.staging(bucket, x.size());
     if (!x.empty())
       cuda_check(cudaMemcpyAsync(dev, x.data(), x.size() * sizeof(float), cudaMemcpyDefault, s), "stage in");
   }
   void finish(cudaStream_t s) {
-    if (own && !user.empty())
+    if (staged && !user.empty()) {
       cuda_check(cudaMemcpyAsync(user.data(), dev, user.size() * sizeof(float), cudaMemcpyDefault, s), "stage out");
-    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+      cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    }
   }
 };
 
@@ -356,7 +358,22 @@ B200Endpoint::B200Endpoint(int rank, int world, int device, AllGather allgather)
   check(b2_comm_create(world_, rank_, device_, allgather_ ? &B200Endpoint::gather_trampoline : nullptr, this, &comm_));
 }
 
+float* B200Endpoint::staging(std::uint32_t bucket, std::size_t n) {
+  auto& p = staging_[{bucket, n}];
+  if (!p) {
+    DeviceScope ds(device_);
+    float* q = nullptr;
+    cuda_check(cudaMalloc(&q, std::max<std::size_t>(n, 4) * sizeof(float)), "cudaMalloc staging");
+    p = q;
+  }
+  return static_cast<float*>(p);
+}
+
 B200Endpoint::~B200Endpoint() {
+  {
+    DeviceScope ds(device_);
+    for (auto& kv : staging_) cudaFree(kv.second);
+  }
   if (comm_) b2_comm_destroy(comm_);
   if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
 }
@@ -372,10 +389,10 @@ void B200Endpoint::sync() { check(b2_comm_sync(comm_, stream_)); }
 double c_fp_s(B200Endpoint& ep, double now, std::span<float> x, std::uint32_t bucket) {
   DeviceScope ds(ep.device());
   auto s = static_cast<cudaStream_t>(ep.stream());
-  Staged b(x, s);
+  Staged b(ep, bucket, x, s);
   check(b2_c_fp_s(ep.handle(), b.dev, x.size(), bucket, s));
+  ep.sync();  // throws on a latched device error before anything is written back
   b.finish(s);
-  ep.sync();
   const int g = ep.world_size(), me = ep.rank();
   if (g > 1) {
     const std::size_t own = owned_partition_len(x.size(), g, me);
@@ -389,11 +406,11 @@ double c_lp_s(B200Endpoint& ep, double now, std::span<float> x, const Codec& cod
   check_codec(codec, rng);
   DeviceScope ds(ep.device());
   auto s = static_cast<cudaStream_t>(ep.stream());
-  Staged b(x, s);
+  Staged b(ep, bucket, x, s);
   check(b2_c_lp_s(ep.handle(), b.dev, x.size(), static_cast<int>(codec.kind), es ? es->delta() : nullptr,
                   es ? es->delta_len() : 0, es ? es->epsilon() : nullptr, es ? es->epsilon_len() : 0, bucket, s));
+  ep.sync();  // throws on a latched device error before anything is written back
   b.finish(s);
-  ep.sync();
   const int g = ep.world_size(), me = ep.rank();
   if (g > 1) {
     std::uint64_t sent = 0;
@@ -417,11 +434,11 @@ double d_fp_s(B200Endpoint& ep, double now, std::span<float> x, const Topology& 
   const auto nb = nbrs_of(ep, topo, round);
   DeviceScope ds(ep.device());
   auto s = static_cast<cudaStream_t>(ep.stream());
-  Staged b(x, s);
+  Staged b(ep, bucket, x, s);
   check(b2_d_fp_s(ep.handle(), b.dev, x.size(), nb.data(), static_cast<int>(nb.size()), static_cast<int>(mode),
                   bucket, s));
+  ep.sync();  // throws on a latched device error before anything is written back
   b.finish(s);
-  ep.sync();
   ep.account((nb.size() - 1) * 4 * x.size(), nb.size() - 1);
   return now;
 }
@@ -432,11 +449,11 @@ double d_lp_s(B200Endpoint& ep, double now, std::span<float> x, const Topology& 
   const auto nb = nbrs_of(ep, topo, round);
   DeviceScope ds(ep.device());
   auto s = static_cast<cudaStream_t>(ep.stream());
-  Staged b(x, s);
+  Staged b(ep, bucket, x, s);
   check(b2_d_lp_s(ep.handle(), b.dev, x.size(), nb.data(), static_cast<int>(nb.size()), static_cast<int>(codec.kind),
                   static_cast<int>(mode), bucket, s));
+  ep.sync();  // throws on a latched device error before anything is written back
   b.finish(s);
-  ep.sync();
   ep.account((nb.size() - 1) * codec.payload_size(x.size()), nb.size() - 1);
   return now;
 }
