@@ -9,7 +9,9 @@ import ctypes as C
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libb2comm.so")
+# B2COMM_LIB: an alternative in-tree build of the same library (A/B runs of
+# compile-time variants, paper_2107_01499_b200/build.py build_variant)
+LIB_PATH = os.environ.get("B2COMM_LIB") or os.path.join(PKG_DIR, "libb2comm.so")
 
 B2_OK, B2_ERR_INVALID, B2_ERR_CUDA, B2_ERR_NONFINITE, B2_ERR_TIMEOUT, B2_ERR_UNSUPPORTED, B2_ERR_BOOTSTRAP = range(7)
 CODEC_IDENTITY, CODEC_UNIFORM8, CODEC_ONEBIT = 0, 1, 2

@@ -46,17 +46,27 @@ def _deps(dirpath: str, exts: tuple[str, ...]) -> list[str]:
     return [os.path.join(dirpath, f) for f in sorted(os.listdir(dirpath)) if f.endswith(exts)]
 
 
-def build_cuda(force: bool = False, verbose: bool = False) -> str:
+def build_variant(name: str, defines: list[str]) -> str:
+    """A compile-time variant of libb2comm.so (e.g. -DB2_RING_STAGES=6) under
+    variants/, selected at run time with B2COMM_LIB (A/B measurements)."""
+    return build_cuda(force=False, out=os.path.join(PKG_DIR, "variants", f"libb2comm_{name}.so"),
+                      extra=[f"-D{d}" for d in defines], objdir=os.path.join(PKG_DIR, "build", name))
+
+
+def build_cuda(force: bool = False, verbose: bool = False, out: str | None = None, extra: list | None = None,
+               objdir: str | None = None) -> str:
+    LIB = out or globals()["LIB"]
     deps = _deps(CSRC, (".cu", ".cuh", ".h")) + [os.path.join(INCLUDE, "b2comm.h")]
     if not force and not _stale(LIB, deps):
         return LIB
-    objdir = os.path.join(PKG_DIR, "build")
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    objdir = objdir or os.path.join(PKG_DIR, "build")
     os.makedirs(objdir, exist_ok=True)
     nvcc = _nvcc()
     objs = []
     for src in CUDA_SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [nvcc, *NVCC_FLAGS, *(extra or []), "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
