@@ -53,7 +53,7 @@ typedef enum {
   B2_ERR_CUDA = 2,        /* CUDA runtime failure                            */
   B2_ERR_NONFINITE = 3,   /* encode saw NaN/Inf  (codec.cpp:26)              */
   B2_ERR_TIMEOUT = 4,     /* a peer never arrived (rendezvous timeout)       */
-  B2_ERR_UNSUPPORTED = 5, /* e.g. stochastic rounding                          */
+  B2_ERR_UNSUPPORTED = 5, /* an unsupported combination                        */
   B2_ERR_BOOTSTRAP = 6    /* the allgather callback failed                   */
 } b2_status;
 
@@ -95,7 +95,7 @@ int b2_u8_decode(const uint8_t* codes, const float* hdr, size_t n, float* out, v
  * b2_u8_encode, levels rounded up with probability q - floor(q); the uniform
  * draws come from a counter hash of (seed, element), not mt19937, so only
  * unbiasedness is shared with the reference (test_codec.cpp:175-192).  The
- * collectives still reject stochastic rounding (B2_ERR_UNSUPPORTED). */
+ * collectives take it through b2_c_lp_s_stochastic / b2_d_lp_s_stochastic. */
 int b2_u8_encode_stochastic(const float* x, size_t n, uint8_t* codes, float* hdr, uint64_t seed,
                             void* stream);
 /* compensate_encode (codec.hpp:49-54, codec.cpp:125-137) with uniform8:
@@ -199,17 +199,27 @@ int b2_comm_read_trace(b2_comm_t comm, uint64_t* out, int max_ctas, int* n_slots
  *   aggregation, algorithms.cpp:141-148) or B2_CODEC_IDENTITY.  delta/eps both
  *   NULL = stateless; else ErrorState (codec.hpp:40-47): delta has n floats,
  *   eps has owned_partition_len(n, world, rank) floats, both updated.
- *   stochastic rounding is not supported (B2_ERR_UNSUPPORTED).
+ *   stochastic rounding: b2_c_lp_s_stochastic below.
  * d_fp_s  (collectives.hpp:64-66; collectives.cpp:229-258)
  * d_lp_s  (collectives.hpp:69-72; collectives.cpp:260-288):
  *   nbrs = Topology::neighbors(rank, round) (sorted, self-inclusive, HOST
  *   array); the neighbour relation must be symmetric, as every rcomm
- *   Topology is.  mode = B2_REDUCE_SUM / B2_REDUCE_AVERAGE.  Any codec. */
+ *   Topology is.  mode = B2_REDUCE_SUM / B2_REDUCE_AVERAGE.  Any codec.
+ * *_stochastic: the uniform8 codec with Rounding::stochastic
+ *   (codec.cpp:67-78) in every encode of the primitive (C_LP_S: both
+ *   phases): level = floor(q) + (u < q - floor(q)), u from a counter hash of
+ *   (seed, rank, phase, element).  `seed` is drawn per call from the caller's
+ *   generator by the host wrappers; the draws are not the reference's
+ *   mt19937 stream, so only unbiasedness is shared with it. */
 int b2_c_fp_s(b2_comm_t comm, float* x, size_t n, uint32_t bucket, void* stream);
 int b2_c_lp_s(b2_comm_t comm, float* x, size_t n, int codec, float* delta, size_t delta_len,
               float* eps, size_t eps_len, uint32_t bucket, void* stream);
 int b2_d_fp_s(b2_comm_t comm, float* x, size_t n, const int* nbrs, int n_nbrs, int mode,
               uint32_t bucket, void* stream);
+int b2_c_lp_s_stochastic(b2_comm_t comm, float* x, size_t n, float* delta, size_t delta_len, float* eps,
+                         size_t eps_len, uint64_t seed, uint32_t bucket, void* stream);
+int b2_d_lp_s_stochastic(b2_comm_t comm, float* x, size_t n, const int* nbrs, int n_nbrs, int mode,
+                         uint64_t seed, uint32_t bucket, void* stream);
 int b2_d_lp_s(b2_comm_t comm, float* x, size_t n, const int* nbrs, int n_nbrs, int codec,
               int mode, uint32_t bucket, void* stream);
 

@@ -69,12 +69,12 @@ class Codec:
         return v
 
     def _check_supported(self, rng, collective: bool = True) -> None:
-        if self.kind == CodecKind.uniform8 and self.rounding == Rounding.stochastic:
-            if rng is None:  # codec.cpp:70 wording
-                raise Error("uniform8 stochastic rounding needs a generator")
-            if collective:
-                raise _lib.B2Error(_lib.B2_ERR_UNSUPPORTED,
-                                   "uniform8 stochastic rounding is implemented for the codec, not the collectives")
+        if self.stochastic() and rng is None:  # codec.cpp:70 wording
+            raise Error("uniform8 stochastic rounding needs a generator")
+
+    def stochastic(self) -> bool:
+        """uniform8 with Rounding::stochastic (codec.cpp:67-78)."""
+        return self.kind == CodecKind.uniform8 and self.rounding == Rounding.stochastic
 
     @staticmethod
     def _seed(rng) -> int:

@@ -484,8 +484,12 @@ def c_lp_s(ep: B200Endpoint, now: float, x, codec: Codec, es: ErrorState | None,
         dptr, dlen = es.delta.data_ptr(), es.delta.numel()
         eptr, elen = (es.epsilon.data_ptr() if own else es.delta.data_ptr()), own
     with _on_device(ep):
-        check(lib.b2_c_lp_s(ep.handle, b.dev.data_ptr(), b.n, int(codec.kind), dptr, dlen, eptr, elen, bucket,
-                            ep.stream()))
+        if codec.stochastic():  # one 64-bit seed per call from the caller's generator (codec.cpp:71-74)
+            check(lib.b2_c_lp_s_stochastic(ep.handle, b.dev.data_ptr(), b.n, dptr, dlen, eptr, elen,
+                                           codec._seed(rng), bucket, ep.stream()))
+        else:
+            check(lib.b2_c_lp_s(ep.handle, b.dev.data_ptr(), b.n, int(codec.kind), dptr, dlen, eptr, elen, bucket,
+                                ep.stream()))
         _finish(ep, b, blocking)
     if g > 1:
         key = ("c_lp_s", int(codec.kind), b.n)
@@ -616,8 +620,12 @@ def d_lp_s(ep: B200Endpoint, now: float, x, topo: Topology, round_: int, codec: 
     arr, m = _neighbors(ep, topo, round_)
     b = _Bucket(ep, x)
     with _on_device(ep):
-        check(lib.b2_d_lp_s(ep.handle, b.dev.data_ptr(), b.n, arr, m, int(codec.kind), int(mode), bucket,
-                            ep.stream()))
+        if codec.stochastic():
+            check(lib.b2_d_lp_s_stochastic(ep.handle, b.dev.data_ptr(), b.n, arr, m, int(mode), codec._seed(rng),
+                                           bucket, ep.stream()))
+        else:
+            check(lib.b2_d_lp_s(ep.handle, b.dev.data_ptr(), b.n, arr, m, int(codec.kind), int(mode), bucket,
+                                ep.stream()))
         _finish(ep, b, blocking)
     ep._account((m - 1) * codec.payload_size(b.n), m - 1)
     return now

@@ -86,6 +86,46 @@ __device__ __forceinline__ uint32_t quantize4(float4 v, float lo, float inv) {
   return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
 
+// Stochastic rounding inside the collectives (Codec{uniform8,
+// Rounding::stochastic}, codec.cpp:67-78): level = floor(q) + (u < q -
+// floor(q)), clamped to [0, 255], u uniform in [0, 1) with 24 random bits
+// (std::uniform_real_distribution<float>'s resolution) from a counter hash of
+// (per-call key, element index) -- the reference draws u from the caller's
+// host mt19937 stream, so only the distribution (unbiased levels) is shared.
+struct Rounder {
+  unsigned long long key;  // 0 with on == false
+  bool on;
+};
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+// per call, rank and encode phase (1: the first encode, 2: the owner's second)
+__device__ __forceinline__ Rounder make_rounder(bool on, unsigned long long seed, int rank, int phase) {
+  return Rounder{on ? mix64(seed ^ mix64((unsigned long long)(rank + 1) * 0x100000001b3ULL + (unsigned long long)phase))
+                    : 0ull,
+                 on};
+}
+__device__ __forceinline__ uint32_t level_sr(float x, float lo, float inv, unsigned long long key, size_t e) {
+  const float q = __fmul_rn(__fsub_rn(x, lo), inv);
+  const float fl = floorf(q);
+  const float u = float(uint32_t(mix64(key + e) >> 40)) * 0x1p-24f;
+  float level = __fadd_rn(fl, u < __fsub_rn(q, fl) ? 1.0f : 0.0f);
+  level = fminf(fmaxf(level, 0.0f), 255.0f);  // NaN -> 0 like the nearest path
+  return uint32_t(level);
+}
+// quantize with the call's rounding; e = index of the (first) element
+__device__ __forceinline__ uint8_t q1r(float x, float lo, float inv, const Rounder& r, size_t e) {
+  return r.on ? uint8_t(level_sr(x, lo, inv, r.key, e)) : quantize1(x, lo, inv);
+}
+__device__ __forceinline__ uint32_t q4r(float4 v, float lo, float inv, const Rounder& r, size_t e) {
+  if (!r.on) return quantize4(v, lo, inv);
+  return level_sr(v.x, lo, inv, r.key, e) | (level_sr(v.y, lo, inv, r.key, e + 1) << 8) |
+         (level_sr(v.z, lo, inv, r.key, e + 2) << 16) | (level_sr(v.w, lo, inv, r.key, e + 3) << 24);
+}
+
 // dequantize_u8 (kernels.cpp:52-56): lo + (float)q * step, rounded multiply
 // then rounded add.  (float)q via the 2^23 magic: PRMT + FADD, exact.
 template <int K>

@@ -133,6 +133,7 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
   // (the two-term fold is two FADDs, fold.cuh sum2_exact), cached in x's own
   // chunk at g >= 3 (4 bytes written + read beat re-running the fp64 fold)
   const bool cache_y2 = a.g >= 3;
+  const Rounder r1 = make_rounder(a.sr_on, a.sr_seed, me, 1), r2 = make_rounder(a.sr_on, a.sr_seed, me, 2);
   auto kstep = [&](int s) { return (me + 1 + s) % g; };  // chunk of step s; s = g-1: my own
   auto src_of = [&](int i) { return (me + g - 1 - i) % g; };  // landing pass i: source rank
   uint8_t* land = a.win[me] + a.off_land;
@@ -250,7 +251,7 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
               for (int gi = gct; gi < int(units * 4); gi += gn) {
                 float4 y = xs[gi];
                 if (EC) y = sub4(y, ds[gi]);
-                const uint32_t q = quantize4(y, p.lo, p.inv);
+                const uint32_t q = q4r(y, p.lo, p.inv, r1, e0 + 4 * size_t(gi));
                 dst[gi] = q;
                 if (EC) dl4[(e0 >> 2) + gi] = sub4(y, dequant4(q, p));
               }
@@ -408,7 +409,7 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
             for (int gi = qct; gi < ng; gi += qn) {
               const size_t e = e0 + 4 * size_t(gi);
               const float4 v = ys[gi];  // y2 (- eps already applied in the fold)
-              const uint32_t q = quantize4(v, p2.lo, p2.inv);
+              const uint32_t q = q4r(v, p2.lo, p2.inv, r2, e);
               *reinterpret_cast<uint32_t*>(out2 + (e - mlo)) = q;
               const float4 d = dequant4(q, p2);
               if (EC) reinterpret_cast<float4*>(a.eps)[(e - mlo) >> 2] = sub4(v, d);
@@ -431,7 +432,7 @@ __device__ __forceinline__ void stag_body(const CentralArgs& a, Ring& r) {
               const size_t e = e0 + 4 * size_t(gg);
               float4 v = y[h];
               if (EC) v = sub4(v, reinterpret_cast<const float4*>(a.eps)[(e - mlo) >> 2]);
-              const uint32_t q = quantize4(v, p2.lo, p2.inv);
+              const uint32_t q = q4r(v, p2.lo, p2.inv, r2, e);
               *reinterpret_cast<uint32_t*>(out2 + (e - mlo)) = q;
               const float4 d = dequant4(q, p2);
               if (EC) reinterpret_cast<float4*>(a.eps)[(e - mlo) >> 2] = sub4(v, d);

@@ -147,6 +147,8 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
   WinHdr* mine = hdr_of(a.win[me]);
   const size_t mbase = mlo & ~size_t(15);
   const unsigned long long gmul = (unsigned long long)g * a.epoch;
+  const Rounder r1 = make_rounder(CODEC == kU8 && a.sr_on, a.sr_seed, me, 1);  // the first encode
+  const Rounder r2 = make_rounder(CODEC == kU8 && a.sr_on, a.sr_seed, me, 2);  // the owner's second
 
   auto xpass = [&](size_t lo, size_t sz) {
     PassDesc p = PassDesc::make();
@@ -241,7 +243,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     return reduce_partials(a.partials + size_t(slot) * G, G, red, ct);
   };
 
-  if (CODEC == kU8 && g == 1 && !EC) {
+  if (CODEC == kU8 && g == 1 && !EC && !a.sr_on) {  // (stochastic Q1 need not emit code 255: no shortcut)
     // ------------------------------------------- single rank, stateless
     // D1(q) = lo1 + q*step1 is monotone in q and codes 0 and 255 always occur
     // (0 at the minimum element, 255 at the maximum; all 0 when degenerate),
@@ -268,13 +270,13 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     r.run(pb, [&](const uint8_t* st, size_t e0, size_t units, int) {
       const float4* xs = reinterpret_cast<const float4*>(st);
       for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
-        const float4 d1 = add0(dequant4(quantize4(xs[gi], p1.lo, p1.inv), p1));
-        __stcs(x4 + ((e0 >> 2) + gi), dequant4(quantize4(d1, p2.lo, p2.inv), p2));
+        const float4 d1 = add0(dequant4(q4r(xs[gi], p1.lo, p1.inv, r1, e0 + 4 * size_t(gi)), p1));
+        __stcs(x4 + ((e0 >> 2) + gi), dequant4(q4r(d1, p2.lo, p2.inv, r2, e0 + 4 * size_t(gi)), p2));
       }
     });
     r.edges(px, [&](size_t e) {
-      const float d1 = __fadd_rn(dequant1(quantize1(a.x[e], p1.lo, p1.inv), p1), 0.0f);
-      a.x[e] = dequant1(quantize1(d1, p2.lo, p2.inv), p2);
+      const float d1 = __fadd_rn(dequant1(q1r(a.x[e], p1.lo, p1.inv, r1, e), p1), 0.0f);
+      a.x[e] = dequant1(q1r(d1, p2.lo, p2.inv, r2, e), p2);
     });
     B2_TRACE(kTrEnd);
     return;
@@ -300,8 +302,8 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
       for (int gi = ct; gi < int(units * 4); gi += kConsumers) {
         float4 y = xs[gi];
         if (EC) y = sub4(y, ds[gi]);
-        const uint32_t q = quantize4(y, p1.lo, p1.inv);
         const size_t e = e0 + 4 * size_t(gi);
+        const uint32_t q = q4r(y, p1.lo, p1.inv, r1, e);
         *reinterpret_cast<uint32_t*>(codes + e) = q;
         const float4 d = dequant4(q, p1);
         if (EC) dl4[e >> 2] = sub4(y, d);
@@ -313,7 +315,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     r.edges(px, [&](size_t e) {
       float y = a.x[e];
       if (EC) y = __fsub_rn(y, a.delta[e]);
-      const uint8_t q = quantize1(y, p1.lo, p1.inv);
+      const uint8_t q = q1r(y, p1.lo, p1.inv, r1, e);
       codes[e] = q;
       const float d = dequant1(q, p1.lo, p1.step);
       if (EC) a.delta[e] = __fsub_rn(y, d);
@@ -343,7 +345,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
         const size_t e = e0 + 4 * size_t(gi);
         float4 y2 = add0(dequant4(cs[gi], p1));
         if (EC) y2 = sub4(y2, eps4(a.eps, e, 0));
-        const float4 d2 = dequant4(quantize4(y2, p2.lo, p2.inv), p2);
+        const float4 d2 = dequant4(q4r(y2, p2.lo, p2.inv, r2, e), p2);
         __stcs(x4 + (e >> 2), d2);
         if (EC) set_eps4(a.eps, e, 0, sub4(y2, d2));
       }
@@ -351,7 +353,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     r.edges(pc, [&](size_t e) {
       float y2 = __fadd_rn(dequant1(codes[e], p1.lo, p1.step), 0.0f);
       if (EC) y2 = __fsub_rn(y2, a.eps[e]);
-      const float d2 = dequant1(quantize1(y2, p2.lo, p2.inv), p2.lo, p2.step);
+      const float d2 = dequant1(q1r(y2, p2.lo, p2.inv, r2, e), p2.lo, p2.step);
       a.x[e] = d2;
       if (EC) a.eps[e] = __fsub_rn(y2, d2);
     });
@@ -503,7 +505,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
           for (int gi = gct; gi < int(units * 4); gi += gn) {
             float4 y = xs[gi];
             if (EC) y = sub4(y, ds[gi]);
-            const uint32_t q = quantize4(y, p.lo, p.inv);
+            const uint32_t q = q4r(y, p.lo, p.inv, r1, e0 + 4 * size_t(gi));
             dst[gi] = q;  // my codes of chunk k, in my window: owner k pulls them
             if (EC) dl4[(e0 >> 2) + gi] = sub4(y, dequant4(q, p));
           }
@@ -560,7 +562,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
         r.edges(pc[i], [&](size_t e) {
           float y = a.x[e];
           if (EC) y = __fsub_rn(y, a.delta[e]);
-          const uint8_t q = quantize1(y, p.lo, p.inv);
+          const uint8_t q = q1r(y, p.lo, p.inv, r1, e);
           dst[e - ebase] = q;
           if (EC) a.delta[e] = __fsub_rn(y, dequant1(q, p.lo, p.step));
         });
@@ -599,12 +601,12 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     // as early as possible; the owner's own chunk of x is decoded from it in
     // phase 3, in the shadow of the NVLink pulls.
     auto emit = [&](size_t e, float4 y) {
-      const uint32_t q = quantize4(y, p.lo, p.inv);
+      const uint32_t q = q4r(y, p.lo, p.inv, r2, e);
       *reinterpret_cast<uint32_t*>(out2 + (e - mbase)) = q;
       if (EC) set_eps4(a.eps, e, mlo, sub4(y, dequant4(q, p)));
     };
     auto emit1 = [&](size_t e, float y) {
-      const uint8_t q = quantize1(y, p.lo, p.inv);
+      const uint8_t q = q1r(y, p.lo, p.inv, r2, e);
       out2[e - mbase] = q;
       if (EC) a.eps[e - mlo] = __fsub_rn(y, dequant1(q, p.lo, p.step));
     };
@@ -851,6 +853,7 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
   const bool cons = r.ct >= 0;
   WinHdr* mine = hdr_of(a.win[me]);
   uint8_t* mybuf = a.win[me] + a.off_dbuf;
+  const Rounder rd = make_rounder(CODEC == kU8 && a.sr_on, a.sr_seed, me, 3);
   float4* x4 = reinterpret_cast<float4*>(a.x);
   int bad = 0;
   B2_TRACE(kTrStart);
@@ -907,10 +910,10 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
       r.run(pb, [&](const uint8_t* st, size_t e0, size_t units, int) {
         const float4* xs = reinterpret_cast<const float4*>(st);
         for (int gi = ct; gi < int(units * 4); gi += kConsumers)
-          __stcs(x4 + ((e0 >> 2) + gi), add0(dequant4(quantize4(xs[gi], q8.lo, q8.inv), q8)));
+          __stcs(x4 + ((e0 >> 2) + gi), add0(dequant4(q4r(xs[gi], q8.lo, q8.inv, rd, e0 + 4 * size_t(gi)), q8)));
       });
       r.edges(px, [&](size_t e) {
-        a.x[e] = __fadd_rn(dequant1(quantize1(a.x[e], q8.lo, q8.inv), q8), 0.0f);
+        a.x[e] = __fadd_rn(dequant1(q1r(a.x[e], q8.lo, q8.inv, rd, e), q8), 0.0f);
       });
     } else {
       r.run(px, [&](const uint8_t* st, size_t e0, size_t units, int) {
@@ -1007,7 +1010,8 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
         r.slot_acquire();
         if (CODEC == kU8) {
           uint32_t* b32 = reinterpret_cast<uint32_t*>(mybuf + e0);
-          for (int gi = gct; gi < int(units * 4); gi += gn) b32[gi] = quantize4(xs[gi], q8.lo, q8.inv);
+          for (int gi = gct; gi < int(units * 4); gi += gn)
+            b32[gi] = q4r(xs[gi], q8.lo, q8.inv, rd, e0 + 4 * size_t(gi));
         } else {
           float4* b4 = reinterpret_cast<float4*>(mybuf + 4 * e0);
           for (int gi = gct; gi < int(units * 4); gi += gn) {
@@ -1061,7 +1065,7 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
   if (cons && blockIdx.x == G - 1 && ct < 32) {
     r.edges(px, [&](size_t e) {
       if (CODEC == kU8) {
-        mybuf[e] = quantize1(a.x[e], q8.lo, q8.inv);
+        mybuf[e] = q1r(a.x[e], q8.lo, q8.inv, rd, e);
       } else {
         reinterpret_cast<float*>(mybuf)[e] = a.x[e];
         if (a.check_finite) bad |= !finite_f(a.x[e]);

@@ -68,6 +68,8 @@ struct CentralArgs {
   Fail* status;                 // failure context of this window (b2_device.cuh)
   unsigned long long timeout_ns;
   unsigned long long* trace;    // [grid * kTraceSlots] globaltimer stamps, or null
+  int sr_on;                    // stochastic rounding (uint8), b2_c_lp_s_stochastic
+  unsigned long long sr_seed;   // per-call seed drawn from the caller's generator
 };
 
 // Dynamic tile counters per window: one per pass of a launch (C_*: at most
@@ -147,6 +149,8 @@ struct DecentArgs {
   Fail* status;
   unsigned long long timeout_ns;
   unsigned long long* trace;
+  int sr_on;                    // stochastic rounding (uint8), b2_d_lp_s_stochastic
+  unsigned long long sr_seed;
 };
 
 }  // namespace b2

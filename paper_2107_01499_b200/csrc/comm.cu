@@ -539,7 +539,8 @@ static bool static_sched() {
 }
 
 static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite, float* delta,
-                   size_t delta_len, float* eps, size_t eps_len, uint32_t bucket, void* stream) {
+                   size_t delta_len, float* eps, size_t eps_len, uint32_t bucket, void* stream, int sr_on = 0,
+                   uint64_t sr_seed = 0) {
   int rc = check_comm(c, x, n);
   if (rc) return rc;
   B2_REQUIRE((delta == nullptr) == (eps == nullptr), "delta and eps must both be set or both null");
@@ -581,6 +582,8 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   a.status = w->fail;
   a.timeout_ns = c->timeout_ns;
   a.trace = c->trace;
+  a.sr_on = sr_on;
+  a.sr_seed = sr_seed;
   // uint8 at g == 2 with 16-aligned equal chunks: the staggered schedule
   // (central_stag.cu; measured faster at g = 2 only); every
   // rank decides identically from (n, g)
@@ -648,7 +651,8 @@ int b2_c_lp_s(b2_comm_t c, float* x, size_t n, int codec, float* delta, size_t d
 }
 
 static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbrs, int codec,
-                     int check_finite, int mode, uint32_t bucket, void* stream) {
+                     int check_finite, int mode, uint32_t bucket, void* stream, int sr_on = 0,
+                     uint64_t sr_seed = 0) {
   int rc = check_comm(c, x, n);
   if (rc) return rc;
   B2_REQUIRE(nbrs && n_nbrs >= 1 && n_nbrs <= c->world, "neighbour list of size %d invalid", n_nbrs);
@@ -716,6 +720,8 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
   a.status = w->fail;
   a.timeout_ns = c->timeout_ns;
   a.trace = c->trace;
+  a.sr_on = sr_on;
+  a.sr_seed = sr_seed;
   rc = launch_decent_small(a, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity, static_cast<cudaStream_t>(stream),
                            c->sm_budget);
   if (rc == B2_ERR_UNSUPPORTED)
@@ -728,6 +734,16 @@ static int decentral(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbr
     ++c->launches;
   }
   return rc;
+}
+
+int b2_c_lp_s_stochastic(b2_comm_t c, float* x, size_t n, float* delta, size_t delta_len, float* eps,
+                         size_t eps_len, uint64_t seed, uint32_t bucket, void* stream) {
+  return central(c, x, n, B2_CODEC_UNIFORM8, 1, delta, delta_len, eps, eps_len, bucket, stream, 1, seed);
+}
+
+int b2_d_lp_s_stochastic(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbrs, int mode, uint64_t seed,
+                         uint32_t bucket, void* stream) {
+  return decentral(c, x, n, nbrs, n_nbrs, B2_CODEC_UNIFORM8, 1, mode, bucket, stream, 1, seed);
 }
 
 int b2_d_fp_s(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbrs, int mode,

@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(kSmallThr) decent_small_kernel(DecentArgs a) {
   float4* x4 = reinterpret_cast<float4*>(a.x);
   WinHdr* mine = whdr(a.win[me]);
   if (threadIdx.x == 0) s_bad = 0;
+  const Rounder rd = make_rounder(CODEC == kU8 && a.sr_on, a.sr_seed, me, 3);
   // phase stamps (b2_comm_enable_trace): start, header final, published, neighbours in, end
   unsigned long long* tr = a.trace ? a.trace + size_t(b) * kTraceSlots : nullptr;
   if (tr && threadIdx.x == 0) tr[kTrStart] = globaltimer();
@@ -124,9 +125,9 @@ __global__ void __launch_bounds__(kSmallThr) decent_small_kernel(DecentArgs a) {
   uint8_t ct[3] = {0, 0, 0};
   if (CODEC == kU8) {
 #pragma unroll
-    for (int k = 0; k < R; ++k) c[k] = quantize4(y[k], q.lo, q.inv);
+    for (int k = 0; k < R; ++k) c[k] = q4r(y[k], q.lo, q.inv, rd, 4 * (gt + size_t(k) * T));
     if (tail)
-      for (size_t e = 4 * ng; e < n; ++e) ct[e - 4 * ng] = quantize1(yt[e - 4 * ng], q.lo, q.inv);
+      for (size_t e = 4 * ng; e < n; ++e) ct[e - 4 * ng] = q1r(yt[e - 4 * ng], q.lo, q.inv, rd, e);
   }
   if (a.nnb == 1) {
     // ---- the neighbourhood is {self}: x' = (float)((0.0 + (double)D(Q(x))) * 1.0) = D(Q(x)) + 0.0f
@@ -295,6 +296,7 @@ __global__ void __launch_bounds__(kSmallThr) decent_stream_kernel(DecentArgs a) 
   WinHdr* mine = whdr(a.win[me]);
   uint8_t* mybuf = a.win[me] + a.off_dbuf;
   if (threadIdx.x == 0) s_bad = 0;
+  const Rounder rd = make_rounder(CODEC == kU8 && a.sr_on, a.sr_seed, me, 3);
   unsigned long long* tr = a.trace ? a.trace + size_t(b) * kTraceSlots : nullptr;
   if (tr && threadIdx.x == 0) tr[kTrStart] = globaltimer();
   const bool tail = gt == T - 1 && (n & 3);
@@ -345,13 +347,13 @@ __global__ void __launch_bounds__(kSmallThr) decent_stream_kernel(DecentArgs a) 
     for (size_t g = gt; g < ng; g += T) {
       const float4 v = x4[g];
       if (CODEC != kU8 && a.check_finite) bad |= !(finite_f(v.x) && finite_f(v.y) && finite_f(v.z) && finite_f(v.w));
-      const float4 d = CODEC == kU8 ? dequant4(quantize4(v, q.lo, q.inv), q) : v;
+      const float4 d = CODEC == kU8 ? dequant4(q4r(v, q.lo, q.inv, rd, 4 * g), q) : v;
       x4[g] = make_float4(__fadd_rn(d.x, 0.0f), __fadd_rn(d.y, 0.0f), __fadd_rn(d.z, 0.0f), __fadd_rn(d.w, 0.0f));
     }
     if (tail)
       for (size_t e = 4 * ng; e < n; ++e) {
         if (CODEC != kU8 && a.check_finite) bad |= !finite_f(a.x[e]);
-        a.x[e] = __fadd_rn(CODEC == kU8 ? dequant1(quantize1(a.x[e], q.lo, q.inv), q) : a.x[e], 0.0f);
+        a.x[e] = __fadd_rn(CODEC == kU8 ? dequant1(q1r(a.x[e], q.lo, q.inv, rd, e), q) : a.x[e], 0.0f);
       }
     if (bad) atomicOr(&s_bad, 1);
     __syncthreads();
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(kSmallThr) decent_stream_kernel(DecentArgs a) 
   for (size_t g = gt; g < ng; g += T) {
     const float4 v = x4[g];
     if (CODEC == kU8) {
-      reinterpret_cast<uint32_t*>(mybuf)[g] = quantize4(v, q.lo, q.inv);
+      reinterpret_cast<uint32_t*>(mybuf)[g] = q4r(v, q.lo, q.inv, rd, 4 * g);
     } else {
       reinterpret_cast<float4*>(mybuf)[g] = v;
       if (a.check_finite) bad |= !(finite_f(v.x) && finite_f(v.y) && finite_f(v.z) && finite_f(v.w));
@@ -377,7 +379,7 @@ __global__ void __launch_bounds__(kSmallThr) decent_stream_kernel(DecentArgs a) 
   if (tail)
     for (size_t e = 4 * ng; e < n; ++e) {
       if (CODEC == kU8) {
-        mybuf[e] = quantize1(a.x[e], q.lo, q.inv);
+        mybuf[e] = q1r(a.x[e], q.lo, q.inv, rd, e);
       } else {
         reinterpret_cast<float*>(mybuf)[e] = a.x[e];
         if (a.check_finite) bad |= !finite_f(a.x[e]);

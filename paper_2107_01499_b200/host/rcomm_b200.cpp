@@ -99,12 +99,13 @@ std::vector<float> to_host(std::span<const float> x) {
 }
 
 void check_codec(const Codec& c, std::mt19937* rng, bool collective = true) {
-  if (c.kind == CodecKind::uniform8 && c.rounding == Rounding::stochastic) {
-    if (!rng) throw Error(B2_ERR_INVALID, "uniform8 stochastic rounding needs a generator");  // codec.cpp:70
-    if (collective)
-      throw Error(B2_ERR_UNSUPPORTED, "uniform8 stochastic rounding is implemented for the codec, not the collectives");
-  }
+  (void)collective;
+  if (c.kind == CodecKind::uniform8 && c.rounding == Rounding::stochastic && !rng)
+    throw Error(B2_ERR_INVALID, "uniform8 stochastic rounding needs a generator");  // codec.cpp:70
 }
+bool stochastic(const Codec& c) { return c.kind == CodecKind::uniform8 && c.rounding == Rounding::stochastic; }
+// one 64-bit seed per call, advancing the caller's generator (codec.cpp:71-74)
+std::uint64_t draw_seed(std::mt19937* rng) { return (std::uint64_t((*rng)()) << 32) | std::uint64_t((*rng)()); }
 
 }  // namespace
 
@@ -407,8 +408,12 @@ double c_lp_s(B200Endpoint& ep, double now, std::span<float> x, const Codec& cod
   DeviceScope ds(ep.device());
   auto s = static_cast<cudaStream_t>(ep.stream());
   Staged b(ep, bucket, x, s);
-  check(b2_c_lp_s(ep.handle(), b.dev, x.size(), static_cast<int>(codec.kind), es ? es->delta() : nullptr,
-                  es ? es->delta_len() : 0, es ? es->epsilon() : nullptr, es ? es->epsilon_len() : 0, bucket, s));
+  if (stochastic(codec))
+    check(b2_c_lp_s_stochastic(ep.handle(), b.dev, x.size(), es ? es->delta() : nullptr, es ? es->delta_len() : 0,
+                               es ? es->epsilon() : nullptr, es ? es->epsilon_len() : 0, draw_seed(rng), bucket, s));
+  else
+    check(b2_c_lp_s(ep.handle(), b.dev, x.size(), static_cast<int>(codec.kind), es ? es->delta() : nullptr,
+                    es ? es->delta_len() : 0, es ? es->epsilon() : nullptr, es ? es->epsilon_len() : 0, bucket, s));
   ep.sync();  // throws on a latched device error before anything is written back
   b.finish(s);
   const int g = ep.world_size(), me = ep.rank();
@@ -450,8 +455,12 @@ double d_lp_s(B200Endpoint& ep, double now, std::span<float> x, const Topology& 
   DeviceScope ds(ep.device());
   auto s = static_cast<cudaStream_t>(ep.stream());
   Staged b(ep, bucket, x, s);
-  check(b2_d_lp_s(ep.handle(), b.dev, x.size(), nb.data(), static_cast<int>(nb.size()), static_cast<int>(codec.kind),
-                  static_cast<int>(mode), bucket, s));
+  if (stochastic(codec))
+    check(b2_d_lp_s_stochastic(ep.handle(), b.dev, x.size(), nb.data(), static_cast<int>(nb.size()),
+                               static_cast<int>(mode), draw_seed(rng), bucket, s));
+  else
+    check(b2_d_lp_s(ep.handle(), b.dev, x.size(), nb.data(), static_cast<int>(nb.size()),
+                    static_cast<int>(codec.kind), static_cast<int>(mode), bucket, s));
   ep.sync();  // throws on a latched device error before anything is written back
   b.finish(s);
   ep.account((nb.size() - 1) * codec.payload_size(x.size()), nb.size() - 1);

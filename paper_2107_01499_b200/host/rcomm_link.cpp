@@ -51,14 +51,15 @@ NvlEndpoint& nvl(Endpoint& ep) {
   return *p;
 }
 
-// The B200 path has no stochastic rounding inside the collectives (the
-// reference draws it from a host std::mt19937 stream, codec.cpp:67-78).
 void check_codec(const Codec& c, std::mt19937* rng) {
-  if (c.kind == CodecKind::uniform8 && c.rounding == Rounding::stochastic) {
-    if (!rng) throw Error("uniform8 stochastic rounding needs a generator");  // codec.cpp:70
-    throw Error("uniform8 stochastic rounding is not supported by the B200 collectives");
-  }
+  if (c.kind == CodecKind::uniform8 && c.rounding == Rounding::stochastic && !rng)
+    throw Error("uniform8 stochastic rounding needs a generator");  // codec.cpp:70
 }
+// Rounding::stochastic: one 64-bit seed per call from the caller's generator
+// (the levels' distribution is the reference's; the draws are a counter hash
+// on the device, not the mt19937 stream, codec.cpp:67-78)
+bool stochastic(const Codec& c) { return c.kind == CodecKind::uniform8 && c.rounding == Rounding::stochastic; }
+std::uint64_t draw_seed(std::mt19937* rng) { return (std::uint64_t((*rng)()) << 32) | std::uint64_t((*rng)()); }
 
 std::size_t payload_bytes(const Codec& c, std::size_t n) {  // codec.cpp:31-38
   return b2_payload_size(static_cast<int>(c.kind), n);
@@ -253,7 +254,11 @@ double c_lp_s(Endpoint& ep_, double now, std::span<float> x, const Codec& codec,
     if (es->delta.size() != len) throw Error("c_lp_s: delta length does not match bucket length");
     if (es->epsilon.size() != mylen) throw Error("c_lp_s: epsilon length does not match owned partition");
   }
+  const std::uint64_t seed = stochastic(codec) ? draw_seed(rng) : 0;
   staged_call(ep, bucket, x, es, [&](float* dx, float* dd, float* de, cudaStream_t s) {
+    if (stochastic(codec))
+      return b2_c_lp_s_stochastic(ep.handle(), dx, len, dd, es ? es->delta.size() : 0, es ? de : nullptr,
+                                  es ? es->epsilon.size() : 0, seed, bucket, s);
     return b2_c_lp_s(ep.handle(), dx, len, static_cast<int>(codec.kind), dd, es ? es->delta.size() : 0,
                      es ? de : nullptr, es ? es->epsilon.size() : 0, bucket, s);
   });
@@ -286,9 +291,14 @@ double d_lp_s(Endpoint& ep_, double now, std::span<float> x, const Topology& top
   check_codec(codec, rng);
   if (topo.n != ep.world_size()) throw Error("topology size mismatch");
   const auto nb = topo.neighbors(ep.rank(), round);
+  const std::uint64_t seed = stochastic(codec) ? draw_seed(rng) : 0;
   staged_call(ep, bucket, x, nullptr, [&](float* dx, float*, float*, cudaStream_t s) {
-    return b2_d_lp_s(ep.handle(), dx, x.size(), nb.data(), static_cast<int>(nb.size()), static_cast<int>(codec.kind),
-                     mode == ReduceMode::average ? B2_REDUCE_AVERAGE : B2_REDUCE_SUM, bucket, s);
+    const int md = mode == ReduceMode::average ? B2_REDUCE_AVERAGE : B2_REDUCE_SUM;
+    if (stochastic(codec))
+      return b2_d_lp_s_stochastic(ep.handle(), dx, x.size(), nb.data(), static_cast<int>(nb.size()), md, seed,
+                                  bucket, s);
+    return b2_d_lp_s(ep.handle(), dx, x.size(), nb.data(), static_cast<int>(nb.size()),
+                     static_cast<int>(codec.kind), md, bucket, s);
   });
   ep.account((nb.size() - 1) * payload_bytes(codec, x.size()), nb.size() - 1);
   return now;

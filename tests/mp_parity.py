@@ -242,6 +242,42 @@ def run(args):
         ck.eq(f"d_lp_s identity n={n}", t.cpu().numpy(),
               orc.d_fp_s_rank([xs[j] for j in topo.neighbors(rank, 0)], 1))
 
+    # ---- stochastic rounding inside C_LP_S / D_LP_S (codec.cpp:67-78): the
+    # expectation over calls is the exact sum / neighbourhood mean; every rank
+    # of a C_LP_S call holds the same bucket
+    import random
+    ST = b2.Codec(b2.CodecKind.uniform8, b2.Rounding.stochastic)
+    n, calls = 20_000, 60
+    bucket += 1
+    xs = [orc.synth(n, 8300 + r) for r in range(g)]
+    rng = random.Random(100 + rank)  # per-rank generators (the seed mixes the rank anyway)
+    acc = np.zeros(n, np.float64)
+    accd = np.zeros(n, np.float64)
+    ring = b2.Topology(b2.TopologyKind.ring, g, 0)
+    nb = ring.neighbors(rank, 0)
+    for c in range(calls):
+        t = torch.as_tensor(xs[rank]).cuda()
+        b2.c_lp_s(ep, 0.0, t, ST, None, rng, bucket=bucket)
+        out = t.cpu().numpy()
+        acc += out
+        if c == 0:
+            replicas_identical(ck, "c_lp_s stochastic", t, g, rank)
+        t = torch.as_tensor(xs[rank]).cuda()
+        b2.d_lp_s(ep, 0.0, t, ring, 0, ST, b2.ReduceMode.average, rng, bucket=bucket + 1)
+        accd += t.cpu().numpy()
+    bucket += 1
+    want = np.sum([x.astype(np.float64) for x in xs], axis=0)
+    wantd = np.mean([xs[j].astype(np.float64) for j in nb], axis=0)
+    # per element the two stochastic roundings add variance <= (g step1^2 + step2^2) / 4
+    step1 = 2.0 / 255.0
+    step2 = 2.0 * g / 255.0
+    tol = 6.0 * np.sqrt((g * step1 ** 2 + step2 ** 2) / 4.0 / calls)
+    if np.abs(acc / calls - want).mean() < tol / 3 and np.abs(accd / calls - wantd).mean() < tol / 3:
+        ck.passed += 1
+    else:
+        ck.fail.append(f"rank{rank} stochastic C_LP_S/D_LP_S biased: {np.abs(acc / calls - want).mean()} "
+                       f"{np.abs(accd / calls - wantd).mean()} tol {tol / 3}")
+
     # ---- D_* between the register capacity and the ring cut-over: the
     # streaming per-CTA kernel (small_coll.cu decent_stream_kernel)
     for n in (6_000_001, 16_000_000):

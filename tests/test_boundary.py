@@ -128,9 +128,13 @@ def test_codec_host_errors():
     with pytest.raises(b2.Error, match="needs a generator"):
         b2.Codec(b2.CodecKind.uniform8, b2.Rounding.stochastic)._check_supported(None)
     import random
-    with pytest.raises(b2.Error):  # the collectives keep rejecting stochastic rounding
-        b2.Codec(b2.CodecKind.uniform8, b2.Rounding.stochastic)._check_supported(random.Random(1))
-    b2.Codec(b2.CodecKind.uniform8, b2.Rounding.stochastic)._check_supported(random.Random(1), collective=False)
+    c = b2.Codec(b2.CodecKind.uniform8, b2.Rounding.stochastic)
+    c._check_supported(random.Random(1))  # the collectives take stochastic rounding (b2_c_lp_s_stochastic)
+    c._check_supported(random.Random(1), collective=False)
+    assert c.stochastic() and not b2.Codec(b2.CodecKind.uniform8).stochastic()
+    r = random.Random(5)
+    s1 = c._seed(r)
+    assert s1 != c._seed(r)  # the generator advances per call (codec.cpp:71-74)
     b2.Codec(b2.CodecKind.onebit)._check_supported(None)  # every primitive takes the onebit codec
     assert b2.phase.make_tag(3, b2.phase.bcast) == 51
 

@@ -85,8 +85,8 @@ def test_nonfinite_raises():
         U8.decode(torch.tensor([1, 2, 3], dtype=torch.uint8).cuda(), 10)
 
 
-def test_stochastic_rounding_is_rejected():
-    with pytest.raises(b2.Error):
+def test_stochastic_rounding_needs_a_generator():
+    with pytest.raises(b2.Error):  # codec.cpp:70
         b2.Codec(b2.CodecKind.uniform8, b2.Rounding.stochastic).encode(dev([1.0, 2.0]))
 
 

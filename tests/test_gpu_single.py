@@ -325,3 +325,43 @@ def test_engine_reports_nonfinite_gradient(oracle):
         oracle.c_lp_s(xs, codec=1)
         assert np.array_equal(bits(eng.arenas[bk.id].cpu().numpy()), bits(xs[0]))
     ep.close()
+
+
+def test_c_lp_s_stochastic_g1_unbiased(ep):
+    """Codec{uniform8, Rounding::stochastic} inside C_LP_S and D_LP_S
+    (codec.cpp:67-78): every encode rounds stochastically; the expected output
+    equals the input (test_codec.cpp:175-192's unbiasedness), outputs lie on
+    the 1/255 grid of the headers (0, 1), the same generator state gives the
+    same result and the generator advances per call."""
+    import random
+    st = b2.Codec(b2.CodecKind.uniform8, b2.Rounding.stochastic)
+    n = 200_000
+    x = np.full(n, 0.3777, np.float32)
+    x[0], x[1] = 0.0, 1.0
+    for prim in ("c_lp_s", "d_lp_s"):
+        rng = random.Random(3)
+        outs = []
+        for _ in range(2):
+            t = torch.as_tensor(x).cuda()
+            if prim == "c_lp_s":
+                b2.c_lp_s(ep, 0.0, t, st, None, rng, bucket=40)
+            else:
+                b2.d_lp_s(ep, 0.0, t, b2.Topology(b2.TopologyKind.ring, 1), 0, st, b2.ReduceMode.average, rng,
+                          bucket=41)
+            outs.append(t.cpu().numpy())
+        y = outs[0].astype(np.float64)
+        assert y[0] == 0.0 and y[1] == 1.0
+        lv = np.round(y * 255.0)
+        assert np.all(np.abs(y - lv / 255.0) < 1e-6)  # on the grid
+        e = y[2:] - np.float64(np.float32(0.3777))
+        assert abs(e.mean()) <= 4.0 * np.sqrt(e.var() / e.size), (prim, e.mean())
+        assert not np.array_equal(outs[0], outs[1])  # the generator advanced
+        t = torch.as_tensor(x).cuda()
+        if prim == "c_lp_s":
+            b2.c_lp_s(ep, 0.0, t, st, None, random.Random(3), bucket=40)
+        else:
+            b2.d_lp_s(ep, 0.0, t, b2.Topology(b2.TopologyKind.ring, 1), 0, st, b2.ReduceMode.average,
+                      random.Random(3), bucket=41)
+        assert np.array_equal(t.cpu().numpy(), outs[0])  # same stream, same draws
+    with pytest.raises(b2.Error):
+        b2.c_lp_s(ep, 0.0, torch.as_tensor(x).cuda(), st, None, None)  # codec.cpp:68-70
