@@ -216,6 +216,14 @@ int b2_c_lp_s(b2_comm_t comm, float* x, size_t n, int codec, float* delta, size_
               float* eps, size_t eps_len, uint32_t bucket, void* stream);
 int b2_d_fp_s(b2_comm_t comm, float* x, size_t n, const int* nbrs, int n_nbrs, int mode,
               uint32_t bucket, void* stream);
+/* hierarchical_c (collectives.hpp:80-82, collectives.cpp:290-385) over ONE
+ * node -- every rank of the communicator shares the NVLink domain: the
+ * reference sums the members in fp64 in ascending rank order from +0.0 and
+ * rounds once, with no compression whatever the codec (collectives.cpp:
+ * 377-380), which is C_FP_S's fold for two or more ranks and (float)(0.0 +
+ * (double)x) for one.  (Node layouts spanning several nodes need an
+ * inter-node transport, which this path does not have.) */
+int b2_hierarchical_c(b2_comm_t comm, float* x, size_t n, uint32_t bucket, void* stream);
 int b2_c_lp_s_stochastic(b2_comm_t comm, float* x, size_t n, float* delta, size_t delta_len, float* eps,
                          size_t eps_len, uint64_t seed, uint32_t bucket, void* stream);
 int b2_d_lp_s_stochastic(b2_comm_t comm, float* x, size_t n, const int* nbrs, int n_nbrs, int mode,

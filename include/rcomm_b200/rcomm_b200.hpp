@@ -172,6 +172,10 @@ double c_lp_s(B200Endpoint& ep, double now, std::span<float> x, const Codec& cod
               std::mt19937* rng = nullptr, std::uint32_t bucket = 0);
 double d_fp_s(B200Endpoint& ep, double now, std::span<float> x, const Topology& topo, std::uint64_t round,
               ReduceMode mode, std::uint32_t bucket = 0);
+// collectives.hpp:80-82 over one NVLink node (every rank of the endpoint):
+// the reference's member fold without compression, whatever the codec
+double hierarchical_c(B200Endpoint& ep, double now, std::span<float> x, const Codec& codec, ErrorState* es,
+                      std::mt19937* rng = nullptr, std::uint32_t bucket = 0);
 double d_lp_s(B200Endpoint& ep, double now, std::span<float> x, const Topology& topo, std::uint64_t round,
               const Codec& codec, ReduceMode mode, std::mt19937* rng = nullptr, std::uint32_t bucket = 0);
 

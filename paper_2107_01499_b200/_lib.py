@@ -64,6 +64,7 @@ _SIGS = {
     "b2_c_fp_s": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint32, C.c_void_p]),
     "b2_c_lp_s": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_size_t,
                             C.c_void_p, C.c_size_t, C.c_uint32, C.c_void_p]),
+    "b2_hierarchical_c": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint32, C.c_void_p]),
     "b2_c_lp_s_stochastic": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_void_p,
                                        C.c_size_t, C.c_uint64, C.c_uint32, C.c_void_p]),
     "b2_d_lp_s_stochastic": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_int), C.c_int, C.c_int,

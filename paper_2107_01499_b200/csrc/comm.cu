@@ -746,6 +746,14 @@ int b2_d_lp_s_stochastic(b2_comm_t c, float* x, size_t n, const int* nbrs, int n
   return decentral(c, x, n, nbrs, n_nbrs, B2_CODEC_UNIFORM8, 1, mode, bucket, stream, 1, seed);
 }
 
+int b2_hierarchical_c(b2_comm_t c, float* x, size_t n, uint32_t bucket, void* stream) {
+  int rc = check_comm(c, x, n);
+  if (rc) return rc;
+  if (c->world > 1) return central(c, x, n, B2_CODEC_IDENTITY, 0, nullptr, 0, nullptr, 0, bucket, stream);
+  const int self = c->rank;  // one rank: (float)(0.0 + (double)x), D_FP_S over {self}
+  return decentral(c, x, n, &self, 1, B2_CODEC_IDENTITY, 0, B2_REDUCE_SUM, bucket, stream);
+}
+
 int b2_d_fp_s(b2_comm_t c, float* x, size_t n, const int* nbrs, int n_nbrs, int mode,
               uint32_t bucket, void* stream) {
   return decentral(c, x, n, nbrs, n_nbrs, B2_CODEC_IDENTITY, 0, mode, bucket, stream);

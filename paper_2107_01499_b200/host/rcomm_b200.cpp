@@ -427,6 +427,20 @@ double c_lp_s(B200Endpoint& ep, double now, std::span<float> x, const Codec& cod
   return now;
 }
 
+double hierarchical_c(B200Endpoint& ep, double now, std::span<float> x, const Codec& codec, ErrorState* es,
+                      std::mt19937* rng, std::uint32_t bucket) {  // collectives.cpp:290-385, one NVLink node
+  (void)codec;
+  (void)es;
+  (void)rng;
+  DeviceScope ds(ep.device());
+  auto s = static_cast<cudaStream_t>(ep.stream());
+  Staged b(ep, bucket, x, s);
+  check(b2_hierarchical_c(ep.handle(), b.dev, x.size(), bucket, s));
+  ep.sync();
+  b.finish(s);
+  return now;
+}
+
 namespace {
 std::vector<int> nbrs_of(B200Endpoint& ep, const Topology& topo, std::uint64_t round) {
   if (topo.n != ep.world_size()) throw Error(B2_ERR_INVALID, "topology size mismatch");  // collectives.cpp:232

@@ -322,10 +322,8 @@ double hierarchical_c(Endpoint& ep_, double now, std::span<float> x, const Codec
     if (ep.node_of(r) != ep.node_of(0))
       throw Error("hierarchical_c: ranks on more than one node need an inter-node transport "
                   "(the B200 path spans one NVLink domain)");
-  if (n > 1) return c_fp_s(ep, now, x, bucket);
-  const int self[1] = {ep.rank()};
   staged_call(ep, bucket, x, nullptr, [&](float* dx, float*, float*, cudaStream_t s) {
-    return b2_d_fp_s(ep.handle(), dx, x.size(), self, 1, B2_REDUCE_SUM, bucket, s);
+    return b2_hierarchical_c(ep.handle(), dx, x.size(), bucket, s);
   });
   return now;
 }

@@ -365,3 +365,19 @@ def test_c_lp_s_stochastic_g1_unbiased(ep):
         assert np.array_equal(t.cpu().numpy(), outs[0])  # same stream, same draws
     with pytest.raises(b2.Error):
         b2.c_lp_s(ep, 0.0, torch.as_tensor(x).cuda(), st, None, None)  # codec.cpp:68-70
+
+
+def test_hierarchical_c_one_rank_c_abi(ep, oracle):
+    """b2_hierarchical_c over one node with one rank: the reference's member
+    fold (float)(0.0 + (double)x) (collectives.cpp:321-332, 377-380), so -0.0
+    becomes +0.0 and every other value is unchanged."""
+    x = oracle.synth(4099, 12)
+    x[::7] = -0.0
+    want = x.copy()
+    oracle.hierarchical_c([want], [0], 1)
+    t = torch.as_tensor(x).cuda()
+    b2._lib.check(b2.lib.b2_hierarchical_c(ep.handle, t.data_ptr(), t.numel(), 50,
+                                           torch.cuda.current_stream().cuda_stream))
+    ep.sync()
+    assert np.array_equal(bits(t.cpu().numpy()), bits(want))
+    assert not np.signbit(t.cpu().numpy()[0])
