@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -260,20 +261,28 @@ __global__ void __launch_bounds__(kSmallThreads) encode_small_kernel(const float
     }
 }
 
-// decode: 4 codes (one 32-bit load) -> one float4 store per thread, no ring
-// (measured: 6.8 us at 4M against 7.7 us for 16 codes per thread -- the
-// kernel is latency-bound and wants the wider grid)
+// decode: V x 4 codes (V 32-bit loads) -> V float4 stores per thread, no
+// ring.  V = 1 by default (measured: 6.0-6.8 us at 4M, against 7.7 us with 16
+// codes per thread: the kernel is latency-bound and wants the wider grid).
+template <int V>
 __global__ void __launch_bounds__(kSmallThreads) decode_small_kernel(const uint8_t* __restrict__ codes,
                                                                      const float* hdr, size_t n,
                                                                      float* __restrict__ out) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the encode's codes and header are complete
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const U8Params q = u8_params(hdr[0], hdr[1]);
-  const size_t ng = n >> 2;
+  const size_t ng = n >> 2, T = size_t(gridDim.x) * kSmallThreads;
   const uint32_t* c32 = reinterpret_cast<const uint32_t*>(codes);
   float4* o4 = reinterpret_cast<float4*>(out);
-  for (size_t g = size_t(blockIdx.x) * kSmallThreads + threadIdx.x; g < ng; g += size_t(gridDim.x) * kSmallThreads)
-    __stcs(o4 + g, dequant4(__ldcs(c32 + g), q));
+  for (size_t g0 = size_t(blockIdx.x) * kSmallThreads + threadIdx.x; g0 < ng; g0 += V * T) {
+    uint32_t c[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (g0 + v * T < ng) c[v] = __ldcs(c32 + g0 + v * T);
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (g0 + v * T < ng) __stcs(o4 + g0 + v * T, dequant4(c[v], q));
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0)
     for (size_t e = 4 * ng; e < n; ++e) out[e] = dequant1(codes[e], q.lo, q.step);
 }
@@ -599,6 +608,15 @@ extern "C" {
 
 const char* b2_last_error(void) { return b2::last_error(); }
 
+// B2_NO_PDL=1: plain launches of the small codec kernels (A/B runs)
+static bool pdl_on() {
+  static const bool v = [] {
+    const char* e = getenv("B2_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return v;
+}
+
 // per-device scratch of the small-bucket encode: one (min, max) partial per CTA
 static float2* small_partials() {
   static std::mutex mu;
@@ -641,7 +659,7 @@ static int try_small_encode(const float* x, float* delta, size_t n, uint8_t* cod
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the launch with the previous kernel's tail
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = pdl_on() ? 2 : 1;
   B2_CUDA_TRY(cudaLaunchKernelExC(&cfg, fn, params));
   return B2_OK;
 }
@@ -748,8 +766,14 @@ int b2_u8_decode(const uint8_t* codes, const float* hdr, size_t n, float* out, v
   B2_REQUIRE(aligned16(out), "b2_u8_decode: out must be 16-byte aligned");
   B2_REQUIRE(aligned16(codes), "b2_u8_decode: codes must be 16-byte aligned");
   if (n <= (size_t(64) << 20)) {  // small buckets: one 32-bit load -> one float4 store per thread
+    static const int V = [] {  // B2_DEC_V: codes-per-thread / 4 (A/B runs)
+      const char* e = getenv("B2_DEC_V");
+      const int v = e ? std::atoi(e) : 1;
+      return v == 2 || v == 4 ? v : 1;
+    }();
     const size_t ng = std::max<size_t>(n >> 2, 1);
-    const int grid = int(std::min<size_t>((ng + kSmallThreads - 1) / kSmallThreads, size_t(sm_count()) * 16));
+    const int grid = int(std::min<size_t>((ng + V * kSmallThreads - 1) / (V * kSmallThreads),
+                                          size_t(sm_count()) * 16));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kSmallThreads);
@@ -758,8 +782,13 @@ int b2_u8_decode(const uint8_t* codes, const float* hdr, size_t n, float* out, v
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
-    B2_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_small_kernel, codes, hdr, n, out));
+    cfg.numAttrs = pdl_on() ? 1 : 0;
+    if (V == 2)
+      B2_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_small_kernel<2>, codes, hdr, n, out));
+    else if (V == 4)
+      B2_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_small_kernel<4>, codes, hdr, n, out));
+    else
+      B2_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_small_kernel<1>, codes, hdr, n, out));
     B2_CUDA_TRY(cudaGetLastError());
     return B2_OK;
   }
