@@ -274,28 +274,33 @@ def run_b200(args, rank: int, world: int):
     # The standalone codec's step (encode + decode, two launches, ~15 us of
     # GPU work) is launch-bound from Python: its steps replay a CUDA graph of
     # the two launches (captured once; the same kernels, same buffers).
+    # A graph holds GK consecutive steps (each a full encode + decode of the
+    # bucket); the timed loop replays it steps / GK times, so the graph's own
+    # launch (~6 us) is paid once per GK steps, as a training loop capturing
+    # its steps would.
     graph = None
     eager_step = step
+    GK = 1
     if prim in ("codec", "onebit") and not args.no_graph:
+        GK = max(1, min(10, args.steps))
+        while args.steps % GK:
+            GK -= 1
         try:
             graph = torch.cuda.CUDAGraph()
             cap = torch.cuda.Stream()
             cap.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(cap):
                 with torch.cuda.graph(graph, stream=cap):
-                    step(xs[0])
+                    for _ in range(GK):
+                        step(xs[0])
             torch.cuda.current_stream().wait_stream(cap)
-            launches_box[0] -= 2  # the capture launched nothing
+            launches_box[0] -= 2 * GK  # the capture launched nothing
             graph.replay()
-            launches_box[0] += 2
+            launches_box[0] += 2 * GK
             torch.cuda.synchronize()
         except Exception as e:  # noqa: BLE001  (capture unsupported: eager launches)
             print(json.dumps({"graph_capture": f"failed: {e}"}), file=sys.stderr)
-            graph = None
-        if graph is not None:
-            def step(buf, _g=graph):  # noqa: F811
-                _g.replay()
-                launches_box[0] += 2
+            graph, GK = None, 1
     launches0 = n_launches()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -303,8 +308,13 @@ def run_b200(args, rank: int, world: int):
         torch.cuda.profiler.start()
     with ClockSampler(dev) as clk:
         ev0.record(stream)
-        for i in range(args.steps):
-            step(xs[i % nbuf])
+        if graph is not None:
+            for _ in range(args.steps // GK):
+                graph.replay()
+                launches_box[0] += 2 * GK
+        else:
+            for i in range(args.steps):
+                step(xs[i % nbuf])
         ev1.record(stream)
         ev1.synchronize()
     if args.profile_range:
@@ -454,6 +464,7 @@ def run_b200(args, rank: int, world: int):
                          if prim not in ("codec", "onebit") else "hand-staged: the standalone codec has no host API"),
                 "ceiling": round(g * 4 * n / (pcie_ms / 1e3) / 1e9, 2), "frac": round(pcie_ms / ems, 3)},
         "gpu_launches": int(launches),
+        "cuda_graph_steps": GK if graph is not None else 0,
         "clocks": clk.summary(),
     }
     if world > 1:  # every rank's GPU clocks during its timed region (run-to-run spread)

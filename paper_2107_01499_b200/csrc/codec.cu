@@ -261,9 +261,9 @@ __global__ void __launch_bounds__(kSmallThreads) encode_small_kernel(const float
     }
 }
 
-// decode: V x 4 codes (V 32-bit loads) -> V float4 stores per thread, no
-// ring.  V = 1 by default (measured: 6.0-6.8 us at 4M, against 7.7 us with 16
-// codes per thread: the kernel is latency-bound and wants the wider grid).
+// decode: V x 4 codes (V 32-bit loads, T apart) -> V float4 stores per
+// thread, no ring.  V = 2 by default (measured in a graph at 4M: 3.8 us,
+// against 4.5 us with V = 1 and 3.9 us with V = 4; tests/cpp/codec_timing.py).
 template <int V>
 __global__ void __launch_bounds__(kSmallThreads) decode_small_kernel(const uint8_t* __restrict__ codes,
                                                                      const float* hdr, size_t n,
@@ -768,8 +768,8 @@ int b2_u8_decode(const uint8_t* codes, const float* hdr, size_t n, float* out, v
   if (n <= (size_t(64) << 20)) {  // small buckets: one 32-bit load -> one float4 store per thread
     static const int V = [] {  // B2_DEC_V: codes-per-thread / 4 (A/B runs)
       const char* e = getenv("B2_DEC_V");
-      const int v = e ? std::atoi(e) : 1;
-      return v == 2 || v == 4 ? v : 1;
+      const int v = e ? std::atoi(e) : 2;
+      return v == 1 || v == 4 ? v : 2;
     }();
     const size_t ng = std::max<size_t>(n >> 2, 1);
     const int grid = int(std::min<size_t>((ng + V * kSmallThreads - 1) / (V * kSmallThreads),
