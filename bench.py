@@ -289,6 +289,9 @@ def run_b200(args, rank: int, world: int):
             graph = torch.cuda.CUDAGraph()
             cap = torch.cuda.Stream()
             cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cap):  # per-stream scratch (onebit) is allocated before the capture
+                step(xs[0])
+            torch.cuda.synchronize()
             with torch.cuda.stream(cap):
                 with torch.cuda.graph(graph, stream=cap):
                     for _ in range(GK):
