@@ -147,6 +147,7 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
   WinHdr* mine = hdr_of(a.win[me]);
   const size_t mbase = mlo & ~size_t(15);
   const unsigned long long gmul = (unsigned long long)g * a.epoch;
+  const bool any_edges = a.n % (16 * size_t(g)) != 0;  // some chunk boundary is not 16-element aligned
   const Rounder r1 = make_rounder(CODEC == kU8 && a.sr_on, a.sr_seed, me, 1);  // the first encode
   const Rounder r2 = make_rounder(CODEC == kU8 && a.sr_on, a.sr_seed, me, 2);  // the owner's second
 
@@ -553,8 +554,10 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     r.timed = false;
     B2_TRACE(kTrP1Done);
     // unaligned heads/tails (warp 0 of the last CTA): pushed with plain stores,
-    // announced on arrive_e; then the fold of my chunk's own heads/tails
-    if (cons && blockIdx.x == G - 1 && ct < 32) {
+    // announced on arrive_e; then the fold of my chunk's own heads/tails.
+    // Every rank knows from (n, g) alone whether any chunk has one: when none
+    // has (n % 16g == 0, the BASELINE sizes) the rendezvous is skipped.
+    if (cons && blockIdx.x == G - 1 && ct < 32 && any_edges) {
       for (int i = 0; i < g; ++i) {
         const U8Params p = s_p1[i];
         uint8_t* dst = a.win[me] + a.off_recv1 + size_t(ck(i)) * a.slot_stride;
@@ -667,8 +670,9 @@ __device__ __forceinline__ void central_body(const CentralArgs& a, Ring& r) {
     r.timed = false;
     B2_TRACE(kTrP1Done);
     // unaligned heads/tails (warp 0 of the last CTA): copies, announced on
-    // arrive_e; then the fold of my chunk's own heads/tails
-    if (cons && blockIdx.x == G - 1 && ct < 32) {
+    // arrive_e; then the fold of my chunk's own heads/tails (skipped when no
+    // chunk has one, as above)
+    if (cons && blockIdx.x == G - 1 && ct < 32 && any_edges) {
       for (int i = 0; i < g; ++i) {
         float* dstf = reinterpret_cast<float*>(a.win[me] + a.off_recv1 + size_t(ck(i)) * a.slot_stride);
         const size_t ebase = pc[i].s & ~size_t(15);
@@ -1062,7 +1066,8 @@ __device__ __forceinline__ void decent_body(const DecentArgs& a, Ring& r) {
   B2_TRACE(kTrP1Done);
   // unaligned tail (warp 0 of the last CTA): encode it, announce it on every
   // neighbour's arrive_e, then fold it once every neighbour's tail is in
-  if (cons && blockIdx.x == G - 1 && ct < 32) {
+  // (every rank skips it alike when n % 16 == 0: there is no tail)
+  if (cons && blockIdx.x == G - 1 && ct < 32 && (a.n & 15)) {
     r.edges(px, [&](size_t e) {
       if (CODEC == kU8) {
         mybuf[e] = q1r(a.x[e], q8.lo, q8.inv, rd, e);
