@@ -18,7 +18,8 @@ INCLUDE = os.path.join(REPO, "include")
 LIB = os.path.join(PKG_DIR, "libb2comm.so")
 HOSTLIB = os.path.join(PKG_DIR, "librcomm_b200.so")
 
-CUDA_SOURCES = ["codec.cu", "collectives.cu", "comm.cu", "onebit_coll.cu", "small_coll.cu", "central_stag.cu"]
+CUDA_SOURCES = ["codec.cu", "collectives.cu", "comm.cu", "onebit_coll.cu", "small_coll.cu", "central_stag.cu",
+                "small_central.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

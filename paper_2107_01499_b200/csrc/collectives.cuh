@@ -60,6 +60,7 @@ struct CentralArgs {
   // staggered C_LP_S (central_stag.cu): per-source arrival counters of my
   // chunk [g][sgate_stride], my out2 publication counters, landing slots
   size_t off_sgate, sgate_stride, off_qgate, off_land;
+  size_t off_sgate2;            // small_central.cu: per-source out2 publication counters [g][sgate_stride]
   float2* partials;             // local workspace [(kMaxRanks + 1) * grid]
   unsigned* cta_done;           // local workspace [kMaxRanks + 2]
   unsigned* gridbar;            // local workspace [2]: consumer grid barrier
@@ -124,6 +125,12 @@ struct SrcDecS {
 // gate_stride > kSmallMaxGridD.
 constexpr size_t kSmallDecentMax = 16000000;
 constexpr size_t kSmallMaxGridD = 1024;
+// C_* buckets up to this many elements try the register-resident kernel
+// (small_central.cu); windows that may take it carry its two per-CTA counter
+// arrays [g][kSmallMaxGridD].  kSmallCentralWin bounds the windows that
+// reserve them (B2_SMALL_C_MAX cannot raise the cut-over above it).
+constexpr size_t kSmallCentralMax = 4000000;
+constexpr size_t kSmallCentralWin = 16000000;
 
 // Decentralized neighbourhood reduce (D_FP_S, D_LP_S).
 struct DecentArgs {

@@ -33,6 +33,7 @@ int launch_central(const CentralArgs& a, int codec, bool ec, cudaStream_t s, int
 int launch_decent(const DecentArgs& a, int codec, cudaStream_t s, int sms);
 int launch_decent_small(const DecentArgs& a, int codec, cudaStream_t s, int sms);
 int launch_central_stag(const CentralArgs& a, bool ec, cudaStream_t s, int sms);
+int launch_central_small(const CentralArgs& a, int codec, bool ec, cudaStream_t s, int sms);
 int max_persistent_grid();
 int launch_onebit_central(const OnebitArgs& a, bool ec, cudaStream_t s, int sms);
 int launch_onebit_decent(const OnebitDecentArgs& a, cudaStream_t s, int sms);
@@ -52,7 +53,9 @@ struct Window {
   bool ipc_opened[kMaxRanks] = {};
   size_t off_gate = 0, gate_stride = 0, off_recv1 = 0, slot_stride = 0, off_out2 = 0, off_dbuf[2] = {0, 0};
   size_t off_sgate = 0, sgate_stride = 0, off_qgate = 0, off_land = 0;  // central_stag.cu
+  size_t off_cgate = 0, off_cgate2 = 0;  // small_central.cu: [g][kSmallMaxGridD] each, or 0
   unsigned long long epoch = 0;
+  unsigned long long small_calls = 0;    // small_central.cu launches (its counters' target)
   unsigned long long exp_reads[2] = {0, 0};
   unsigned long long sends_from[kMaxRanks] = {};  // D_*: calls (|N| > 1) in which rank j sent to me
   float2* partials = nullptr;
@@ -141,6 +144,12 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
     off += round_up(sizeof(unsigned long long) * nreg * size_t(g), 256);
     w->off_qgate = off;
     off += round_up(sizeof(unsigned long long) * nreg, 256);
+    if (n <= kSmallCentralWin && g > 1) {  // small_central.cu: per-CTA counters
+      w->off_cgate = off;
+      off += round_up(sizeof(unsigned long long) * kSmallMaxGridD * size_t(g), 256);
+      w->off_cgate2 = off;
+      off += round_up(sizeof(unsigned long long) * kSmallMaxGridD * size_t(g), 256);
+    }
     // chunk k sits at slot offset e - (lo_k & ~15): up to 15 elements of head room
     w->slot_stride = round_up(size_t(elem) * (maxchunk + 16), 256);
     w->off_recv1 = off;
@@ -190,7 +199,8 @@ int get_window(b2_comm* c, uint32_t bucket, int family, size_t n, int elem, Wind
       cudaMalloc(&w->local, w->bytes) == cudaSuccess &&
       cudaMemset(w->local, 0, (family == kDecentral || family == kOnebitD) ? w->off_dbuf[0] : w->off_recv1) ==
           cudaSuccess &&
-      cudaMalloc(&w->partials, sizeof(float2) * (kMaxRanks + 1) * max_persistent_grid()) == cudaSuccess &&
+      cudaMalloc(&w->partials, sizeof(float2) * (kMaxRanks + 1) *
+                                   std::max<size_t>(max_persistent_grid(), kSmallMaxGridD)) == cudaSuccess &&
       cudaMalloc(&w->cta_done, sizeof(unsigned) * (kMaxRanks + 4)) == cudaSuccess &&
       cudaMemset(w->cta_done, 0, sizeof(unsigned) * (kMaxRanks + 4)) == cudaSuccess &&
       cudaMalloc(&w->sched, sizeof(unsigned long long) * (kSchedPasses + 1)) == cudaSuccess &&
@@ -562,7 +572,6 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   a.g = c->world;
   a.me = c->rank;
   a.check_finite = check_finite;
-  a.epoch = ++w->epoch;
   a.delta = delta;
   a.eps = eps;
   for (int j = 0; j < c->world; ++j) a.win[j] = w->peer[j];
@@ -584,6 +593,25 @@ static int central(b2_comm_t c, float* x, size_t n, int codec, int check_finite,
   a.trace = c->trace;
   a.sr_on = sr_on;
   a.sr_seed = sr_seed;
+  // small buckets: the register-resident kernel (small_central.cu), with its
+  // own call counter and counter arrays
+  rc = B2_ERR_UNSUPPORTED;
+  if (w->off_cgate) {
+    CentralArgs sa = a;
+    sa.epoch = w->small_calls + 1;
+    sa.off_sgate = w->off_cgate;
+    sa.off_sgate2 = w->off_cgate2;
+    sa.sgate_stride = kSmallMaxGridD;
+    rc = launch_central_small(sa, codec == B2_CODEC_UNIFORM8 ? kU8 : kIdentity, delta != nullptr,
+                              static_cast<cudaStream_t>(stream), c->sm_budget);
+    if (rc == B2_OK) {
+      ++w->small_calls;
+      ++c->launches;
+      return rc;
+    }
+    if (rc != B2_ERR_UNSUPPORTED) return rc;
+  }
+  a.epoch = ++w->epoch;
   // uint8 at g == 2 with 16-aligned equal chunks: the staggered schedule
   // (central_stag.cu; measured faster at g = 2 only); every
   // rank decides identically from (n, g)

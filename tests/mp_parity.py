@@ -322,6 +322,33 @@ def run(args):
         ck.eq(f"c_lp_s+EC aligned n={n} delta", es.delta.cpu().numpy(), deltas[rank])
         ck.eq(f"c_lp_s+EC aligned n={n} eps", es.epsilon.cpu().numpy(), eps[rank])
 
+    # ---- one window switching between the register-resident C_* kernel
+    # (small_central.cu) and the TMA ring as the SM budget changes: separate
+    # call counters per protocol, buffers reused across the two
+    n = 1_000_003
+    bucket += 1
+    own = b2.owned_partition_len(n, g, rank)
+    es = b2.ErrorState(n, own)
+    deltas = [np.zeros(n, np.float32) for _ in range(g)]
+    eps = [np.zeros(b2.owned_partition_len(n, g, r), np.float32) for r in range(g)]
+    for t_, sms in enumerate((0, 4, 4, 0, 0, 4, 0)):
+        ep.set_sm_budget(sms)
+        grads = [orc.synth(n, 7600 + 1000 * r + t_) for r in range(g)]
+        want = [x.copy() for x in grads]
+        orc.c_lp_s(want, codec=1, deltas=deltas, eps=eps)
+        t = torch.as_tensor(grads[rank]).cuda()
+        b2.c_lp_s(ep, 0.0, t, U8, es, bucket=bucket)
+        ck.eq(f"c_lp_s+EC budget-switch n={n} round={t_} sms={sms}", t.cpu().numpy(), want[rank])
+        want = [x.copy() for x in grads]
+        orc.c_fp_s(want)
+        t = torch.as_tensor(grads[rank]).cuda()
+        b2.c_fp_s(ep, 0.0, t, bucket=bucket + 1)
+        ck.eq(f"c_fp_s budget-switch n={n} round={t_} sms={sms}", t.cpu().numpy(), want[rank])
+    ep.set_sm_budget(0)
+    ck.eq(f"c_lp_s+EC budget-switch n={n} delta", es.delta.cpu().numpy(), deltas[rank])
+    ck.eq(f"c_lp_s+EC budget-switch n={n} eps", es.epsilon.cpu().numpy(), eps[rank])
+    bucket += 1
+
     # ---- C_LP_S uint8 + error feedback, acceptance c4 style (many rounds, state carried)
     for n, rounds in ((37, 200), (100_003, 10)):
         bucket += 1

@@ -18,11 +18,12 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def _torchrun(script, args, port, timeout):
+def _torchrun(script, args, port, timeout, env=None):
     g = min(_ngpu(), 8)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={g}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(HERE, script), *args]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout,
+                       env=None if env is None else {**os.environ, **env})
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert lines, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(lines[-1])
@@ -35,6 +36,14 @@ def test_all_primitives_multi_gpu():
     """Every primitive, codec, topology and the stress/EC/engine cases at
     sizes up to 1M (world = every visible GPU up to 8)."""
     res = _torchrun("mp_parity.py", ["--quick"], 29517, 900)
+    assert res["passed"] > 100
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+def test_all_primitives_ring_paths_multi_gpu():
+    """The same cases with the register-resident C_* kernel switched off
+    (B2_SMALL_C_MAX=0): the small buckets take the TMA-ring kernels."""
+    res = _torchrun("mp_parity.py", ["--quick"], 29547, 900, env={"B2_SMALL_C_MAX": "0"})
     assert res["passed"] > 100
 
 
