@@ -92,6 +92,27 @@ def algorithmic_bytes(prim: str, n: int, g: int):
     return 10 * n, 0  # codec: read x, write codes, read codes, write x
 
 
+def kernel_label(prim: str, n: int, g: int) -> str:
+    """The kernel a step launches (the library's dispatch: comm.cu central /
+    decentral, codec.cu small_encode)."""
+    if prim in ("c_lp_s", "c_fp_s"):
+        cod = "uint8" if prim == "c_lp_s" else "identity"
+        if g > 1 and n <= 4_000_000:
+            return f"central_small_kernel<{cod}, g={g}> (register-resident, one cooperative launch per step)"
+        if prim == "c_lp_s" and g == 2 and n % 32 == 0:
+            return "central_stag_kernel<uint8> (staggered schedule, one cooperative launch per step)"
+        return f"central_kernel<{cod}> (one fused launch per step)"
+    if prim in ("d_lp_s", "d_fp_s"):
+        cod = "uint8" if prim == "d_lp_s" else "identity"
+        if n <= 16_000_000:
+            return f"decent_small_kernel / decent_stream_kernel<{cod}> (per-CTA hand-off, one launch per step)"
+        return f"decent_kernel<{cod}> (one fused launch per step)"
+    return {"c_lp_s_onebit": "onebit_central_kernel<g, false> (one cooperative launch per step)",
+            "d_lp_s_onebit": "onebit_decent_kernel<|N|> (one cooperative launch per step)",
+            "codec": "encode_small_kernel + decode_small_kernel (register-resident; ring kernels above the capacity)",
+            "onebit": "onebit_encode_kernel (fp64 |x| sum + sign bits) + onebit_decode_kernel"}[prim]
+
+
 def ncu_traffic(prim: str, g: int):
     """DRAM bytes per launch measured by ncu (profiles/ncu_traffic.json), or None."""
     try:
@@ -437,14 +458,16 @@ def run_b200(args, rank: int, world: int):
     roof["traffic"] = args.traffic if args.traffic is not None else ncu_traffic(prim, g)
     roof["algorithmic_bytes"] = {"hbm": hbm_b, "nvlink_ingress": nvl_b}
     roof["t_roof_us"] = round(max(t_roof_hbm, t_roof_nvl) * 1e6, 1)
-    roof["kernel"] = {"c_lp_s": "central_kernel<uint8> (one fused launch per step)",
-                      "c_lp_s_onebit": "onebit_central_kernel<g, false> (one cooperative launch per step)",
-                      "d_lp_s_onebit": "onebit_decent_kernel<|N|> (one cooperative launch per step)",
-                      "c_fp_s": "central_kernel<identity> (one fused launch per step)",
-                      "d_fp_s": "decent_kernel<identity> (one fused launch per step)",
-                      "d_lp_s": "decent_kernel<uint8> (one fused launch per step)",
-                      "codec": "encode_ring_kernel (min/max, grid barrier, quantize) + decode_ring_kernel",
-                      "onebit": "onebit_encode_kernel (fp64 |x| sum + sign bits) + onebit_decode_kernel"}[prim]
+    roof["kernel"] = kernel_label(prim, n, g)
+    if prim == "c_lp_s" and g > 1:
+        # the phase-serialized bound -- encode (HBM: x read +
+        # codes written, 5N), scatter and gather (NVLink: N(g-1)/g each)
+        ph = [5 * n / (hbm_peak * 1e9), n * (g - 1) / g / (NVL_PEER_GBS * 1e9), n * (g - 1) / g / (NVL_PEER_GBS * 1e9)]
+        phn = ph[:1] + [t * NVL_PEER_GBS / NVL_NOMINAL_GBS for t in ph[1:]]
+        roof["phase_serialized"] = {"phases_us": [round(t * 1e6, 1) for t in ph], "t_us": round(sum(ph) * 1e6, 1),
+                                    "frac": round(sum(ph) / t_s, 4),
+                                    "t_us_nominal_900": round(sum(phn) * 1e6, 1),
+                                    "frac_nominal_900": round(sum(phn) / t_s, 4)}
 
     per_gpu = 4 * n / t_s / 1e9
     label = PRIMS[prim][2]
