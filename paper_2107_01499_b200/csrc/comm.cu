@@ -91,6 +91,8 @@ struct b2_comm {
   unsigned long long launches = 0;
   unsigned long long* trace = nullptr;  // device [max grid * kTraceSlots], when enabled
   int trace_grid = 0;
+  cudaStream_t aux = nullptr;      // non-blocking: poison reads while kernels run
+  unsigned long long* poison_h = nullptr;  // pinned landing word of those reads
   std::mutex mu;
 };
 
@@ -416,6 +418,8 @@ int b2_comm_destroy(b2_comm_t c) {
   cudaDeviceSynchronize();
   for (auto& kv : c->wins) free_window(c, kv.second);
   if (c->trace) cudaFree(c->trace);
+  if (c->aux) cudaStreamDestroy(c->aux);
+  if (c->poison_h) cudaFreeHost(c->poison_h);
   if (c->status_h) cudaFreeHost(c->status_h);
   delete c;
   return B2_OK;
@@ -455,9 +459,35 @@ int b2_comm_set_sm_budget(b2_comm_t c, int sms) {
   return B2_OK;
 }
 
+// A peer that timed out writes the poison word of every rank's window
+// (b2_device.cuh latch); a rank whose own calls never waited for the late
+// rank (a D_* rank outside its neighbourhood) has not run a kernel that saw
+// it, so the windows' poison words are read here too (a copy on a
+// non-blocking stream: it does not wait for kernels still spinning).
 int b2_comm_poisoned(b2_comm_t c) {
   if (!c) return 0;
+  std::lock_guard<std::mutex> lk(c->mu);
   if (__atomic_load_n(c->status_h, __ATOMIC_ACQUIRE) & kStatusTimeout) c->poisoned = true;
+  if (!c->poisoned && !c->wins.empty()) {
+    DeviceGuard dg(c->device);
+    if (!c->aux && cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess) c->aux = nullptr;
+    if (!c->poison_h && cudaHostAlloc(reinterpret_cast<void**>(&c->poison_h), sizeof(unsigned long long),
+                                      cudaHostAllocDefault) != cudaSuccess)
+      c->poison_h = nullptr;
+    if (c->aux && c->poison_h) {
+      for (auto& kv : c->wins) {
+        *c->poison_h = 0;
+        if (cudaMemcpyAsync(c->poison_h, kv.second->local + offsetof(WinHdr, poison), sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, c->aux) != cudaSuccess ||
+            cudaStreamSynchronize(c->aux) != cudaSuccess)
+          break;
+        if (*c->poison_h) {
+          c->poisoned = true;
+          break;
+        }
+      }
+    }
+  }
   return c->poisoned ? 1 : 0;
 }
 
