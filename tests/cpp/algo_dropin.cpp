@@ -43,7 +43,16 @@ float synth(std::uint64_t seed, std::uint64_t i) {
   return static_cast<float>(static_cast<std::int64_t>(z >> 40) - (1 << 23)) / static_cast<float>(1 << 23);
 }
 
-const std::vector<std::size_t> kLayers = {1000, 37, 70001, 5, 250000, 4096, 33333};
+const std::vector<std::size_t> kLayers0 = {1000, 37, 70001, 5, 250000, 4096, 33333};
+// B2_DROPIN_SCALE=<k>: every layer k times larger (the ring kernels' sizes)
+std::vector<std::size_t> layers() {
+  const char* e = std::getenv("B2_DROPIN_SCALE");
+  const std::size_t k = e ? std::strtoull(e, nullptr, 10) : 1;
+  std::vector<std::size_t> v = kLayers0;
+  for (auto& n : v) n *= (k > 0 ? k : 1);
+  return v;
+}
+const std::vector<std::size_t> kLayers = layers();
 
 void worker(Endpoint& ep, AlgorithmName algo, int steps, const std::string& out) {
   const int r = ep.rank();
@@ -125,11 +134,20 @@ int main(int argc, char** argv) {
       }
     });
 #else
+  // B2_DEVICES=<d>: rank r on GPU r % d (several ranks per GPU, each with its
+  // own stream; with B2_SM_BUDGET=<148/(ranks per GPU)> their cooperative
+  // kernels are co-resident) -- how tests/cpp/g8_emulation.py runs 8 ranks
+  // on a 4-GPU box.  B2_TIMEOUT_MS bounds every rendezvous.
+  const int ndev = std::getenv("B2_DEVICES") ? std::atoi(std::getenv("B2_DEVICES")) : world;
+  const int budget = std::getenv("B2_SM_BUDGET") ? std::atoi(std::getenv("B2_SM_BUDGET")) : 0;
+  const int tmo = std::getenv("B2_TIMEOUT_MS") ? std::atoi(std::getenv("B2_TIMEOUT_MS")) : 0;
   NvlThreadGroup tg(world);
   for (int r = 0; r < world; ++r)
     th.emplace_back([&, r] {
       try {
-        NvlEndpoint ep(r, world, r, tg.allgather(r));
+        NvlEndpoint ep(r, world, r % (ndev > 0 ? ndev : world), tg.allgather(r));
+        if (budget > 0) b2_comm_set_sm_budget(ep.handle(), budget);
+        if (tmo > 0) b2_comm_set_timeout_ms(ep.handle(), static_cast<std::uint64_t>(tmo));
         worker(ep, algo, steps, out);
         // a peer may still be pulling my last payload: nobody frees its
         // windows before everybody is done (the allgather is a barrier)

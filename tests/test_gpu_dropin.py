@@ -70,3 +70,25 @@ def test_reference_algorithms_on_b200(algo, tmp_path):
             assert float(np.abs(got[k].astype(np.float64) - want[k]).max()) <= tol, k
         else:
             assert np.array_equal(got[k].view(np.uint32), want[k].view(np.uint32)), (algo, k)
+
+
+@pytest.mark.gpu
+@pytest.mark.multigpu
+def test_reference_algorithms_two_ranks_per_gpu():
+    """Twice as many workers as GPUs (up to 8; two ranks per GPU, thread per
+    rank, half the SMs each): on a 4-GPU box this is the g = 8 code path of
+    every primitive -- small and TMA-ring kernels, the onebit g > 4 fold --
+    bit-exact against the reference's SimCluster (tests/cpp/g8_emulation.py)."""
+    _binaries()
+    n = _ngpu()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    g = min(2 * n, 8)
+    import json
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(HERE, "cpp", "g8_emulation.py"), str(g), str(g // 2)],
+                       capture_output=True, text=True, timeout=1800)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert lines, r.stdout[-2000:] + r.stderr[-2000:]
+    res = json.loads(lines[-1])
+    assert r.returncode == 0 and res["ok"], json.dumps(res)[:3000]
