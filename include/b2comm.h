@@ -169,7 +169,10 @@ int b2_comm_set_timeout_ms(b2_comm_t comm, uint64_t ms);
  * 0 = all SMs (default).  Every rank must set the same budget (checked when a
  * window is first exchanged). */
 int b2_comm_set_sm_budget(b2_comm_t comm, int sms);
-/* 1 when the communicator is poisoned by a rendezvous timeout (see above). */
+/* 1 when the communicator is poisoned by a rendezvous timeout (see above):
+ * its own latched status, or a poison word a peer wrote into one of its
+ * windows (read with a small copy on a private non-blocking stream, so it
+ * does not wait for kernels still running). */
 int b2_comm_poisoned(b2_comm_t comm);
 /* Collective (every rank, same bucket id): free every window of `bucket`
  * (all primitive families and sizes).  Drains this GPU, then synchronises the
