@@ -1,4 +1,4 @@
-"""Host-side multi-process logic on CPU (world_size 2 and 4, gloo): the
+"""Host-side multi-process logic on CPU (world_size 2, 4 and 8, gloo): the
 window-handle bootstrap that b2_comm_create's allgather hook runs through
 (TorchBootstrap), the in-process ThreadBootstrap, and the callback marshalling
 of B200Endpoint._allgather."""
@@ -41,7 +41,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_torch_bootstrap_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
